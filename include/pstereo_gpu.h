@@ -1,0 +1,207 @@
+/*
+ * pstereo_gpu.h -- C ABI of the B200-native BDIS matching core.
+ *
+ * Drop-in boundary for the reference's matching core:
+ *   PipelineOutput run_pipeline(const GrayImage&, const GrayImage&,
+ *                               const PipelineConfig&, const CameraParams&)
+ *       (proj/include/pstereo/pipeline.hpp:20-22, src/pipeline.cpp:9-37)
+ *   MatchResult match_stereo(const GrayImage&, const GrayImage&,
+ *                            const PipelineConfig&)
+ *       (proj/include/pstereo/coarse_to_fine.hpp:102-103)
+ * The reference has no FFI; its callers are C++ (src/bench.cpp:24,
+ * src/runner.cpp:140). This header is what such a caller -- or a ctypes /
+ * cgo / JNI binding -- links against instead: plain pointers and sizes, no
+ * C++ or torch types. include/pstereo_gpu.hpp re-exposes the reference's own
+ * C++ signatures on top of it.
+ *
+ * Semantics follow the reference exactly (bit-identical disparity,
+ * probability, validity and depth), batched over
+ * independent pairs. There is no CPU fallback: every entry point that
+ * computes requires a CUDA device with compute capability 10.0 (sm_100a).
+ *
+ * Error convention (inc/runner.hpp:16-19, src/runner.cpp:107-124):
+ *   PSTEREO_ECONFIG     <- ConfigError (validate, src/coarse_to_fine.cpp:18-49)
+ *   PSTEREO_EDEGENERATE <- DegenerateInputError (build_pyramid,
+ *                          src/pyramid.cpp:46-58,84-89; make_patch_grid :56-61)
+ *   PSTEREO_EINTERNAL   <- anything else (CUDA errors, bad arguments)
+ * pstereo_gpu_last_error() returns the message of the last failure.
+ */
+#ifndef PSTEREO_GPU_H
+#define PSTEREO_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PSTEREO_OK 0
+#define PSTEREO_EINTERNAL 1
+#define PSTEREO_ECONFIG 2
+#define PSTEREO_EDEGENERATE 4
+
+#define PSTEREO_MAX_OFFSETS 16
+#define PSTEREO_MAX_PATCH 32
+#define PSTEREO_MAX_LEVELS 17
+
+#define PSTEREO_F32 0
+#define PSTEREO_F64 1
+
+/* PipelineConfig (inc/config.hpp:12-33), window offsets inline. */
+typedef struct pstereo_params {
+  int coarsest_exp;          /* default 5 */
+  int finest_exp;            /* default 1 */
+  int patch_size;            /* default 10 (GPU path: 2..PSTEREO_MAX_PATCH) */
+  double overlap;            /* default 0.55 */
+  int min_iterations;        /* default 12 */
+  int max_iterations;        /* default 12 */
+  double early_stop_good;    /* default 0.05 */
+  double early_stop_bad;     /* default 0.95 */
+  double early_stop_improve; /* default 0.10 */
+  int n_window_offsets;      /* default 2 */
+  double window_offsets[PSTEREO_MAX_OFFSETS]; /* default {0.5, 1.0} */
+  double sigma_s;            /* default 4.0 */
+  double pixel_threshold;    /* default 0.15 */
+  double gamma;              /* default 0.75 */
+  double valid_patch_ratio;  /* default 0.75 */
+  int estimate_variance;     /* default 0 */
+  int threads;               /* default 1; validated, scheduling only */
+} pstereo_params;
+
+/* MatchStats::Level (inc/coarse_to_fine.hpp:80-89). */
+typedef struct pstereo_level_stats {
+  int exp;
+  int grid_patches;
+  int extracted;
+  int converged;
+  int accepted;
+} pstereo_level_stats;
+
+/* PatchEstimate (inc/coarse_to_fine.hpp:39-47) of the finest level. */
+typedef struct pstereo_patch_estimate {
+  double cx, cy, u, prob, posterior, sigma_k;
+} pstereo_patch_estimate;
+
+/*
+ * Output planes, all [n_pairs][height][width] row-major top-to-bottom.
+ * Value planes are float (PSTEREO_F32) or double (PSTEREO_F64); values at
+ * invalid pixels equal the reference's (the unfiltered match value, or 0).
+ * Any pointer may be NULL to skip that plane. When on_device is 0 the
+ * pointers are host memory and the call blocks until they are written.
+ *   disparity / disparity_valid   <- PipelineOutput::disparity (filtered)
+ *   probability                   <- PipelineOutput::probability (its valid
+ *                                    mask equals disparity_valid)
+ *   depth / depth_valid           <- DepthResult::depth
+ *   depth_sigma / sigma_valid     <- DepthResult::sigma (estimate_variance)
+ *   match_disparity/match_valid   <- MatchResult::disparity (pre-filter)
+ *   var_disp                      <- MatchResult::var_disp (estimate_variance;
+ *                                    valid mask equals match_valid)
+ *   stats       (host) [n_pairs][n_levels], coarsest level first
+ *   finest      (host) [n_pairs][finest_cap] accepted finest-level patches
+ *               in patch-index order, count per pair in finest_count[n_pairs]
+ */
+typedef struct pstereo_outputs {
+  int dtype;
+  int on_device;
+  void* disparity;
+  uint8_t* disparity_valid;
+  void* probability;
+  void* depth;
+  uint8_t* depth_valid;
+  void* depth_sigma;
+  uint8_t* sigma_valid;
+  void* match_disparity;
+  uint8_t* match_valid;
+  void* var_disp;
+  pstereo_level_stats* stats;
+  pstereo_patch_estimate* finest;
+  int* finest_count;
+  int finest_cap;
+} pstereo_outputs;
+
+typedef struct pstereo_ctx pstereo_ctx;
+
+/* Published defaults, inc/config.hpp:12-33. */
+void pstereo_default_params(pstereo_params* p);
+
+/* validate(), src/coarse_to_fine.cpp:18-49 (plus the GPU path's patch-size
+ * cap). Returns PSTEREO_OK or PSTEREO_ECONFIG with the message in msg. */
+int pstereo_validate(const pstereo_params* p, char* msg, size_t msg_cap);
+
+/* Number of pyramid levels and their dimensions for a width x height pair. */
+int pstereo_level_dims(const pstereo_params* p, int width, int height,
+                       int* n_levels, int* widths, int* heights, int* exps);
+
+/*
+ * Creates a context on `device` sized for up to max_pairs pairs of at most
+ * max_width x max_height (any channel count). Validates params
+ * (PSTEREO_ECONFIG) and checks the device is sm_100 (PSTEREO_EINTERNAL).
+ * One context per device and host thread; a context is not re-entrant.
+ */
+int pstereo_gpu_create(int device, const pstereo_params* p, int max_width,
+                       int max_height, int max_pairs, pstereo_ctx** out);
+void pstereo_gpu_destroy(pstereo_ctx* ctx);
+const char* pstereo_gpu_last_error(const pstereo_ctx* ctx);
+
+/*
+ * Batched run_pipeline on uint8 rasters (Raster, inc/image.hpp:12-17;
+ * channels 1 = gray, 3 = RGB, 4 = RGBA with alpha==0 invalid), converted
+ * with the reference's to_grayscale (src/image.cpp:16-43) on the device.
+ * left/right: [n_pairs][height][width][channels] contiguous, host or device
+ * memory per inputs_on_device. focal_px * baseline is the CameraParams
+ * product (inc/depth_variance.hpp:20-23). `stream` is a cudaStream_t (NULL =
+ * the context's own stream). With device inputs and device outputs and no
+ * host stats/finest requested, the call only enqueues work on `stream`.
+ */
+int pstereo_gpu_match_u8(pstereo_ctx* ctx, int n_pairs, int width, int height,
+                         int channels, const uint8_t* left,
+                         const uint8_t* right, int inputs_on_device,
+                         double focal_px, double baseline,
+                         const pstereo_outputs* out, void* stream);
+
+/*
+ * Batched run_pipeline on GrayImage planes (inc/image.hpp:21-26): fp32
+ * [n_pairs][height][width] plus optional u8 validity (NULL = all valid).
+ */
+int pstereo_gpu_match_f32(pstereo_ctx* ctx, int n_pairs, int width, int height,
+                          const float* left, const uint8_t* left_valid,
+                          const float* right, const uint8_t* right_valid,
+                          int inputs_on_device, double focal_px,
+                          double baseline, const pstereo_outputs* out,
+                          void* stream);
+
+/* Kernel launches issued by the last match call (telemetry for bench.py). */
+int pstereo_gpu_last_launch_count(const pstereo_ctx* ctx);
+
+/* Device time (ms) of each stage of the last match call when profiling is
+ * enabled with pstereo_gpu_set_profiling(ctx, 1); names via
+ * pstereo_gpu_stage_name. Returns the number of stages written. */
+int pstereo_gpu_set_profiling(pstereo_ctx* ctx, int enable);
+int pstereo_gpu_stage_times(const pstereo_ctx* ctx, float* ms, int cap);
+const char* pstereo_gpu_stage_name(int stage);
+
+/* ---- deterministic synthetic pairs (BASELINE.json configs) ---- */
+typedef struct pstereo_synth_spec {
+  int width, height, channels;
+  uint64_t seed;
+  int octaves;
+  double base_wavelength;
+  double d_min, d_range, blur_sigma;
+  double noise_sigma;
+  int stress;
+} pstereo_synth_spec;
+
+/* Defaults for BASELINE.json configs[config] (0..3). */
+void pstereo_synth_default(pstereo_synth_spec* s, int config);
+int pstereo_synth_pair(const pstereo_synth_spec* s, uint64_t seed,
+                       uint8_t* left, uint8_t* right, float* disparity);
+int pstereo_synth_batch(const pstereo_synth_spec* s, int n_pairs,
+                        uint64_t seed0, uint8_t* left, uint8_t* right,
+                        int threads);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PSTEREO_GPU_H */

@@ -1,0 +1,474 @@
+"""B200-native BDIS matching core -- Python host mirror of the reference API.
+
+The product is libpstereo_gpu.so (hand-written sm_100a kernels behind the C ABI
+in include/pstereo_gpu.h). This module binds that ABI with ctypes and mirrors
+the reference's interface for the hot path (proj/include/pstereo/*.hpp):
+
+  PipelineConfig             inc/config.hpp:12-33      -> PipelineConfig
+  validate                   src/coarse_to_fine.cpp:18-49 -> validate
+  ConfigError / DegenerateInputError  inc/errors.hpp:9-31
+  CameraParams               inc/depth_variance.hpp:20-23
+  match_stereo               inc/coarse_to_fine.hpp:102-103 -> match_stereo
+  run_pipeline               inc/pipeline.hpp:20-22    -> run_pipeline
+  (batched)                                            -> Matcher.run_batch
+
+There is no CPU fallback: loading fails loudly when the library is missing,
+and every compute call needs an sm_100 device.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from pathlib import Path
+
+import numpy as np
+
+PKG = Path(__file__).resolve().parent
+LIB_PATH = PKG / "libpstereo_gpu.so"
+
+PSTEREO_OK, PSTEREO_EINTERNAL, PSTEREO_ECONFIG, PSTEREO_EDEGENERATE = 0, 1, 2, 4
+MAX_OFF = 16
+F32, F64 = 0, 1
+
+u8p = C.POINTER(C.c_uint8)
+f32p = C.POINTER(C.c_float)
+i32p = C.POINTER(C.c_int)
+
+
+class ConfigError(ValueError):
+    """Bad parameter values (inc/errors.hpp:9-11)."""
+
+
+class DegenerateInputError(ValueError):
+    """Structurally unusable input, e.g. smaller than a patch (inc/errors.hpp:28-30)."""
+
+
+class GpuError(RuntimeError):
+    """CUDA / internal failure (exit code 1 in src/runner.cpp:107-124)."""
+
+
+class _Params(C.Structure):
+    _fields_ = [
+        ("coarsest_exp", C.c_int), ("finest_exp", C.c_int), ("patch_size", C.c_int),
+        ("overlap", C.c_double), ("min_iterations", C.c_int), ("max_iterations", C.c_int),
+        ("early_stop_good", C.c_double), ("early_stop_bad", C.c_double),
+        ("early_stop_improve", C.c_double), ("n_window_offsets", C.c_int),
+        ("window_offsets", C.c_double * MAX_OFF), ("sigma_s", C.c_double),
+        ("pixel_threshold", C.c_double), ("gamma", C.c_double),
+        ("valid_patch_ratio", C.c_double), ("estimate_variance", C.c_int), ("threads", C.c_int),
+    ]
+
+
+class LevelStats(C.Structure):
+    """MatchStats::Level (inc/coarse_to_fine.hpp:80-89)."""
+    _fields_ = [("exp", C.c_int), ("grid_patches", C.c_int), ("extracted", C.c_int),
+                ("converged", C.c_int), ("accepted", C.c_int)]
+
+    def as_tuple(self):
+        return (self.exp, self.grid_patches, self.extracted, self.converged, self.accepted)
+
+
+class PatchEstimate(C.Structure):
+    _fields_ = [("cx", C.c_double), ("cy", C.c_double), ("u", C.c_double),
+                ("prob", C.c_double), ("posterior", C.c_double), ("sigma_k", C.c_double)]
+
+
+class _Outputs(C.Structure):
+    _fields_ = [
+        ("dtype", C.c_int), ("on_device", C.c_int), ("disparity", C.c_void_p),
+        ("disparity_valid", C.c_void_p), ("probability", C.c_void_p), ("depth", C.c_void_p),
+        ("depth_valid", C.c_void_p), ("depth_sigma", C.c_void_p), ("sigma_valid", C.c_void_p),
+        ("match_disparity", C.c_void_p), ("match_valid", C.c_void_p), ("var_disp", C.c_void_p),
+        ("stats", C.POINTER(LevelStats)), ("finest", C.POINTER(PatchEstimate)),
+        ("finest_count", i32p), ("finest_cap", C.c_int),
+    ]
+
+
+class SynthSpec(C.Structure):
+    _fields_ = [("width", C.c_int), ("height", C.c_int), ("channels", C.c_int),
+                ("seed", C.c_uint64), ("octaves", C.c_int), ("base_wavelength", C.c_double),
+                ("d_min", C.c_double), ("d_range", C.c_double), ("blur_sigma", C.c_double),
+                ("noise_sigma", C.c_double), ("stress", C.c_int)]
+
+
+_LIB = None
+
+
+def lib() -> C.CDLL:
+    """The product library. Raises if it was not built -- no fallback."""
+    global _LIB
+    if _LIB is None:
+        if not LIB_PATH.exists():
+            raise ImportError(f"{LIB_PATH} missing: run python -m paper_2205_03133_b200.build")
+        L = C.CDLL(str(LIB_PATH))
+        L.pstereo_gpu_last_error.restype = C.c_char_p
+        L.pstereo_gpu_last_error.argtypes = [C.c_void_p]
+        L.pstereo_gpu_stage_name.restype = C.c_char_p
+        L.pstereo_gpu_create.argtypes = [C.c_int, C.POINTER(_Params), C.c_int, C.c_int, C.c_int,
+                                         C.POINTER(C.c_void_p)]
+        L.pstereo_gpu_destroy.argtypes = [C.c_void_p]
+        L.pstereo_gpu_last_launch_count.argtypes = [C.c_void_p]
+        L.pstereo_gpu_set_profiling.argtypes = [C.c_void_p, C.c_int]
+        L.pstereo_gpu_stage_times.argtypes = [C.c_void_p, f32p, C.c_int]
+        L.pstereo_gpu_match_u8.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
+                                           C.c_void_p, C.c_void_p, C.c_int, C.c_double,
+                                           C.c_double, C.POINTER(_Outputs), C.c_void_p]
+        L.pstereo_gpu_match_f32.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p,
+                                            C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
+                                            C.c_double, C.c_double, C.POINTER(_Outputs),
+                                            C.c_void_p]
+        L.pstereo_validate.argtypes = [C.POINTER(_Params), C.c_char_p, C.c_size_t]
+        L.pstereo_level_dims.argtypes = [C.POINTER(_Params), C.c_int, C.c_int, i32p, i32p,
+                                         i32p, i32p]
+        L.pstereo_synth_default.argtypes = [C.POINTER(SynthSpec), C.c_int]
+        L.pstereo_synth_pair.argtypes = [C.POINTER(SynthSpec), C.c_uint64, u8p, u8p, f32p]
+        L.pstereo_synth_batch.argtypes = [C.POINTER(SynthSpec), C.c_int, C.c_uint64, u8p, u8p,
+                                          C.c_int]
+        _LIB = L
+    return _LIB
+
+
+# Exported symbols of include/pstereo_gpu.h (checked by tests/test_abi.py).
+ABI_SYMBOLS = [
+    "pstereo_default_params", "pstereo_validate", "pstereo_level_dims", "pstereo_gpu_create",
+    "pstereo_gpu_destroy", "pstereo_gpu_last_error", "pstereo_gpu_match_u8",
+    "pstereo_gpu_match_f32", "pstereo_gpu_last_launch_count", "pstereo_gpu_set_profiling",
+    "pstereo_gpu_stage_times", "pstereo_gpu_stage_name", "pstereo_synth_default",
+    "pstereo_synth_pair", "pstereo_synth_batch",
+]
+
+
+@dataclass
+class PipelineConfig:
+    """inc/config.hpp:12-33, published defaults."""
+    coarsest_exp: int = 5
+    finest_exp: int = 1
+    patch_size: int = 10
+    overlap: float = 0.55
+    min_iterations: int = 12
+    max_iterations: int = 12
+    early_stop_good: float = 0.05
+    early_stop_bad: float = 0.95
+    early_stop_improve: float = 0.10
+    window_offsets: list = field(default_factory=lambda: [0.5, 1.0])
+    sigma_s: float = 4.0
+    pixel_threshold: float = 0.15
+    gamma: float = 0.75
+    valid_patch_ratio: float = 0.75
+    estimate_variance: bool = False
+    threads: int = 1
+
+    def to_c(self) -> _Params:
+        p = _Params()
+        for k in ("coarsest_exp", "finest_exp", "patch_size", "min_iterations",
+                  "max_iterations", "threads"):
+            setattr(p, k, int(getattr(self, k)))
+        for k in ("overlap", "early_stop_good", "early_stop_bad", "early_stop_improve",
+                  "sigma_s", "pixel_threshold", "gamma", "valid_patch_ratio"):
+            setattr(p, k, float(getattr(self, k)))
+        p.estimate_variance = int(bool(self.estimate_variance))
+        p.n_window_offsets = len(self.window_offsets)
+        for i, v in enumerate(list(self.window_offsets)[:MAX_OFF]):
+            p.window_offsets[i] = float(v)
+        if len(self.window_offsets) > MAX_OFF:
+            p.n_window_offsets = MAX_OFF + 1  # rejected by validate
+        return p
+
+    @staticmethod
+    def baseline(config: int) -> "PipelineConfig":
+        """BASELINE.json configs -> PipelineConfig (SURVEY.md section 8a mapping)."""
+        if config in (0, 2):
+            return PipelineConfig(coarsest_exp=3, finest_exp=1, patch_size=8, overlap=0.5)
+        if config == 1:
+            return PipelineConfig(coarsest_exp=3, finest_exp=1, patch_size=8, overlap=0.5,
+                                  estimate_variance=True)
+        if config == 3:
+            return PipelineConfig(coarsest_exp=4, finest_exp=1, patch_size=12,
+                                  overlap=1.0 - 4.0 / 12.0, estimate_variance=True)
+        raise ValueError(f"no fixed PipelineConfig for config {config}")
+
+
+@dataclass
+class CameraParams:
+    """inc/depth_variance.hpp:20-23."""
+    focal_px: float = 0.0
+    baseline: float = 0.0
+
+
+def _raise(code: int, msg: str):
+    if code == PSTEREO_ECONFIG:
+        raise ConfigError(msg)
+    if code == PSTEREO_EDEGENERATE:
+        raise DegenerateInputError(msg)
+    raise GpuError(msg or f"pstereo error {code}")
+
+
+def validate(cfg: PipelineConfig) -> None:
+    """Raises ConfigError like validate() (src/coarse_to_fine.cpp:18-49)."""
+    p = cfg.to_c()
+    buf = C.create_string_buffer(256)
+    rc = lib().pstereo_validate(C.byref(p), buf, 256)
+    if rc:
+        _raise(rc, buf.value.decode())
+
+
+def level_dims(cfg: PipelineConfig, width: int, height: int):
+    p = cfg.to_c()
+    n = C.c_int()
+    ws, hs, es = (np.zeros(32, np.int32) for _ in range(3))
+    rc = lib().pstereo_level_dims(C.byref(p), width, height, C.byref(n),
+                                  ws.ctypes.data_as(i32p), hs.ctypes.data_as(i32p),
+                                  es.ctypes.data_as(i32p))
+    if rc:
+        _raise(rc, "level_dims")
+    return [(int(es[i]), int(ws[i]), int(hs[i])) for i in range(n.value)]
+
+
+def synth_spec(config: int = 0, **overrides) -> SynthSpec:
+    s = SynthSpec()
+    lib().pstereo_synth_default(C.byref(s), config)
+    for k, v in overrides.items():
+        setattr(s, k, v)
+    return s
+
+
+def synth_pair(config: int = 0, seed: int | None = None, with_disparity=False, **overrides):
+    """One deterministic BASELINE.json pair: (left, right[, disparity])."""
+    s = synth_spec(config, **overrides)
+    shape = (s.height, s.width) if s.channels == 1 else (s.height, s.width, s.channels)
+    left = np.zeros(shape, np.uint8)
+    right = np.zeros(shape, np.uint8)
+    disp = np.zeros((s.height, s.width), np.float32)
+    seed = s.seed if seed is None else seed
+    rc = lib().pstereo_synth_pair(C.byref(s), seed, left.ctypes.data_as(u8p),
+                                  right.ctypes.data_as(u8p), disp.ctypes.data_as(f32p))
+    if rc:
+        _raise(rc, "synth_pair")
+    return (left, right, disp) if with_disparity else (left, right)
+
+
+def synth_batch(config: int, n: int, seed0: int = 0, threads: int = 8, **overrides):
+    s = synth_spec(config, **overrides)
+    shape = (n, s.height, s.width) if s.channels == 1 else (n, s.height, s.width, s.channels)
+    left = np.zeros(shape, np.uint8)
+    right = np.zeros(shape, np.uint8)
+    rc = lib().pstereo_synth_batch(C.byref(s), n, seed0, left.ctypes.data_as(u8p),
+                                   right.ctypes.data_as(u8p), threads)
+    if rc:
+        _raise(rc, "synth_batch")
+    return left, right
+
+
+class Matcher:
+    """A device context (pstereo_gpu_create) for batches up to max_pairs of
+    at most max_width x max_height."""
+
+    def __init__(self, cfg: PipelineConfig, max_width: int, max_height: int, max_pairs: int = 1,
+                 device: int = 0):
+        self.cfg = cfg
+        validate(cfg)
+        self._p = cfg.to_c()
+        h = C.c_void_p()
+        rc = lib().pstereo_gpu_create(device, C.byref(self._p), max_width, max_height,
+                                      max_pairs, C.byref(h))
+        if rc:
+            _raise(rc, f"pstereo_gpu_create failed (device {device}: needs an sm_100 GPU)")
+        self._h = h
+        self.n_levels = cfg.coarsest_exp - cfg.finest_exp + 1
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().pstereo_gpu_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    @property
+    def handle(self):
+        return self._h
+
+    def last_error(self) -> str:
+        return lib().pstereo_gpu_last_error(self._h).decode()
+
+    def launch_count(self) -> int:
+        return lib().pstereo_gpu_last_launch_count(self._h)
+
+    def set_profiling(self, on: bool):
+        lib().pstereo_gpu_set_profiling(self._h, int(on))
+
+    def stage_times(self) -> dict:
+        ms = np.zeros(8, np.float32)
+        n = lib().pstereo_gpu_stage_times(self._h, ms.ctypes.data_as(f32p), 8)
+        return {lib().pstereo_gpu_stage_name(i).decode(): float(ms[i]) for i in range(n)}
+
+    # ---- host-memory batched API (numpy in, numpy out)
+    def run_batch(self, left, right, focal=1.0, baseline=1.0, dtype=F32, left_valid=None,
+                  right_valid=None, want=("disparity", "disparity_valid"), stats=False,
+                  finest_cap=0):
+        """Batched run_pipeline. left/right: uint8 [n,h,w] / [n,h,w,c], or float32
+        [n,h,w] GrayImage planes (+ optional u8 validity)."""
+        left = np.ascontiguousarray(left)
+        right = np.ascontiguousarray(right)
+        is_u8 = left.dtype == np.uint8
+        if is_u8:
+            if left.ndim == 3:
+                n, h, w = left.shape
+                ch = 1
+            else:
+                n, h, w, ch = left.shape
+        else:
+            left = np.ascontiguousarray(left, np.float32)
+            right = np.ascontiguousarray(right, np.float32)
+            n, h, w = left.shape
+        vt = np.float64 if dtype == F64 else np.float32
+        res = {}
+        o = _Outputs()
+        o.dtype = dtype
+        o.on_device = 0
+        planes = {"disparity": vt, "disparity_valid": np.uint8, "probability": vt, "depth": vt,
+                  "depth_valid": np.uint8, "depth_sigma": vt, "sigma_valid": np.uint8,
+                  "match_disparity": vt, "match_valid": np.uint8, "var_disp": vt}
+        for k in want:
+            a = np.zeros((n, h, w), planes[k])
+            res[k] = a
+            setattr(o, k, a.ctypes.data)
+        st = None
+        if stats:
+            st = (LevelStats * (n * self.n_levels))()
+            o.stats = st
+        fin = cnt = None
+        if finest_cap:
+            fin = (PatchEstimate * (n * finest_cap))()
+            cnt = np.zeros(n, np.int32)
+            o.finest = fin
+            o.finest_count = cnt.ctypes.data_as(i32p)
+            o.finest_cap = finest_cap
+        if is_u8:
+            rc = lib().pstereo_gpu_match_u8(self._h, n, w, h, ch, left.ctypes.data,
+                                            right.ctypes.data, 0, focal, baseline, C.byref(o),
+                                            None)
+        else:
+            lv = None if left_valid is None else np.ascontiguousarray(left_valid, np.uint8)
+            rv = None if right_valid is None else np.ascontiguousarray(right_valid, np.uint8)
+            rc = lib().pstereo_gpu_match_f32(self._h, n, w, h, left.ctypes.data,
+                                             None if lv is None else lv.ctypes.data,
+                                             right.ctypes.data,
+                                             None if rv is None else rv.ctypes.data, 0, focal,
+                                             baseline, C.byref(o), None)
+        if rc:
+            _raise(rc, self.last_error())
+        if stats:
+            res["stats"] = np.array([s.as_tuple() for s in st], np.int64).reshape(
+                n, self.n_levels, 5)
+        if finest_cap:
+            res["finest"] = []
+            for p in range(n):
+                rows = [(fin[p * finest_cap + k].cx, fin[p * finest_cap + k].cy,
+                         fin[p * finest_cap + k].u, fin[p * finest_cap + k].prob,
+                         fin[p * finest_cap + k].posterior, fin[p * finest_cap + k].sigma_k)
+                        for k in range(min(int(cnt[p]), finest_cap))]
+                res["finest"].append(np.array(rows, np.float64).reshape(-1, 6))
+            res["finest_count"] = cnt
+        return res
+
+    # ---- device-pointer batched API (the zero-copy path used by bench.py)
+    def run_device_u8(self, n, width, height, channels, left_ptr, right_ptr, outputs: dict,
+                      dtype=F32, focal=1.0, baseline=1.0, stream=None):
+        o = _Outputs()
+        o.dtype = dtype
+        o.on_device = 1
+        for k, ptr in outputs.items():
+            setattr(o, k, ptr)
+        rc = lib().pstereo_gpu_match_u8(self._h, n, width, height, channels, left_ptr, right_ptr,
+                                        1, focal, baseline, C.byref(o), stream)
+        if rc:
+            _raise(rc, self.last_error())
+
+    def run_host_u8(self, n, width, height, channels, left_ptr, right_ptr, outputs: dict,
+                    dtype=F32, focal=1.0, baseline=1.0, stream=None):
+        """Host (ideally pinned) buffers in and out; H2D/D2H inside the call."""
+        o = _Outputs()
+        o.dtype = dtype
+        o.on_device = 0
+        for k, ptr in outputs.items():
+            setattr(o, k, ptr)
+        rc = lib().pstereo_gpu_match_u8(self._h, n, width, height, channels, left_ptr, right_ptr,
+                                        0, focal, baseline, C.byref(o), stream)
+        if rc:
+            _raise(rc, self.last_error())
+
+
+_MATCHERS: dict = {}
+
+
+def _matcher_for(cfg: PipelineConfig, w: int, h: int) -> Matcher:
+    key = (repr(cfg), w, h)
+    m = _MATCHERS.get(key)
+    if m is None:
+        m = _MATCHERS[key] = Matcher(cfg, w, h, 1)
+    return m
+
+
+def _as_gray(img):
+    """GrayImage-like input: (data fp32 [h,w], valid u8 or None)."""
+    if isinstance(img, tuple):
+        return np.ascontiguousarray(img[0], np.float32), img[1]
+    return np.ascontiguousarray(img, np.float32), None
+
+
+def run_pipeline(left, right, cfg: PipelineConfig, cam: CameraParams, dtype=F64) -> dict:
+    """run_pipeline (inc/pipeline.hpp:20-22) on one GrayImage pair: left/right are
+    float32 [h,w] planes or (plane, valid) tuples. Returns the PipelineOutput
+    fields as numpy arrays plus per-level MatchStats."""
+    validate(cfg)
+    (l, lv), (r, rv) = _as_gray(left), _as_gray(right)
+    if l.shape != r.shape:
+        raise DegenerateInputError(f"build_pipeline: left is {l.shape} but right is {r.shape}")
+    h, w = l.shape
+    m = _matcher_for(cfg, max(w, 1), max(h, 1))
+    want = ["disparity", "disparity_valid", "probability", "depth", "depth_valid"]
+    if cfg.estimate_variance:
+        want += ["depth_sigma", "sigma_valid"]
+    out = m.run_batch(l[None], r[None], focal=cam.focal_px, baseline=cam.baseline, dtype=dtype,
+                      left_valid=None if lv is None else np.asarray(lv)[None],
+                      right_valid=None if rv is None else np.asarray(rv)[None], want=want,
+                      stats=True)
+    res = {k: v[0] for k, v in out.items() if k != "stats"}
+    res["probability_valid"] = res["disparity_valid"]
+    res["stats"] = out["stats"][0]
+    res["has_sigma"] = bool(cfg.estimate_variance)
+    return res
+
+
+def match_stereo(left, right, cfg: PipelineConfig, dtype=F64, finest_cap=1 << 16) -> dict:
+    """match_stereo (inc/coarse_to_fine.hpp:102-103): pre-filter full-resolution
+    disparity/probability(/var_disp), MatchStats and the finest-level patches."""
+    validate(cfg)
+    (l, lv), (r, rv) = _as_gray(left), _as_gray(right)
+    if l.shape != r.shape:
+        raise DegenerateInputError(f"match_stereo: left is {l.shape} but right is {r.shape}")
+    h, w = l.shape
+    m = _matcher_for(cfg, max(w, 1), max(h, 1))
+    want = ["match_disparity", "match_valid"]
+    if cfg.estimate_variance:
+        want.append("var_disp")
+    out = m.run_batch(l[None], r[None], dtype=dtype,
+                      left_valid=None if lv is None else np.asarray(lv)[None],
+                      right_valid=None if rv is None else np.asarray(rv)[None], want=want,
+                      stats=True, finest_cap=finest_cap)
+    res = {"disparity": out["match_disparity"][0], "disparity_valid": out["match_valid"][0],
+           "stats": out["stats"][0], "finest": out["finest"][0],
+           "has_variance": bool(cfg.estimate_variance)}
+    if cfg.estimate_variance:
+        res["var_disp"] = out["var_disp"][0]
+    return res

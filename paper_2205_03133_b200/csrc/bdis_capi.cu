@@ -1,0 +1,761 @@
+// bdis_capi.cu -- host runtime behind include/pstereo_gpu.h.
+//
+// Owns the device arena of a context (pyramid planes, per-level patch
+// records, finest-level fields, component labels), the level/grid
+// bookkeeping the reference does in match_stereo (src/coarse_to_fine.cpp:
+// 211-341), and the launch sequence of one batched run_pipeline call
+// (src/pipeline.cpp:9-37). No CPU compute path exists: every field is
+// produced by the kernels in bdis_kernels.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/pstereo_gpu.h"
+#include "bdis_kernels.h"
+
+using namespace bdis;
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// parameters
+
+void fast_exp_host(double x, double* out) {
+  // inc/fast_exp.hpp:16-28 evaluated on the host for the spatial mask.
+  if (x < -30.0) {
+    *out = 0.0;
+    return;
+  }
+  const double scale = 4503599627370496.0 / 0.6931471805599453;
+  const long long bias = (1023LL << 52) - (60801LL << 32);
+  const long long bits = (long long)(x * scale) + bias;
+  std::memcpy(out, &bits, sizeof(double));
+}
+
+int validate_params(const pstereo_params* c, std::string* msg) {
+  auto fail = [&](const char* m) {
+    *msg = std::string("config: ") + m;
+    return PSTEREO_ECONFIG;
+  };
+  // src/coarse_to_fine.cpp:18-49, same order and messages.
+  if (c->patch_size < 2) return fail("patch_size must be >= 2");
+  if (c->finest_exp < 0) return fail("finest_exp must be >= 0");
+  if (c->coarsest_exp < c->finest_exp) return fail("coarsest_exp must be >= finest_exp");
+  if (c->coarsest_exp > 16) return fail("coarsest_exp is unreasonably large");
+  if (!(c->overlap >= 0.0 && c->overlap < 1.0)) return fail("overlap must lie in [0, 1)");
+  if (c->min_iterations < 1) return fail("min_iterations must be >= 1");
+  if (c->max_iterations < c->min_iterations)
+    return fail("max_iterations must be >= min_iterations");
+  if (!(c->early_stop_good > 0.0)) return fail("early_stop_good must be > 0");
+  if (!(c->early_stop_bad > 0.0)) return fail("early_stop_bad must be > 0");
+  if (!(c->early_stop_improve >= 0.0)) return fail("early_stop_improve must be >= 0");
+  if (c->n_window_offsets <= 0) return fail("window_offsets must not be empty");
+  if (c->n_window_offsets > PSTEREO_MAX_OFFSETS) return fail("at most 16 window offsets");
+  for (int i = 0; i < c->n_window_offsets; ++i)
+    if (!(c->window_offsets[i] > 0.0)) return fail("window offsets must be positive magnitudes");
+  {
+    std::vector<double> s(c->window_offsets, c->window_offsets + c->n_window_offsets);
+    std::sort(s.begin(), s.end());
+    if (std::adjacent_find(s.begin(), s.end()) != s.end())
+      return fail("window offsets must be distinct");
+  }
+  if (!(c->sigma_s > 0.0)) return fail("sigma_s must be > 0");
+  if (!(c->pixel_threshold >= 0.0 && c->pixel_threshold <= 1.0))
+    return fail("pixel_threshold must lie in [0, 1]");
+  if (!(c->gamma >= 0.0)) return fail("gamma must be >= 0");
+  if (!(c->valid_patch_ratio > 0.0 && c->valid_patch_ratio <= 1.0))
+    return fail("valid_patch_ratio must lie in (0, 1]");
+  if (c->threads < 1) return fail("threads must be >= 1");
+  // GPU path limit (documented in DESIGN.md): patch_size <= 32.
+  if (c->patch_size > PSTEREO_MAX_PATCH) return fail("patch_size must be <= 32 on the GPU path");
+  return PSTEREO_OK;
+}
+
+struct LevelGeom {
+  int e, w, h;
+  Grid g;
+  double level_w;
+};
+
+// make_patch_grid (src/coarse_to_fine.cpp:51-88). Returns false when the
+// level is smaller than one patch.
+bool make_grid(int w, int h, int size, double overlap, Grid* g) {
+  const double c0 = (size - 1) * 0.5;
+  const double cmax_x = (w - 1) - c0;
+  const double cmax_y = (h - 1) - c0;
+  if (cmax_x < c0 || cmax_y < c0) return false;
+  const int stride = std::max(1, int(std::lrint(size * (1.0 - overlap))));
+  auto count = [&](double cmax) {
+    int n = 0;
+    for (int k = 0;; ++k) {
+      const double c = c0 + double(k) * stride;
+      ++n;
+      if (c >= cmax - 1e-9) break;
+    }
+    return n;
+  };
+  g->nx = count(cmax_x);
+  g->ny = count(cmax_y);
+  g->stride = stride;
+  g->size = size;
+  g->c0 = c0;
+  g->cmax_x = cmax_x;
+  g->cmax_y = cmax_y;
+  g->lastx0 = w - size;
+  g->lasty0 = h - size;
+  return true;
+}
+
+// ---------------------------------------------------------------------------
+// device arena
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaError_t ensure(size_t count) {
+    if (count <= n && p) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    if (count == 0) count = 1;
+    cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+    if (e == cudaSuccess) n = count;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+struct LevelBufs {
+  DevBuf<float> left, right, grad;
+  DevBuf<uint8_t> lvalid, rvalid, lq, rq, stage;
+  DevBuf<float2> rab;
+  DevBuf<double> u, prob, post, sigma;
+};
+
+}  // namespace
+
+enum { kStageH2D, kStagePyramid, kStagePatches, kStageFinalize, kStageD2H, kNumStages };
+static const char* kStageNames[kNumStages] = {"h2d", "pyramid", "patches", "finalize", "d2h"};
+
+struct pstereo_ctx {
+  int device = 0;
+  pstereo_params params{};
+  int max_w = 0, max_h = 0, max_pairs = 0;
+  cudaStream_t stream = nullptr;
+  std::string last_error;
+  int launches = 0;
+  bool profiling = false;
+  cudaEvent_t ev[kNumStages + 1] = {};
+  float stage_ms[kNumStages] = {};
+  // window / mask
+  int nwin = 0, wcenter = 0;
+  double woff[kMaxWin] = {};
+  DevBuf<double> mask;
+  // inputs
+  DevBuf<uint8_t> in_u8[2];
+  DevBuf<float> full[2];
+  DevBuf<uint8_t> full_valid[2];
+  std::vector<LevelBufs> levels;  // index e (0 unused unless finest_exp == 0)
+  // finest fields
+  DevBuf<double> fdisp, fprob, fvar;
+  DevBuf<uint8_t> fmvalid, fmask;
+  DevBuf<int> flabel, farea;
+  DevBuf<int> stats;
+  // staging for host outputs
+  DevBuf<uint8_t> out_stage[10];
+};
+
+namespace {
+
+int fail(pstereo_ctx* ctx, int code, const std::string& msg) {
+  if (ctx) ctx->last_error = msg;
+  return code;
+}
+
+int cuda_fail(pstereo_ctx* ctx, cudaError_t e, const char* where) {
+  return fail(ctx, PSTEREO_EINTERNAL,
+              std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(expr)                                              \
+  do {                                                        \
+    cudaError_t _e = (expr);                                  \
+    if (_e != cudaSuccess) return cuda_fail(ctx, _e, #expr);  \
+  } while (0)
+
+// Level geometry of a W x H call: exps coarsest..finest plus intermediate.
+int level_geometry(const pstereo_params* p, int W, int H, std::vector<LevelGeom>* out,
+                   std::string* msg) {
+  out->clear();
+  if (W <= 0 || H <= 0) {
+    *msg = "build_pyramid: empty image";
+    return PSTEREO_EDEGENERATE;
+  }
+  const int ce = p->coarsest_exp, fe = p->finest_exp;
+  std::vector<int> ws(ce + 1), hs(ce + 1);
+  ws[0] = W;
+  hs[0] = H;
+  for (int e = 1; e <= ce; ++e) {
+    ws[e] = (ws[e - 1] + 1) / 2;
+    hs[e] = (hs[e - 1] + 1) / 2;
+  }
+  // build_pyramid's check (src/pyramid.cpp:84-89)
+  if (ws[ce] < p->patch_size || hs[ce] < p->patch_size) {
+    char buf[160];
+    std::snprintf(buf, sizeof buf,
+                  "build_pyramid: coarsest level %dx%d is smaller than one patch (%d)",
+                  ws[ce], hs[ce], p->patch_size);
+    *msg = buf;
+    return PSTEREO_EDEGENERATE;
+  }
+  double denom = 0.0;
+  for (int e = ce; e >= fe; --e) denom += std::exp2(double(e));
+  for (int e = ce; e >= fe; --e) {
+    LevelGeom L;
+    L.e = e;
+    L.w = ws[e];
+    L.h = hs[e];
+    L.level_w = std::exp2(double(e)) / denom;
+    if (!make_grid(L.w, L.h, p->patch_size, p->overlap, &L.g)) {
+      *msg = "make_patch_grid: level is smaller than one patch";
+      return PSTEREO_EDEGENERATE;
+    }
+    out->push_back(L);
+  }
+  return PSTEREO_OK;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C ABI
+
+extern "C" {
+
+void pstereo_default_params(pstereo_params* p) {
+  std::memset(p, 0, sizeof *p);
+  p->coarsest_exp = 5;
+  p->finest_exp = 1;
+  p->patch_size = 10;
+  p->overlap = 0.55;
+  p->min_iterations = 12;
+  p->max_iterations = 12;
+  p->early_stop_good = 0.05;
+  p->early_stop_bad = 0.95;
+  p->early_stop_improve = 0.10;
+  p->n_window_offsets = 2;
+  p->window_offsets[0] = 0.5;
+  p->window_offsets[1] = 1.0;
+  p->sigma_s = 4.0;
+  p->pixel_threshold = 0.15;
+  p->gamma = 0.75;
+  p->valid_patch_ratio = 0.75;
+  p->estimate_variance = 0;
+  p->threads = 1;
+}
+
+int pstereo_validate(const pstereo_params* p, char* msg, size_t cap) {
+  std::string m;
+  const int rc = validate_params(p, &m);
+  if (msg && cap) {
+    std::snprintf(msg, cap, "%s", m.c_str());
+  }
+  return rc;
+}
+
+int pstereo_level_dims(const pstereo_params* p, int width, int height, int* n_levels,
+                       int* widths, int* heights, int* exps) {
+  std::string m;
+  int rc = validate_params(p, &m);
+  if (rc) return rc;
+  std::vector<LevelGeom> g;
+  rc = level_geometry(p, width, height, &g, &m);
+  if (rc) return rc;
+  *n_levels = int(g.size());
+  for (size_t i = 0; i < g.size(); ++i) {
+    if (widths) widths[i] = g[i].w;
+    if (heights) heights[i] = g[i].h;
+    if (exps) exps[i] = g[i].e;
+  }
+  return PSTEREO_OK;
+}
+
+int pstereo_gpu_create(int device, const pstereo_params* p, int max_width, int max_height,
+                       int max_pairs, pstereo_ctx** out) {
+  *out = nullptr;
+  std::string m;
+  int rc = validate_params(p, &m);
+  if (rc) {
+    pstereo_ctx tmp;
+    (void)tmp;
+    return rc;
+  }
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev <= device || device < 0) return PSTEREO_EINTERNAL;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return PSTEREO_EINTERNAL;
+  if (prop.major != 10) return PSTEREO_EINTERNAL;  // built for sm_100a only
+  if (max_width <= 0 || max_height <= 0 || max_pairs <= 0) return PSTEREO_EINTERNAL;
+  auto* ctx = new pstereo_ctx();
+  ctx->device = device;
+  ctx->params = *p;
+  ctx->max_w = max_width;
+  ctx->max_h = max_height;
+  ctx->max_pairs = max_pairs;
+  if (cudaSetDevice(device) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete ctx;
+    return PSTEREO_EINTERNAL;
+  }
+  for (auto& ev : ctx->ev) cudaEventCreate(&ev);
+  // window offsets: sorted symmetric closure with 0 (src/window_posterior.cpp:13-22)
+  std::vector<double> mags(p->window_offsets, p->window_offsets + p->n_window_offsets);
+  std::sort(mags.begin(), mags.end());
+  int k = 0;
+  for (auto it = mags.rbegin(); it != mags.rend(); ++it) ctx->woff[k++] = -*it;
+  ctx->wcenter = k;
+  ctx->woff[k++] = 0.0;
+  for (double v : mags) ctx->woff[k++] = v;
+  ctx->nwin = k;
+  // spatial mask (src/spatial_mask.cpp:7-23)
+  const int s = p->patch_size;
+  std::vector<double> mask(size_t(s) * s);
+  const double half = (s - 1) * 0.5, denom = 2.0 * p->sigma_s * p->sigma_s;
+  for (int j = 0; j < s; ++j)
+    for (int i = 0; i < s; ++i) {
+      const double dx = i - half, dy = j - half;
+      fast_exp_host(-(dx * dx + dy * dy) / denom, &mask[size_t(j) * s + i]);
+    }
+  if (ctx->mask.ensure(mask.size()) != cudaSuccess ||
+      cudaMemcpy(ctx->mask.p, mask.data(), mask.size() * sizeof(double),
+                 cudaMemcpyHostToDevice) != cudaSuccess) {
+    pstereo_gpu_destroy(ctx);
+    return PSTEREO_EINTERNAL;
+  }
+  ctx->levels.resize(size_t(p->coarsest_exp) + 1);
+  *out = ctx;
+  return PSTEREO_OK;
+}
+
+void pstereo_gpu_destroy(pstereo_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  ctx->mask.release();
+  for (auto& b : ctx->in_u8) b.release();
+  for (auto& b : ctx->full) b.release();
+  for (auto& b : ctx->full_valid) b.release();
+  for (auto& L : ctx->levels) {
+    L.left.release();
+    L.right.release();
+    L.grad.release();
+    L.lvalid.release();
+    L.rvalid.release();
+    L.lq.release();
+    L.rq.release();
+    L.stage.release();
+    L.rab.release();
+    L.u.release();
+    L.prob.release();
+    L.post.release();
+    L.sigma.release();
+  }
+  ctx->fdisp.release();
+  ctx->fprob.release();
+  ctx->fvar.release();
+  ctx->fmvalid.release();
+  ctx->fmask.release();
+  ctx->flabel.release();
+  ctx->farea.release();
+  ctx->stats.release();
+  for (auto& b : ctx->out_stage) b.release();
+  for (auto& ev : ctx->ev)
+    if (ev) cudaEventDestroy(ev);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+const char* pstereo_gpu_last_error(const pstereo_ctx* ctx) {
+  return ctx ? ctx->last_error.c_str() : "no context";
+}
+
+int pstereo_gpu_last_launch_count(const pstereo_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int pstereo_gpu_set_profiling(pstereo_ctx* ctx, int enable) {
+  if (!ctx) return PSTEREO_EINTERNAL;
+  ctx->profiling = enable != 0;
+  return PSTEREO_OK;
+}
+
+int pstereo_gpu_stage_times(const pstereo_ctx* ctx, float* ms, int cap) {
+  if (!ctx) return 0;
+  const int n = std::min(cap, int(kNumStages));
+  for (int i = 0; i < n; ++i) ms[i] = ctx->stage_ms[i];
+  return n;
+}
+
+const char* pstereo_gpu_stage_name(int stage) {
+  return (stage >= 0 && stage < kNumStages) ? kStageNames[stage] : "";
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// the batched pipeline
+
+namespace {
+
+int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left_u8,
+        const uint8_t* right_u8, const float* left_f, const uint8_t* left_v,
+        const float* right_f, const uint8_t* right_v, int inputs_on_device, double focal,
+        double baseline, const pstereo_outputs* out, cudaStream_t stream) {
+  const pstereo_params& prm = ctx->params;
+  ctx->launches = 0;
+  std::memset(ctx->stage_ms, 0, sizeof ctx->stage_ms);
+  if (n < 0) return fail(ctx, PSTEREO_EINTERNAL, "n_pairs must be >= 0");
+  if (n == 0) return PSTEREO_OK;
+  if (!out) return fail(ctx, PSTEREO_EINTERNAL, "outputs must not be NULL");
+  std::vector<LevelGeom> geo;
+  std::string m;
+  int rc = level_geometry(&prm, W, H, &geo, &m);
+  if (rc) return fail(ctx, rc, m);
+  if (W > ctx->max_w || H > ctx->max_h || n > ctx->max_pairs)
+    return fail(ctx, PSTEREO_EINTERNAL, "batch exceeds the context's max_width/max_height/max_pairs");
+  if (left_u8 && channels != 1 && channels != 3 && channels != 4)
+    return fail(ctx, PSTEREO_EINTERNAL, "to_grayscale: unsupported channel count");
+  CK(cudaSetDevice(ctx->device));
+  const cudaStream_t s = stream ? stream : ctx->stream;
+  const bool prof = ctx->profiling;
+  if (prof) CK(cudaEventRecord(ctx->ev[0], s));
+
+  const int ce = prm.coarsest_exp, fe = prm.finest_exp, S = prm.patch_size;
+  const long long n_full = (long long)W * H;
+  const long long npx = n_full * n;
+
+  // ---- inputs -> full-resolution fp32 planes
+  for (int v = 0; v < 2; ++v) {
+    CK(ctx->full[v].ensure(size_t(npx)));
+    CK(ctx->full_valid[v].ensure(size_t(npx)));
+  }
+  if (left_u8) {
+    const size_t bytes = size_t(npx) * channels;
+    const uint8_t* src[2] = {left_u8, right_u8};
+    for (int v = 0; v < 2; ++v) {
+      if (!inputs_on_device) {
+        CK(ctx->in_u8[v].ensure(bytes));
+        CK(cudaMemcpyAsync(ctx->in_u8[v].p, src[v], bytes, cudaMemcpyHostToDevice, s));
+        src[v] = ctx->in_u8[v].p;
+      }
+    }
+    if (prof) CK(cudaEventRecord(ctx->ev[1], s));
+    for (int v = 0; v < 2; ++v) {
+      launch_gray_u8(src[v], channels, npx, ctx->full[v].p, ctx->full_valid[v].p, s);
+      ++ctx->launches;
+    }
+  } else {
+    const float* fsrc[2] = {left_f, right_f};
+    const uint8_t* vsrc[2] = {left_v, right_v};
+    const cudaMemcpyKind kind = inputs_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    for (int v = 0; v < 2; ++v) {
+      CK(cudaMemcpyAsync(ctx->full[v].p, fsrc[v], size_t(npx) * sizeof(float), kind, s));
+      if (vsrc[v]) CK(cudaMemcpyAsync(ctx->full_valid[v].p, vsrc[v], size_t(npx), kind, s));
+      else CK(cudaMemsetAsync(ctx->full_valid[v].p, 1, size_t(npx), s));
+    }
+    if (prof) CK(cudaEventRecord(ctx->ev[1], s));
+  }
+
+  // ---- pyramid cascade (src/pyramid.cpp:59-81)
+  std::vector<int> ws(ce + 1), hs(ce + 1);
+  ws[0] = W;
+  hs[0] = H;
+  for (int e = 1; e <= ce; ++e) {
+    ws[e] = (ws[e - 1] + 1) / 2;
+    hs[e] = (hs[e - 1] + 1) / 2;
+    LevelBufs& B = ctx->levels[e];
+    const size_t np = size_t(ws[e]) * hs[e] * n;
+    CK(B.left.ensure(np));
+    CK(B.right.ensure(np));
+    CK(B.lvalid.ensure(np));
+    CK(B.rvalid.ensure(np));
+    const float* sl = e == 1 ? ctx->full[0].p : ctx->levels[e - 1].left.p;
+    const float* sr = e == 1 ? ctx->full[1].p : ctx->levels[e - 1].right.p;
+    const uint8_t* slv = e == 1 ? ctx->full_valid[0].p : ctx->levels[e - 1].lvalid.p;
+    const uint8_t* srv = e == 1 ? ctx->full_valid[1].p : ctx->levels[e - 1].rvalid.p;
+    launch_downsample(sl, slv, sr, srv, ws[e - 1], hs[e - 1], B.left.p, B.lvalid.p, B.right.p,
+                      B.rvalid.p, ws[e], hs[e], n, s);
+    ++ctx->launches;
+  }
+  std::vector<Level> lv(geo.size());
+  for (size_t li = 0; li < geo.size(); ++li) {
+    const LevelGeom& G = geo[li];
+    LevelBufs& B = ctx->levels[G.e];
+    Level& L = lv[li];
+    std::memset(&L, 0, sizeof L);
+    L.e = G.e;
+    L.w = G.w;
+    L.h = G.h;
+    L.plane = (long long)G.w * G.h;
+    const size_t np = size_t(L.plane) * n;
+    if (G.e == 0) {
+      L.left = ctx->full[0].p;
+      L.right = ctx->full[1].p;
+      L.lvalid = ctx->full_valid[0].p;
+      L.rvalid = ctx->full_valid[1].p;
+    } else {
+      L.left = B.left.p;
+      L.right = B.right.p;
+      L.lvalid = B.lvalid.p;
+      L.rvalid = B.rvalid.p;
+    }
+    CK(B.grad.ensure(np));
+    CK(B.lq.ensure(np));
+    CK(B.rq.ensure(np));
+    CK(B.rab.ensure(np));
+    const size_t nrec = size_t(G.g.nx) * G.g.ny * n;
+    CK(B.stage.ensure(nrec));
+    CK(B.u.ensure(nrec));
+    CK(B.prob.ensure(nrec));
+    CK(B.post.ensure(nrec));
+    CK(B.sigma.ensure(nrec));
+    L.grad = B.grad.p;
+    L.lq = B.lq.p;
+    L.rq = B.rq.p;
+    L.rab = B.rab.p;
+    L.g = G.g;
+    L.u = B.u.p;
+    L.prob = B.prob.p;
+    L.post = B.post.p;
+    L.sigma = B.sigma.p;
+    L.stage = B.stage.p;
+    L.level_w = G.level_w;
+    launch_level_tables(L, n, s);
+    ++ctx->launches;
+  }
+  if (prof) CK(cudaEventRecord(ctx->ev[2], s));
+
+  // ---- per-level patch solves, coarsest first (src/coarse_to_fine.cpp:235-326)
+  PatchParams pp;
+  std::memset(&pp, 0, sizeof pp);
+  pp.n_pairs = n;
+  pp.size = S;
+  pp.vpr = prm.valid_patch_ratio;
+  pp.min_it = prm.min_iterations;
+  pp.max_it = prm.max_iterations;
+  pp.stop_good = prm.early_stop_good;
+  pp.stop_bad = prm.early_stop_bad;
+  pp.stop_improve = prm.early_stop_improve;
+  pp.nwin = ctx->nwin;
+  pp.wcenter = ctx->wcenter;
+  for (int q = 0; q < ctx->nwin; ++q) pp.woff[q] = ctx->woff[q];
+  pp.prev_mask = ctx->mask.p;
+  for (size_t li = 0; li < lv.size(); ++li) {
+    pp.want_var = prm.estimate_variance && lv[li].e == fe;
+    pp.have_prev = li > 0;
+    const Level& P = li > 0 ? lv[li - 1] : lv[li];
+    launch_patches(lv[li], P, pp, s);
+    ++ctx->launches;
+  }
+  if (prof) CK(cudaEventRecord(ctx->ev[3], s));
+
+  // ---- finest fusion, confidence filter, output (src/pipeline.cpp:15-27)
+  const Level& F = lv.back();
+  const size_t fnp = size_t(F.plane) * n;
+  CK(ctx->fdisp.ensure(fnp));
+  CK(ctx->fprob.ensure(fnp));
+  if (prm.estimate_variance) CK(ctx->fvar.ensure(fnp));
+  CK(ctx->fmvalid.ensure(fnp));
+  CK(ctx->fmask.ensure(fnp));
+  CK(ctx->flabel.ensure(fnp));
+  CK(ctx->farea.ensure(fnp));
+  FinestBufs fb{ctx->fdisp.p, ctx->fprob.p, prm.estimate_variance ? ctx->fvar.p : nullptr,
+                ctx->fmvalid.p, ctx->fmask.p, ctx->flabel.p};
+  launch_fuse_finest(F, fb, ctx->mask.p, prm.estimate_variance, prm.pixel_threshold, n, s);
+  ++ctx->launches;
+  CK(cudaMemsetAsync(ctx->farea.p, 0, fnp * sizeof(int), s));
+  launch_ccl(F.w, F.h, F.plane, W, H, fe, ctx->fmask.p, ctx->flabel.p, ctx->farea.p, n, s);
+  ctx->launches += 2;
+
+  // outputs: device pointers directly, or device staging + D2H
+  const int f64 = out->dtype == PSTEREO_F64;
+  const size_t esz = f64 ? sizeof(double) : sizeof(float);
+  const size_t nout = size_t(n_full) * n;
+  void* host_ptr[10] = {out->disparity, out->disparity_valid, out->probability, out->depth,
+                        out->depth_valid, out->depth_sigma, out->sigma_valid,
+                        out->match_disparity, out->match_valid, out->var_disp};
+  const size_t sizes[10] = {esz, 1, esz, esz, 1, esz, 1, esz, 1, esz};
+  void* dev_ptr[10];
+  for (int q = 0; q < 10; ++q) {
+    dev_ptr[q] = host_ptr[q];
+    if (!prm.estimate_variance && (q == 5 || q == 6 || q == 9)) dev_ptr[q] = nullptr;
+    if (host_ptr[q] && dev_ptr[q] && !out->on_device) {
+      CK(ctx->out_stage[q].ensure(nout * sizes[q]));
+      dev_ptr[q] = ctx->out_stage[q].p;
+    }
+  }
+  OutputArgs oa;
+  std::memset(&oa, 0, sizeof oa);
+  oa.W = W;
+  oa.H = H;
+  oa.e = fe;
+  oa.fw = F.w;
+  oa.fh = F.h;
+  oa.fplane = F.plane;
+  oa.disp = ctx->fdisp.p;
+  oa.prob = ctx->fprob.p;
+  oa.var = prm.estimate_variance ? ctx->fvar.p : nullptr;
+  oa.mvalid = ctx->fmvalid.p;
+  oa.fmask = ctx->fmask.p;
+  oa.label = ctx->flabel.p;
+  oa.area = ctx->farea.p;
+  {
+    const long long mp = llround(std::ceil(prm.gamma * double(S) * double(S) - 1e-9));
+    oa.min_px = std::max(mp, 1ll);  // src/depth_variance.cpp:87-90
+  }
+  oa.scale_d = fe == 0 ? 1.0 : std::pow(2.0, fe);
+  oa.scale_v = fe == 0 ? 1.0 : std::pow(4.0, fe);
+  oa.fb = focal * baseline;
+  oa.has_var = prm.estimate_variance;
+  oa.out_disp = dev_ptr[0];
+  oa.out_dvalid = (uint8_t*)dev_ptr[1];
+  oa.out_prob = dev_ptr[2];
+  oa.out_depth = dev_ptr[3];
+  oa.out_depth_valid = (uint8_t*)dev_ptr[4];
+  oa.out_sigma = dev_ptr[5];
+  oa.out_sigma_valid = (uint8_t*)dev_ptr[6];
+  oa.out_mdisp = dev_ptr[7];
+  oa.out_mvalid = (uint8_t*)dev_ptr[8];
+  oa.out_var = dev_ptr[9];
+  launch_output(oa, f64, n, s);
+  ++ctx->launches;
+
+  const bool want_stats = out->stats != nullptr;
+  if (want_stats) {
+    StatsArgs sa;
+    std::memset(&sa, 0, sizeof sa);
+    sa.n_levels = int(lv.size());
+    for (size_t li = 0; li < lv.size(); ++li) {
+      sa.stage[li] = lv[li].stage;
+      sa.np[li] = lv[li].g.nx * lv[li].g.ny;
+    }
+    CK(ctx->stats.ensure(size_t(n) * lv.size() * 3));
+    sa.out = ctx->stats.p;
+    launch_stats(sa, n, s);
+    ++ctx->launches;
+  }
+  CK(cudaGetLastError());
+  if (prof) CK(cudaEventRecord(ctx->ev[4], s));
+
+  // ---- device -> host
+  bool need_sync = false;
+  if (!out->on_device) {
+    for (int q = 0; q < 10; ++q) {
+      if (!host_ptr[q] || !dev_ptr[q]) continue;
+      CK(cudaMemcpyAsync(host_ptr[q], dev_ptr[q], nout * sizes[q], cudaMemcpyDeviceToHost, s));
+      need_sync = true;
+    }
+  }
+  std::vector<int> hstats;
+  if (want_stats) {
+    hstats.resize(size_t(n) * lv.size() * 3);
+    CK(cudaMemcpyAsync(hstats.data(), ctx->stats.p, hstats.size() * sizeof(int),
+                       cudaMemcpyDeviceToHost, s));
+    need_sync = true;
+  }
+  // finest-level accepted patches (diagnostics; MatchResult::finest.patches)
+  std::vector<uint8_t> fst;
+  std::vector<double> fu, fpr, fpo, fsg;
+  const bool want_finest = out->finest && out->finest_count && out->finest_cap > 0;
+  if (want_finest) {
+    const size_t nrec = size_t(F.g.nx) * F.g.ny * n;
+    fst.resize(nrec);
+    fu.resize(nrec);
+    fpr.resize(nrec);
+    fpo.resize(nrec);
+    fsg.resize(nrec);
+    CK(cudaMemcpyAsync(fst.data(), F.stage, nrec, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(fu.data(), F.u, nrec * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(fpr.data(), F.prob, nrec * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(fpo.data(), F.post, nrec * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(fsg.data(), F.sigma, nrec * 8, cudaMemcpyDeviceToHost, s));
+    need_sync = true;
+  }
+  if (prof) CK(cudaEventRecord(ctx->ev[5], s));
+  if (need_sync || prof) CK(cudaStreamSynchronize(s));
+  if (prof) {
+    for (int q = 0; q < kNumStages; ++q)
+      cudaEventElapsedTime(&ctx->stage_ms[q], ctx->ev[q], ctx->ev[q + 1]);
+  }
+  if (want_stats) {
+    for (int p = 0; p < n; ++p)
+      for (size_t li = 0; li < lv.size(); ++li) {
+        pstereo_level_stats& st = out->stats[size_t(p) * lv.size() + li];
+        const int* c = &hstats[(size_t(p) * lv.size() + li) * 3];
+        st.exp = lv[li].e;
+        st.grid_patches = lv[li].g.nx * lv[li].g.ny;
+        st.extracted = c[0];
+        st.converged = c[1];
+        st.accepted = c[2];
+      }
+  }
+  if (want_finest) {
+    const Grid& g = F.g;
+    const int np = g.nx * g.ny;
+    for (int p = 0; p < n; ++p) {
+      int cnt = 0;
+      for (int k = 0; k < np; ++k) {
+        const size_t r = size_t(p) * np + k;
+        if (fst[r] != kAccepted) continue;
+        if (cnt < out->finest_cap) {
+          pstereo_patch_estimate& pe = out->finest[size_t(p) * out->finest_cap + cnt];
+          const int kx = k % g.nx, ky = k / g.nx;
+          pe.cx = kx == g.nx - 1 ? g.cmax_x : g.c0 + double(kx) * g.stride;
+          pe.cy = ky == g.ny - 1 ? g.cmax_y : g.c0 + double(ky) * g.stride;
+          pe.u = fu[r];
+          pe.prob = fpr[r];
+          pe.posterior = fpo[r];
+          pe.sigma_k = fsg[r];
+        }
+        ++cnt;
+      }
+      out->finest_count[p] = cnt;
+    }
+  }
+  return PSTEREO_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pstereo_gpu_match_u8(pstereo_ctx* ctx, int n_pairs, int width, int height, int channels,
+                         const uint8_t* left, const uint8_t* right, int inputs_on_device,
+                         double focal_px, double baseline, const pstereo_outputs* out,
+                         void* stream) {
+  if (!ctx) return PSTEREO_EINTERNAL;
+  if (n_pairs > 0 && (!left || !right)) return fail(ctx, PSTEREO_EINTERNAL, "null input");
+  return run(ctx, n_pairs, width, height, channels, left, right, nullptr, nullptr, nullptr,
+             nullptr, inputs_on_device, focal_px, baseline, out, (cudaStream_t)stream);
+}
+
+int pstereo_gpu_match_f32(pstereo_ctx* ctx, int n_pairs, int width, int height,
+                          const float* left, const uint8_t* left_valid, const float* right,
+                          const uint8_t* right_valid, int inputs_on_device, double focal_px,
+                          double baseline, const pstereo_outputs* out, void* stream) {
+  if (!ctx) return PSTEREO_EINTERNAL;
+  if (n_pairs > 0 && (!left || !right)) return fail(ctx, PSTEREO_EINTERNAL, "null input");
+  return run(ctx, n_pairs, width, height, 1, nullptr, nullptr, left, left_valid, right,
+             right_valid, inputs_on_device, focal_px, baseline, out, (cudaStream_t)stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,109 @@
+// bdis_device.cuh -- device-side numerics shared by the BDIS kernels.
+//
+// Everything here mirrors the reference's double/float arithmetic operation
+// for operation (the TU is compiled with --fmad=false and the critical spots
+// use explicit _rn intrinsics), so the GPU produces the same bits as the x86-64
+// SSE2 reference build. Citations: src/ = proj/src/, inc/ = proj/include/pstereo/.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace bdis {
+
+constexpr int kMaxPatch = 32;
+constexpr int kMaxWin = 33;  // 2 * PSTEREO_MAX_OFFSETS + 1
+
+enum Stage : uint8_t { kSkipped = 0, kSolved = 1, kConverged = 2, kAccepted = 3 };
+
+// Patch lattice of one level (src/coarse_to_fine.cpp:51-88). Centre k < n-1 is
+// c0 + k*stride, the last one is clamped to cmax, so the footprint of patch k
+// starts at k*stride (k < n-1) or at L - size (k = n-1): all integers.
+struct Grid {
+  int nx, ny, stride, size;
+  double c0, cmax_x, cmax_y;
+  int lastx0, lasty0;
+};
+
+// One pyramid level of a batch of pairs: planes are [pair][h][w].
+struct Level {
+  int e, w, h;
+  long long plane;
+  const float* left;
+  const uint8_t* lvalid;
+  const float* right;
+  const uint8_t* rvalid;
+  float* grad;     // gradient_x of left (src/pyramid.cpp:30-42)
+  uint8_t* lq;     // 4-tap validity of left at (x,y) (inc/image.hpp:68-69)
+  uint8_t* rq;     // 4-tap validity of right at (x,y)
+  float2* rab;     // right (x, min(x+1,w-1)) tap pair
+  Grid g;
+  // per-patch records [pair][ny][nx] (PatchEstimate, inc/coarse_to_fine.hpp:39-47)
+  double* u;
+  double* prob;
+  double* post;
+  double* sigma;
+  uint8_t* stage;
+  double level_w;  // level_weight(e, levels), src/coarse_to_fine.cpp:90-94
+};
+
+// inc/fast_exp.hpp:16-28 -- Schraudolph's exponent-field trick, double layout.
+__device__ __forceinline__ double fast_exp(double x) {
+  if (x < -30.0) return 0.0;
+  const double scale = 4503599627370496.0 / 0.6931471805599453;
+  const long long bias = (1023LL << 52) - (60801LL << 32);
+  const long long bits = __double2ll_rz(__dmul_rn(x, scale)) + bias;
+  return __longlong_as_double(bits);
+}
+
+__device__ __forceinline__ int clampi(int v, int lo, int hi) {
+  return v < lo ? lo : (hi < v ? hi : v);
+}
+
+// std::lround: half away from zero.
+__device__ __forceinline__ int lround_i(double v) { return (int)llround(v); }
+
+// Weighted gather of the accepted patches of level P that cover pixel (x, y),
+// in ascending patch index -- the exact accumulation order of fuse_level's
+// scatter (src/coarse_to_fine.cpp:120-135), so the sums are bit-identical.
+struct Fused {
+  double sw, swu, swp, sw2s;
+};
+
+template <bool kProb, bool kVar>
+__device__ __forceinline__ Fused gather(const Level& P, long long pair, int x,
+                                        int y, const double* __restrict__ mask) {
+  const Grid& g = P.g;
+  const int s = g.size, st = g.stride;
+  const long long base = pair * (long long)g.nx * g.ny;
+  Fused f{0.0, 0.0, 0.0, 0.0};
+  const int ky_lo = (y - s + 1 <= 0) ? 0 : (y - s + 1 + st - 1) / st;
+  const int ky_hi = min(g.ny - 2, y / st);
+  const int kx_lo = (x - s + 1 <= 0) ? 0 : (x - s + 1 + st - 1) / st;
+  const int kx_hi = min(g.nx - 2, x / st);
+  const bool last_x = x >= g.lastx0;
+  auto add = [&](long long idx, double m) {
+    if (P.stage[idx] != kAccepted) return;
+    const double pr = P.prob[idx];
+    const double w = __dmul_rn(pr, m);
+    f.sw = __dadd_rn(f.sw, w);
+    f.swu = __dadd_rn(f.swu, __dmul_rn(w, P.u[idx]));
+    if (kProb) f.swp = __dadd_rn(f.swp, __dmul_rn(w, pr));
+    if (kVar) {
+      const double sk = P.sigma[idx];
+      f.sw2s = __dadd_rn(f.sw2s, __dmul_rn(__dmul_rn(__dmul_rn(w, w), sk), sk));
+    }
+  };
+  auto row = [&](int ky, int y0) {
+    const int j = y - y0;
+    const double* mrow = mask + j * s;
+    const long long rbase = base + (long long)ky * g.nx;
+    for (int kx = kx_lo; kx <= kx_hi; ++kx) add(rbase + kx, mrow[x - kx * st]);
+    if (last_x) add(rbase + g.nx - 1, mrow[x - g.lastx0]);
+  };
+  for (int ky = ky_lo; ky <= ky_hi; ++ky) row(ky, ky * st);
+  if (y >= g.lasty0) row(g.ny - 1, g.lasty0);
+  return f;
+}
+
+}  // namespace bdis
