@@ -1,0 +1,370 @@
+#!/usr/bin/env python
+"""BDIS matching-core throughput on B200 (BASELINE.json metric: 640x480 stereo
+pairs/sec, fraction of the memory roofline).
+
+A "step" = one batched run_pipeline (pyramid -> per-level patch solves ->
+finest fusion -> confidence filter -> depth) over BATCH pairs of the config-2
+workload (seeded config-0 generator pairs, 640x480 uint8 gray, exps 3..1, 8x8
+patches at stride 4, variance off). Pairs are independent, so under torchrun
+each rank processes its own BATCH pairs (seeds rank*BATCH...), no collective on
+the data path ("scaling": "weak"); the only NCCL call is the max-over-ranks
+reduction of the timings.
+
+  value   device-resident inputs/outputs, CUDA events on the launch stream
+  e2e     the same through the public C ABI with pinned HOST buffers: H2D of
+          both views and D2H of disparity+validity inside every timed step
+  roofline  dominant kernel (k_patches, all levels) from live CUDA events
+  cpu_baseline  the reference (oracle/_ref, the unmodified reference sources)
+          on this host's cores, bounded sample (rank 0, N=1 only)
+
+--impl reference times the reference CPU implementation itself, all host cores,
+same metric/config.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+W, H = 640, 480
+HBM_FALLBACK_GBS = 6650.0
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return HBM_FALLBACK_GBS, "fallback"
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (oracle/_ref = the reference's own sources, or the C port)
+
+def _cpu_oracle():
+    from oracle import pyoracle
+
+    kind = "reference" if pyoracle.available("reference") else "port"
+    return pyoracle.load(kind), kind
+
+
+def cpu_throughput(left, right, cfg, threads, focal=500.0, baseline=5.0):
+    """Runs run_pipeline on every pair with `threads` workers (threads=1 each,
+    pair-level parallelism, the fair CPU throughput per SURVEY.md 8d).
+    Returns (pairs/s over the wall time, per-pair runtime_ms list)."""
+    orc, _ = _cpu_oracle()
+    grays = [(orc.to_grayscale(left[k])[0], orc.to_grayscale(right[k])[0])
+             for k in range(left.shape[0])]
+    idx = [0]
+    lock = threading.Lock()
+    times = []
+
+    def worker():
+        while True:
+            with lock:
+                k = idx[0]
+                idx[0] += 1
+            if k >= len(grays):
+                return
+            r = orc.run_pipeline(grays[k][0], grays[k][1], cfg, focal, baseline)
+            with lock:
+                times.append(r["runtime_ms"])
+
+    ths = [threading.Thread(target=worker) for _ in range(threads)]
+    t0 = time.perf_counter()
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    wall = time.perf_counter() - t0
+    return len(grays) / wall, times
+
+
+def oracle_cfg():
+    from oracle import pyoracle
+
+    return pyoracle.Config(coarsest_exp=3, finest_exp=1, patch_size=8, overlap=0.5)
+
+
+def run_reference_arm(args):
+    import paper_2205_03133_b200 as P
+
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cores = host_cores()
+    orc, kind = _cpu_oracle()
+    n = max(cores, 1)
+    left, right = P.synth_batch(0, n * (args.steps + args.warmup), seed0=0, threads=cores)
+    cfg = oracle_cfg()
+    total_pairs, total_t = 0, 0.0
+    for step in range(args.warmup + args.steps):
+        sl = slice(step * n, (step + 1) * n)
+        rate, _ = cpu_throughput(left[sl], right[sl], cfg, cores)
+        if step >= args.warmup:
+            total_pairs += n
+            total_t += n / rate
+    value = total_pairs / total_t
+    sample = (f"{args.steps} steps x {n} config-2 pairs (640x480, seeds 0..), one pair per core "
+              f"per step, run_pipeline threads=1")
+    line = {
+        "impl": "reference", "metric": "640x480 stereo pairs/sec", "value": value,
+        "unit": "pairs/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total_t / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "config2: 640x480 u8 gray, exps 3..1, s=8 stride 4, var off",
+                   "global_batch": n, "parallelism": f"{cores} host threads"},
+        "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": cores, "kind": kind,
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU clocks during the timed region
+
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for line in Path(self.path).read_text().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                rows.append((float(parts[1]), float(parts[2]), parts[5:9]))
+            except ValueError:
+                continue
+        os.unlink(self.path)
+        if not rows:
+            return None
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for _, _, fl in rows for i, v in enumerate(fl)
+                          if v.lower() == "active"})
+        return {"sm_mhz": float(np.median([r[0] for r in rows])),
+                "sm_max_mhz": max(r[1] for r in rows), "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2205_03133_b200 as P
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    B = args.batch
+    cfg = P.PipelineConfig.baseline(0)
+    left, right = P.synth_batch(0, B, seed0=rank * B, threads=max(1, host_cores() // max(world, 1)))
+    dev = torch.device("cuda", local)
+    dl = torch.from_numpy(left).to(dev)
+    dr = torch.from_numpy(right).to(dev)
+    disp = torch.empty((B, H, W), dtype=torch.float32, device=dev)
+    valid = torch.empty((B, H, W), dtype=torch.uint8, device=dev)
+    m = P.Matcher(cfg, W, H, B, device=local)
+    stream = torch.cuda.current_stream(dev)
+    sh = stream.cuda_stream
+    outs = {"disparity": disp.data_ptr(), "disparity_valid": valid.data_ptr()}
+
+    def step():
+        m.run_device_u8(B, W, H, 1, dl.data_ptr(), dr.data_ptr(), outs, stream=sh)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    launches_per_step = m.launch_count()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    m.set_profiling(True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    stages, calls = m.stage_times()
+    m.set_profiling(False)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = world * B * args.steps / (ms_max / 1e3)
+
+    # ---- e2e through the public ABI with pinned host buffers
+    hl = torch.from_numpy(left).pin_memory()
+    hr = torch.from_numpy(right).pin_memory()
+    hd = torch.empty((B, H, W), dtype=torch.float32).pin_memory()
+    hv = torch.empty((B, H, W), dtype=torch.uint8).pin_memory()
+    houts = {"disparity": hd.data_ptr(), "disparity_valid": hv.data_ptr()}
+
+    def step_e2e():
+        m.run_host_u8(B, W, H, 1, hl.data_ptr(), hr.data_ptr(), houts, stream=sh)
+
+    e2e_steps = max(3, min(args.steps, 10))
+    step_e2e()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        step_e2e()
+    torch.cuda.synchronize(dev)
+    e2e_s = time.perf_counter() - t0
+    te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = world * B * e2e_steps / float(te.item())
+    # parity spot check of the e2e output against the device-resident run
+    assert torch.equal(hd, disp.cpu()) and torch.equal(hv, valid.cpu()), "e2e output differs"
+
+    # ---- roofline of the dominant kernel (k_patches, one launch per level)
+    hbm, peak_kind = peaks()
+    dims = P.level_dims(cfg, W, H)
+    alg_bytes = 0.0
+    for e, w, h in dims:
+        s, st = cfg.patch_size, max(1, int(round(cfg.patch_size * (1 - cfg.overlap))))
+        nx = len(_axis(w, s, st))
+        ny = len(_axis(h, s, st))
+        # read left/right/grad fp32 planes (12 B/px) and
+        # the coarser level's records (16 B/patch), write records (32 B/patch)
+        alg_bytes += B * (12.0 * w * h + 48.0 * nx * ny)
+    patch_ms = sum(v for k, v in stages.items() if k.startswith("patches_")) / max(calls, 1)
+    achieved = alg_bytes / (patch_ms / 1e3) / 1e9
+    step_ms = ms_max / args.steps
+    b_pair = W * H * (2 * 1 + 4 + 1)
+    line = {
+        "metric": "640x480 stereo pairs/sec", "value": value, "unit": "pairs/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded config-0 generator, see DESIGN.md)",
+        "config": {"workload": "config2: batch of 640x480 u8 gray pairs, exps 3..1, 8x8 patches "
+                               "stride 4, variance off",
+                   "global_batch": world * B, "per_gpu_batch": B,
+                   "parallelism": f"pair-sharded x{world} (no collective)",
+                   "l2": "inputs 157 MB/step per GPU > 126 MB L2 (no flush needed)"},
+        "gpu_launches": launches_per_step * args.steps,
+        "e2e": {"value": e2e_value, "unit": "pairs/s", "h2d_bytes_per_step": 2 * B * W * H,
+                "d2h_bytes_per_step": B * W * H * 5, "steps": e2e_steps},
+        "roofline": {"bound": "hbm", "kernel": "k_patches (all levels)", "achieved": achieved,
+                     "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
+                     "peak_kind": peak_kind,
+                     "alg_bytes_per_step": alg_bytes, "kernel_ms_per_step": patch_ms,
+                     "kernel_share_of_step": patch_ms / step_ms,
+                     "note": "FP64 issue-bound (bit-exact mirror of the reference's double "
+                             "arithmetic); see DESIGN.md"},
+        "path_roofline": {"bytes_per_pair": b_pair, "roofline_pairs_s": hbm * 1e9 / b_pair,
+                          "frac": value / (world * hbm * 1e9 / b_pair)},
+        "stage_ms_per_step": {k: v / max(calls, 1) for k, v in stages.items()},
+        "clocks": clk,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cores = host_cores()
+        n_cpu = min(B, max(16, 16 * cores))
+        rate, times = cpu_throughput(left[:n_cpu], right[:n_cpu], oracle_cfg(), cores)
+        _, kind = _cpu_oracle()
+        line["cpu_baseline"] = {
+            "value": rate, "unit": "pairs/s", "cores": cores, "kind": kind,
+            "sample": f"first {n_cpu} pairs of this batch, {cores} workers x run_pipeline "
+                      f"threads=1; median single-pair runtime_ms {float(np.median(times)):.1f}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    m.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _axis(L, s, stride):
+    c0 = (s - 1) * 0.5
+    cmax = (L - 1) - c0
+    out = []
+    k = 0
+    while True:
+        c = c0 + k * stride
+        if c >= cmax - 1e-9:
+            out.append(cmax)
+            return out
+        out.append(c)
+        k += 1
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--batch", type=int, default=256)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

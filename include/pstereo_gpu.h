@@ -174,12 +174,15 @@ int pstereo_gpu_match_f32(pstereo_ctx* ctx, int n_pairs, int width, int height,
 /* Kernel launches issued by the last match call (telemetry for bench.py). */
 int pstereo_gpu_last_launch_count(const pstereo_ctx* ctx);
 
-/* Device time (ms) of each stage of the last match call when profiling is
- * enabled with pstereo_gpu_set_profiling(ctx, 1); names via
- * pstereo_gpu_stage_name. Returns the number of stages written. */
+/* Stage timing with CUDA events recorded on the launch stream (no extra
+ * synchronisation inside match calls). set_profiling(ctx, 1) resets the
+ * accumulators; stage_times() waits for the recorded calls and returns the
+ * number of stages, writing the total device ms per stage summed over
+ * *n_calls calls. Stages: h2d, pyramid, patches_e<exp> per level (coarsest
+ * first), finalize, d2h; names via pstereo_gpu_stage_name. */
 int pstereo_gpu_set_profiling(pstereo_ctx* ctx, int enable);
-int pstereo_gpu_stage_times(const pstereo_ctx* ctx, float* ms, int cap);
-const char* pstereo_gpu_stage_name(int stage);
+int pstereo_gpu_stage_times(pstereo_ctx* ctx, double* ms_total, int cap, int* n_calls);
+const char* pstereo_gpu_stage_name(const pstereo_ctx* ctx, int stage);
 
 /* ---- deterministic synthetic pairs (BASELINE.json configs) ---- */
 typedef struct pstereo_synth_spec {

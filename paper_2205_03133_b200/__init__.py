@@ -104,12 +104,13 @@ def lib() -> C.CDLL:
         L.pstereo_gpu_last_error.restype = C.c_char_p
         L.pstereo_gpu_last_error.argtypes = [C.c_void_p]
         L.pstereo_gpu_stage_name.restype = C.c_char_p
+        L.pstereo_gpu_stage_name.argtypes = [C.c_void_p, C.c_int]
         L.pstereo_gpu_create.argtypes = [C.c_int, C.POINTER(_Params), C.c_int, C.c_int, C.c_int,
                                          C.POINTER(C.c_void_p)]
         L.pstereo_gpu_destroy.argtypes = [C.c_void_p]
         L.pstereo_gpu_last_launch_count.argtypes = [C.c_void_p]
         L.pstereo_gpu_set_profiling.argtypes = [C.c_void_p, C.c_int]
-        L.pstereo_gpu_stage_times.argtypes = [C.c_void_p, f32p, C.c_int]
+        L.pstereo_gpu_stage_times.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.c_int, i32p]
         L.pstereo_gpu_match_u8.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
                                            C.c_void_p, C.c_void_p, C.c_int, C.c_double,
                                            C.c_double, C.POINTER(_Outputs), C.c_void_p]
@@ -306,10 +307,14 @@ class Matcher:
     def set_profiling(self, on: bool):
         lib().pstereo_gpu_set_profiling(self._h, int(on))
 
-    def stage_times(self) -> dict:
-        ms = np.zeros(8, np.float32)
-        n = lib().pstereo_gpu_stage_times(self._h, ms.ctypes.data_as(f32p), 8)
-        return {lib().pstereo_gpu_stage_name(i).decode(): float(ms[i]) for i in range(n)}
+    def stage_times(self):
+        """(total device ms per stage since set_profiling(True), number of calls)."""
+        ms = np.zeros(32, np.float64)
+        calls = C.c_int()
+        n = lib().pstereo_gpu_stage_times(self._h, ms.ctypes.data_as(C.POINTER(C.c_double)), 32,
+                                          C.byref(calls))
+        names = [lib().pstereo_gpu_stage_name(self._h, i).decode() for i in range(n)]
+        return dict(zip(names, (float(v) for v in ms[:n]))), calls.value
 
     # ---- host-memory batched API (numpy in, numpy out)
     def run_batch(self, left, right, focal=1.0, baseline=1.0, dtype=F32, left_valid=None,

@@ -144,8 +144,12 @@ struct LevelBufs {
 
 }  // namespace
 
-enum { kStageH2D, kStagePyramid, kStagePatches, kStageFinalize, kStageD2H, kNumStages };
-static const char* kStageNames[kNumStages] = {"h2d", "pyramid", "patches", "finalize", "d2h"};
+// Stage boundaries recorded per call when profiling: h2d, pyramid, one
+// k_patches launch per level (coarsest first), finalize, d2h.
+struct EvSet {
+  std::vector<cudaEvent_t> ev;
+  int n_marks = 0;
+};
 
 struct pstereo_ctx {
   int device = 0;
@@ -155,8 +159,10 @@ struct pstereo_ctx {
   std::string last_error;
   int launches = 0;
   bool profiling = false;
-  cudaEvent_t ev[kNumStages + 1] = {};
-  float stage_ms[kNumStages] = {};
+  std::vector<EvSet> ev_pending, ev_free;
+  std::vector<double> stage_ms;
+  std::vector<std::string> stage_names;
+  int prof_calls = 0;
   // window / mask
   int nwin = 0, wcenter = 0;
   double woff[kMaxWin] = {};
@@ -318,7 +324,6 @@ int pstereo_gpu_create(int device, const pstereo_params* p, int max_width, int m
     delete ctx;
     return PSTEREO_EINTERNAL;
   }
-  for (auto& ev : ctx->ev) cudaEventCreate(&ev);
   // window offsets: sorted symmetric closure with 0 (src/window_posterior.cpp:13-22)
   std::vector<double> mags(p->window_offsets, p->window_offsets + p->n_window_offsets);
   std::sort(mags.begin(), mags.end());
@@ -380,8 +385,9 @@ void pstereo_gpu_destroy(pstereo_ctx* ctx) {
   ctx->farea.release();
   ctx->stats.release();
   for (auto& b : ctx->out_stage) b.release();
-  for (auto& ev : ctx->ev)
-    if (ev) cudaEventDestroy(ev);
+  for (auto* pool : {&ctx->ev_pending, &ctx->ev_free})
+    for (auto& set : *pool)
+      for (auto ev : set.ev) cudaEventDestroy(ev);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -394,19 +400,41 @@ int pstereo_gpu_last_launch_count(const pstereo_ctx* ctx) { return ctx ? ctx->la
 
 int pstereo_gpu_set_profiling(pstereo_ctx* ctx, int enable) {
   if (!ctx) return PSTEREO_EINTERNAL;
+  cudaSetDevice(ctx->device);
+  for (auto& set : ctx->ev_pending) ctx->ev_free.push_back(std::move(set));
+  ctx->ev_pending.clear();
+  ctx->stage_ms.clear();
+  ctx->stage_names.clear();
+  ctx->prof_calls = 0;
   ctx->profiling = enable != 0;
   return PSTEREO_OK;
 }
 
-int pstereo_gpu_stage_times(const pstereo_ctx* ctx, float* ms, int cap) {
+int pstereo_gpu_stage_times(pstereo_ctx* ctx, double* ms_total, int cap, int* n_calls) {
   if (!ctx) return 0;
-  const int n = std::min(cap, int(kNumStages));
-  for (int i = 0; i < n; ++i) ms[i] = ctx->stage_ms[i];
+  cudaSetDevice(ctx->device);
+  for (auto& set : ctx->ev_pending) {
+    if (set.n_marks < 2) continue;
+    cudaEventSynchronize(set.ev[size_t(set.n_marks) - 1]);
+    if (ctx->stage_ms.size() < size_t(set.n_marks) - 1) ctx->stage_ms.resize(size_t(set.n_marks) - 1, 0.0);
+    for (int q = 0; q + 1 < set.n_marks; ++q) {
+      float t = 0.0f;
+      cudaEventElapsedTime(&t, set.ev[size_t(q)], set.ev[size_t(q) + 1]);
+      ctx->stage_ms[size_t(q)] += t;
+    }
+    ++ctx->prof_calls;
+    ctx->ev_free.push_back(std::move(set));
+  }
+  ctx->ev_pending.clear();
+  const int n = std::min(cap, int(ctx->stage_ms.size()));
+  for (int i = 0; i < n; ++i) ms_total[i] = ctx->stage_ms[size_t(i)];
+  if (n_calls) *n_calls = ctx->prof_calls;
   return n;
 }
 
-const char* pstereo_gpu_stage_name(int stage) {
-  return (stage >= 0 && stage < kNumStages) ? kStageNames[stage] : "";
+const char* pstereo_gpu_stage_name(const pstereo_ctx* ctx, int stage) {
+  if (!ctx || stage < 0 || size_t(stage) >= ctx->stage_names.size()) return "";
+  return ctx->stage_names[size_t(stage)].c_str();
 }
 
 }  // extern "C"
@@ -422,7 +450,6 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
         double baseline, const pstereo_outputs* out, cudaStream_t stream) {
   const pstereo_params& prm = ctx->params;
   ctx->launches = 0;
-  std::memset(ctx->stage_ms, 0, sizeof ctx->stage_ms);
   if (n < 0) return fail(ctx, PSTEREO_EINTERNAL, "n_pairs must be >= 0");
   if (n == 0) return PSTEREO_OK;
   if (!out) return fail(ctx, PSTEREO_EINTERNAL, "outputs must not be NULL");
@@ -437,7 +464,29 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
   CK(cudaSetDevice(ctx->device));
   const cudaStream_t s = stream ? stream : ctx->stream;
   const bool prof = ctx->profiling;
-  if (prof) CK(cudaEventRecord(ctx->ev[0], s));
+  EvSet evs;
+  if (prof) {
+    if (!ctx->ev_free.empty()) {
+      evs = std::move(ctx->ev_free.back());
+      ctx->ev_free.pop_back();
+    }
+    evs.n_marks = 0;
+    ctx->stage_names.assign({"h2d", "pyramid"});
+    for (const auto& G : geo) ctx->stage_names.push_back("patches_e" + std::to_string(G.e));
+    ctx->stage_names.push_back("finalize");
+    ctx->stage_names.push_back("d2h");
+  }
+  auto mark = [&]() -> cudaError_t {
+    if (!prof) return cudaSuccess;
+    if (evs.ev.size() <= size_t(evs.n_marks)) {
+      cudaEvent_t e;
+      cudaError_t err = cudaEventCreate(&e);
+      if (err != cudaSuccess) return err;
+      evs.ev.push_back(e);
+    }
+    return cudaEventRecord(evs.ev[size_t(evs.n_marks++)], s);
+  };
+  CK(mark());
 
   const int ce = prm.coarsest_exp, fe = prm.finest_exp, S = prm.patch_size;
   const long long n_full = (long long)W * H;
@@ -458,7 +507,7 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
         src[v] = ctx->in_u8[v].p;
       }
     }
-    if (prof) CK(cudaEventRecord(ctx->ev[1], s));
+    CK(mark());
     for (int v = 0; v < 2; ++v) {
       launch_gray_u8(src[v], channels, npx, ctx->full[v].p, ctx->full_valid[v].p, s);
       ++ctx->launches;
@@ -472,7 +521,7 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
       if (vsrc[v]) CK(cudaMemcpyAsync(ctx->full_valid[v].p, vsrc[v], size_t(npx), kind, s));
       else CK(cudaMemsetAsync(ctx->full_valid[v].p, 1, size_t(npx), s));
     }
-    if (prof) CK(cudaEventRecord(ctx->ev[1], s));
+    CK(mark());
   }
 
   // ---- pyramid cascade (src/pyramid.cpp:59-81)
@@ -542,7 +591,7 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
     launch_level_tables(L, n, s);
     ++ctx->launches;
   }
-  if (prof) CK(cudaEventRecord(ctx->ev[2], s));
+  CK(mark());
 
   // ---- per-level patch solves, coarsest first (src/coarse_to_fine.cpp:235-326)
   PatchParams pp;
@@ -565,8 +614,8 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
     const Level& P = li > 0 ? lv[li - 1] : lv[li];
     launch_patches(lv[li], P, pp, s);
     ++ctx->launches;
+    CK(mark());
   }
-  if (prof) CK(cudaEventRecord(ctx->ev[3], s));
 
   // ---- finest fusion, confidence filter, output (src/pipeline.cpp:15-27)
   const Level& F = lv.back();
@@ -654,7 +703,7 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
     ++ctx->launches;
   }
   CK(cudaGetLastError());
-  if (prof) CK(cudaEventRecord(ctx->ev[4], s));
+  CK(mark());
 
   // ---- device -> host
   bool need_sync = false;
@@ -690,12 +739,9 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
     CK(cudaMemcpyAsync(fsg.data(), F.sigma, nrec * 8, cudaMemcpyDeviceToHost, s));
     need_sync = true;
   }
-  if (prof) CK(cudaEventRecord(ctx->ev[5], s));
-  if (need_sync || prof) CK(cudaStreamSynchronize(s));
-  if (prof) {
-    for (int q = 0; q < kNumStages; ++q)
-      cudaEventElapsedTime(&ctx->stage_ms[q], ctx->ev[q], ctx->ev[q + 1]);
-  }
+  CK(mark());
+  if (prof) ctx->ev_pending.push_back(std::move(evs));
+  if (need_sync) CK(cudaStreamSynchronize(s));
   if (want_stats) {
     for (int p = 0; p < n; ++p)
       for (size_t li = 0; li < lv.size(); ++li) {

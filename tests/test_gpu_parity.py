@@ -1,0 +1,140 @@
+"""GPU parity: the sm_100a path through the C ABI against the CPU oracle
+(oracle/bdis_oracle.c, itself pinned bit-exact to the reference build) on the
+same seeded inputs. Bit-exact except var_disp / depth sigma (1e-3 rel, see
+tests/parity.py)."""
+import numpy as np
+import pytest
+
+from tests.parity import compare_pair, run_gpu_batch, run_oracle
+
+pytestmark = pytest.mark.gpu
+
+FOCAL, BASELINE = 500.0, 5.0
+
+
+def _check(P, port, cfg, left_u8, right_u8, lv=None, rv=None):
+    """left_u8/right_u8: [n,h,w(,c)] uint8 rasters."""
+    gpu = run_gpu_batch(P, cfg, left_u8, right_u8, FOCAL, BASELINE)
+    out = []
+    for k in range(left_u8.shape[0]):
+        lf, lvk = port.to_grayscale(left_u8[k])
+        rf, rvk = port.to_grayscale(right_u8[k])
+        pipe, match = run_oracle(port, lf, rf, cfg, FOCAL, BASELINE, lvk, rvk)
+        out.append(compare_pair(gpu, k, pipe, match, cfg))
+    return out
+
+
+def test_config0_pair_bitexact(gpu, port):
+    P = gpu
+    l, r = P.synth_pair(0)
+    _check(P, port, P.PipelineConfig.baseline(0), l[None], r[None])
+
+
+def test_config1_stress_variance(gpu, port):
+    P = gpu
+    l, r = P.synth_pair(1)
+    st = _check(P, port, P.PipelineConfig.baseline(1), l[None], r[None])
+    print("config1 agreement", st)
+
+
+def test_reference_defaults(gpu, port):
+    P = gpu
+    l, r = P.synth_pair(0, seed=7)
+    _check(P, port, P.PipelineConfig(), l[None], r[None])
+
+
+def test_batch_of_seeds(gpu, port):
+    P = gpu
+    left, right = P.synth_batch(0, 4, seed0=10, width=320, height=240)
+    _check(P, port, P.PipelineConfig.baseline(0), left, right)
+
+
+@pytest.mark.parametrize("size,stride", [(8, 2), (12, 4), (16, 6), (10, 5), (9, 3)])
+def test_patch_size_stride_sweep(gpu, port, size, stride):
+    P = gpu
+    l, r = P.synth_pair(0, seed=3, width=200, height=150)
+    cfg = P.PipelineConfig(coarsest_exp=2, finest_exp=1, patch_size=size,
+                           overlap=1.0 - stride / size, estimate_variance=True)
+    _check(P, port, cfg, l[None], r[None])
+
+
+@pytest.mark.parametrize("w,h", [(97, 75), (64, 48), (33, 17)])
+def test_odd_dimensions(gpu, port, w, h):
+    P = gpu
+    l, r = P.synth_pair(0, seed=5, width=w, height=h, blur_sigma=8.0, d_range=6.0, d_min=1.0)
+    cfg = P.PipelineConfig(coarsest_exp=1, finest_exp=0, patch_size=6, overlap=0.5,
+                           estimate_variance=True)
+    _check(P, port, cfg, l[None], r[None])
+
+
+def test_rgb_and_rgba_validity(gpu, port):
+    P = gpu
+    l, r = P.synth_pair(0, seed=11, width=160, height=120, channels=3)
+    cfg = P.PipelineConfig(coarsest_exp=2, finest_exp=1, patch_size=8, overlap=0.5)
+    _check(P, port, cfg, l[None], r[None])
+    # RGBA: alpha == 0 marks invalid pixels (src/image.cpp:32-34)
+    rng = np.random.default_rng(0)
+    la = np.concatenate([l, np.full(l.shape[:2] + (1,), 255, np.uint8)], axis=2)
+    ra = np.concatenate([r, np.full(r.shape[:2] + (1,), 255, np.uint8)], axis=2)
+    la[30:60, 40:80, 3] = 0
+    ra[rng.random(ra.shape[:2]) < 0.01, 3] = 0
+    _check(P, port, cfg, la[None], ra[None])
+
+
+def test_float_api_with_mask(gpu, port):
+    """GrayImage entry point with an explicit validity mask."""
+    P = gpu
+    l, r = P.synth_pair(0, seed=2, width=128, height=96)
+    lf, _ = port.to_grayscale(l)
+    rf, _ = port.to_grayscale(r)
+    lv = np.ones_like(l, np.uint8)
+    lv[:, 100:] = 0
+    cfg = P.PipelineConfig(coarsest_exp=2, finest_exp=1, patch_size=8, overlap=0.5,
+                           estimate_variance=True)
+    gpu_out = run_gpu_batch(P, cfg, lf[None], rf[None], FOCAL, BASELINE, left_valid=lv[None])
+    pipe, match = run_oracle(port, lf, rf, cfg, FOCAL, BASELINE, lv, None)
+    compare_pair(gpu_out, 0, pipe, match, cfg)
+
+
+def test_shifted_analytic_pair(gpu, port):
+    """The reference's own end-to-end case (tests/test_coarse_to_fine.cpp:253-287):
+    64x48 sinusoid pair shifted by 2 px, exps 2..1, recovered within 0.2 px."""
+    P = gpu
+    y, x = np.mgrid[0:48, 0:64].astype(np.float64)
+
+    def tex(xx):
+        return (0.5 + 0.2 * np.sin(xx * 0.37 + 0.8) + 0.15 * np.sin(y * 0.29)
+                + 0.1 * np.sin((xx + y) * 0.143)).astype(np.float32)
+
+    left, right = tex(x), tex(x + 2.0)
+    cfg = P.PipelineConfig(coarsest_exp=2, finest_exp=1)
+    res = P.match_stereo(left, right, cfg)
+    st = res["stats"]
+    assert st[0][0] == 2 and st[1][0] == 1
+    assert all(s[4] > 0 for s in st)
+    valid = res["disparity_valid"].astype(bool)
+    assert valid.sum() > 64 * 48 / 2
+    assert np.abs(res["disparity"][valid] - 2.0).max() < 0.2
+    pipe, match = run_oracle(port, left, right, cfg, 1.0, 1.0)
+    np.testing.assert_array_equal(res["disparity"], match["disparity"])
+
+
+def test_determinism(gpu):
+    P = gpu
+    left, right = P.synth_batch(0, 2, seed0=0, width=320, height=240)
+    cfg = P.PipelineConfig.baseline(1)
+    a = run_gpu_batch(P, cfg, left, right, FOCAL, BASELINE)
+    b = run_gpu_batch(P, cfg, left, right, FOCAL, BASELINE)
+    for k in ("disparity", "disparity_valid", "depth", "var_disp"):
+        assert np.array_equal(a[k], b[k]), k
+
+
+def test_errors(gpu):
+    P = gpu
+    with pytest.raises(P.ConfigError):
+        P.Matcher(P.PipelineConfig(patch_size=1), 64, 48)
+    m = P.Matcher(P.PipelineConfig(coarsest_exp=5, finest_exp=1, patch_size=10), 64, 48)
+    l = np.zeros((1, 48, 64), np.uint8)
+    with pytest.raises(P.DegenerateInputError):
+        m.run_batch(l, l)  # 64x48 at 1/32 is 2x2 < 10 px (tests/test_pyramid.cpp:90-92)
+    m.close()
