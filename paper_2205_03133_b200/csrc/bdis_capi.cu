@@ -138,7 +138,7 @@ struct DevBuf {
 struct LevelBufs {
   DevBuf<float> left, right, grad;
   DevBuf<uint8_t> lvalid, rvalid, lq, rq, stage;
-  DevBuf<float2> rab;
+  DevBuf<double> rd;
   DevBuf<double> u, prob, post, sigma;
 };
 
@@ -155,6 +155,7 @@ struct pstereo_ctx {
   int device = 0;
   pstereo_params params{};
   int max_w = 0, max_h = 0, max_pairs = 0;
+  int max_smem = 0;  // opt-in shared memory per CTA
   cudaStream_t stream = nullptr;
   std::string last_error;
   int launches = 0;
@@ -319,6 +320,7 @@ int pstereo_gpu_create(int device, const pstereo_params* p, int max_width, int m
   ctx->max_w = max_width;
   ctx->max_h = max_height;
   ctx->max_pairs = max_pairs;
+  cudaDeviceGetAttribute(&ctx->max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   if (cudaSetDevice(device) != cudaSuccess ||
       cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
     delete ctx;
@@ -370,7 +372,7 @@ void pstereo_gpu_destroy(pstereo_ctx* ctx) {
     L.lq.release();
     L.rq.release();
     L.stage.release();
-    L.rab.release();
+    L.rd.release();
     L.u.release();
     L.prob.release();
     L.post.release();
@@ -570,7 +572,7 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
     CK(B.grad.ensure(np));
     CK(B.lq.ensure(np));
     CK(B.rq.ensure(np));
-    CK(B.rab.ensure(np));
+    CK(B.rd.ensure(size_t(G.w + 1) * G.h * n));
     const size_t nrec = size_t(G.g.nx) * G.g.ny * n;
     CK(B.stage.ensure(nrec));
     CK(B.u.ensure(nrec));
@@ -580,7 +582,7 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
     L.grad = B.grad.p;
     L.lq = B.lq.p;
     L.rq = B.rq.p;
-    L.rab = B.rab.p;
+    L.rd = B.rd.p;
     L.g = G.g;
     L.u = B.u.p;
     L.prob = B.prob.p;
@@ -608,11 +610,15 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
   pp.wcenter = ctx->wcenter;
   for (int q = 0; q < ctx->nwin; ++q) pp.woff[q] = ctx->woff[q];
   pp.prev_mask = ctx->mask.p;
+  // every input pixel is valid for gray/RGB rasters and for float planes
+  // without masks: the kernels then skip the 4-tap validity tests
+  pp.all_valid = left_u8 ? (channels != 4) : (left_v == nullptr && right_v == nullptr);
   for (size_t li = 0; li < lv.size(); ++li) {
     pp.want_var = prm.estimate_variance && lv[li].e == fe;
     pp.have_prev = li > 0;
     const Level& P = li > 0 ? lv[li - 1] : lv[li];
-    launch_patches(lv[li], P, pp, s);
+    const BandPlan bp = plan_bands(lv[li], pp, ctx->max_smem);
+    CK(launch_patches(lv[li], P, pp, bp, s));
     ++ctx->launches;
     CK(mark());
   }
@@ -633,7 +639,7 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
   ++ctx->launches;
   CK(cudaMemsetAsync(ctx->farea.p, 0, fnp * sizeof(int), s));
   launch_ccl(F.w, F.h, F.plane, W, H, fe, ctx->fmask.p, ctx->flabel.p, ctx->farea.p, n, s);
-  ctx->launches += 2;
+  ctx->launches += 3;
 
   // outputs: device pointers directly, or device staging + D2H
   const int f64 = out->dtype == PSTEREO_F64;

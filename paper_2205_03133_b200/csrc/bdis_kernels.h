@@ -22,7 +22,67 @@ struct PatchParams {
   int want_var;
   int have_prev;
   const double* prev_mask;  // spatial mask (s*s doubles, device)
+  int all_valid;            // every input pixel valid: skip the 4-tap tests
 };
+
+// Row-band decomposition of one level for k_patches (host-planned).
+struct BandPlan {
+  int rb;          // patch rows per CTA
+  int n_bands;     // ceil(ny / rb)
+  int threads;     // CTA size
+  int smem_rows;   // (rb - 1) * stride + size
+  int rpitch;      // smem slots per right-view row (doubles)
+  int fpitch;      // smem slots per left/gradient row (floats)
+  int bpitch;      // bytes per validity row
+  int use_smem;    // 0: read the level tables from global memory
+  size_t smem_bytes;
+  int npb;         // max patches per band = rb * nx
+};
+
+// Shared-memory layout of one k_patches CTA (byte offsets), shared by the
+// host planner and the kernel.
+struct BandLayout {
+  size_t oR, oL, oG, oLQ, oRQ;
+  size_t oMean, oHess, oTmsq, oU, oPrev, oLastd, oWres;
+  size_t oCnt, oList0, oList1, oCounters;
+  size_t oIter, oStage, oWok;
+  size_t total;
+};
+
+__host__ __device__ inline BandLayout band_layout(int rows, int rpitch, int fpitch, int bpitch,
+                                                  int npb, int nwin, bool valid) {
+  BandLayout l;
+  size_t o = 0;
+  auto take = [&](size_t bytes, size_t align) {
+    o = (o + align - 1) / align * align;
+    const size_t r = o;
+    o += bytes;
+    return r;
+  };
+  l.oR = take(size_t(rows) * rpitch * 8, 16);
+  l.oL = take(size_t(rows) * fpitch * 4, 16);
+  l.oG = take(size_t(rows) * fpitch * 4, 16);
+  l.oLQ = take(valid ? size_t(rows) * bpitch : 0, 16);
+  l.oRQ = take(valid ? size_t(rows) * bpitch : 0, 16);
+  l.oMean = take(size_t(npb) * 8, 8);
+  l.oHess = take(size_t(npb) * 8, 8);
+  l.oTmsq = take(size_t(npb) * 8, 8);
+  l.oU = take(size_t(npb) * 8, 8);
+  l.oPrev = take(size_t(npb) * 8, 8);
+  l.oLastd = take(size_t(npb) * 8, 8);
+  l.oWres = take(size_t(npb) * nwin * 8, 8);
+  l.oCnt = take(size_t(npb) * 4, 4);
+  l.oList0 = take(size_t(npb) * nwin * 4, 4);
+  l.oList1 = take(size_t(npb) * nwin * 4, 4);
+  l.oCounters = take(4 * 4, 4);
+  l.oIter = take(size_t(npb), 1);
+  l.oStage = take(size_t(npb), 1);
+  l.oWok = take(size_t(npb) * nwin, 1);
+  l.total = (o + 15) / 16 * 16;
+  return l;
+}
+
+BandPlan plan_bands(const Level& L, const PatchParams& pp, int max_smem_per_cta);
 
 struct FinestBufs {
   double* disp;
@@ -72,7 +132,8 @@ void launch_downsample(const float* sl, const uint8_t* slv, const float* sr,
                        float* dr, uint8_t* drv, int dw, int dh, int n_pairs,
                        cudaStream_t s);
 void launch_level_tables(const Level& L, int n_pairs, cudaStream_t s);
-void launch_patches(const Level& L, const Level& P, const PatchParams& pp, cudaStream_t s);
+cudaError_t launch_patches(const Level& L, const Level& P, const PatchParams& pp,
+                           const BandPlan& bp, cudaStream_t s);
 void launch_fuse_finest(const Level& L, const FinestBufs& fb, const double* mask,
                         int want_var, double threshold, int n_pairs, cudaStream_t s);
 void launch_ccl(int w, int h, long long plane, int full_w, int full_h, int e,

@@ -1,0 +1,612 @@
+// bdis_patches.cu -- k_patches: the per-patch body of match_stereo
+// (src/coarse_to_fine.cpp:247-300) for every patch of one pyramid level of a
+// batch of pairs: extract_patch + precompute_patch_system (src/patch.cpp:5-38,
+// src/lk_solver.cpp:7-36), the 1-D inverse-compositional LK solve
+// (src/lk_solver.cpp:83-132), the residual window (src/window_posterior.cpp:
+// 10-96), probability propagation (src/coarse_to_fine.cpp:90-99) and the
+// optional Gauss-Newton variance fit (src/depth_variance.cpp:94-170).
+//
+// B200 mapping
+//   * one CTA per (pair, band of `rb` patch rows); the band's rows of the
+//     right view (fp64), left view and gradient (fp32) are staged in shared
+//     memory once, padded (x + x/16 for 8-byte, x + x/32 for 4-byte slots) so
+//     the stride-`stride` accesses of neighbouring patches hit distinct banks;
+//   * a thread owns a patch evaluation at a time and sums its samples in the
+//     reference's sequential row-major order -- that is what makes every sum
+//     bit-identical to the CPU (a warp tree reduction would reorder them);
+//   * the LK iterations and the window samples are scheduled as work items in
+//     rounds: after every round the still-active items are compacted, so the
+//     1..12 iteration spread between patches costs no idle lanes, and the
+//     window evaluations of a converged patch run in parallel in the next
+//     round;
+//   * per-evaluation constant-fraction fast path: for a lattice patch the
+//     right samples of one row are x_i = (x0 + i) - u. When x_first and
+//     x_last are inside [0, w-1] and share one binade, fl((x0+i) - u) =
+//     (x0+i) + c for one c (the integers x0+i are multiples of the binade's
+//     ulp, and round-to-nearest-even of (x0+i) + (-u) then only depends on
+//     -u), so floor(x_i) = floor(x_first) + i and the interpolation weight
+//     fx = x_i - floor(x_i) is the same double for every i. That removes the
+//     per-sample double->int->double conversions without changing a bit;
+//     every other evaluation falls back to the literal per-sample
+//     sample_bilinear arithmetic.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <math.h>
+#include <math_constants.h>
+#include <stdint.h>
+
+#include "bdis_device.cuh"
+#include "bdis_kernels.h"
+
+namespace bdis {
+
+namespace {
+
+struct Ev {
+  double msq, jr;
+  int n;
+};
+
+template <bool kSmem>
+struct Rows {
+  const double* R;   // right view, fp64, rows of (w+1)
+  const float* Lf;   // left view
+  const float* Gf;   // gradient of the left view
+  const uint8_t* lq; // 4-tap validity (kValid only)
+  const uint8_t* rq;
+  int rp, fp, bp;    // row pitches (slots)
+  __device__ __forceinline__ static int s8(int x) { return kSmem ? x + (x >> 4) : x; }
+  __device__ __forceinline__ static int s4(int x) { return kSmem ? x + (x >> 5) : x; }
+};
+
+// eval_patch_residual (src/lk_solver.cpp:38-81) of a lattice patch whose
+// footprint starts at column x0 and row r0 of `rw`.
+template <int S, bool kSmem, bool kValid>
+__device__ __forceinline__ Ev eval_patch(const Rows<kSmem>& rw, int w, int s_rt, int x0, int r0,
+                                         double xd0, double xdl, double mean, double u) {
+  const int s = S > 0 ? S : s_rt;
+  const double xf = __dsub_rn(xd0, u);
+  const double xl = __dsub_rn(xdl, u);
+  const double wm1 = (double)(w - 1);
+  const bool fast = xf >= 0.0 && xl <= wm1 &&
+                    (__double2hiint(xf) >> 20) == (__double2hiint(xl) >> 20);
+  double sum = 0.0;
+  int n = 0;
+  Ev ev;
+  ev.jr = 0.0;
+  if (fast) {
+    const int base = __double2int_rz(xf);
+    const double fx = __dsub_rn(xf, (double)base);
+    const double omf = __dsub_rn(1.0, fx);
+    // pass 1: mean of the right samples over jointly valid pixels. Sample i
+    // reads taps (base+i, base+i+1); tap base+i+1 is sample i+1's first tap.
+#pragma unroll 1
+    for (int j = 0; j < s; ++j) {
+      const double* rr = rw.R + (r0 + j) * rw.rp;
+      double a = rr[rw.s8(base)];
+      auto body = [&](int i) {
+        const double b = rr[rw.s8(base + i + 1)];
+        const double v = __dadd_rn(__dmul_rn(omf, a), __dmul_rn(fx, b));
+        a = b;
+        if (kValid) {
+          if (!(rw.lq[(r0 + j) * rw.bp + x0 + i] && rw.rq[(r0 + j) * rw.bp + base + i])) return;
+          ++n;
+        }
+        sum = __dadd_rn(sum, v);
+      };
+      if (S > 0) {
+#pragma unroll
+        for (int i = 0; i < (S > 0 ? S : 1); ++i) body(i);
+      } else {
+        for (int i = 0; i < s; ++i) body(i);
+      }
+    }
+    if (!kValid) n = s * s;
+    ev.n = n;
+    ev.msq = CUDART_INF;
+    if (n == 0) return ev;
+    const double rmean = __ddiv_rn(sum, (double)n);
+    double ssr = 0.0, jr = 0.0;
+#pragma unroll 1
+    for (int j = 0; j < s; ++j) {
+      const double* rr = rw.R + (r0 + j) * rw.rp;
+      const float* lr = rw.Lf + (r0 + j) * rw.fp;
+      const float* gr = rw.Gf + (r0 + j) * rw.fp;
+      double a = rr[rw.s8(base)];
+      auto body = [&](int i) {
+        const double b = rr[rw.s8(base + i + 1)];
+        const double v = __dadd_rn(__dmul_rn(omf, a), __dmul_rn(fx, b));
+        a = b;
+        if (kValid && !(rw.lq[(r0 + j) * rw.bp + x0 + i] && rw.rq[(r0 + j) * rw.bp + base + i]))
+          return;
+        const double t = __dsub_rn((double)lr[rw.s4(x0 + i)], mean);
+        const double r = __dsub_rn(__dsub_rn(v, rmean), t);
+        ssr = __dadd_rn(ssr, __dmul_rn(r, r));
+        jr = __dadd_rn(jr, __dmul_rn((double)gr[rw.s4(x0 + i)], r));
+      };
+      if (S > 0) {
+#pragma unroll
+        for (int i = 0; i < (S > 0 ? S : 1); ++i) body(i);
+      } else {
+        for (int i = 0; i < s; ++i) body(i);
+      }
+    }
+    ev.msq = __ddiv_rn(ssr, (double)n);
+    ev.jr = jr;
+    return ev;
+  }
+  // General path: the literal per-sample arithmetic of sample_bilinear
+  // (inc/image.hpp:53-71) at integer rows -- bounds test, truncation, weight.
+#pragma unroll 1
+  for (int j = 0; j < s; ++j) {
+    const double* rr = rw.R + (r0 + j) * rw.rp;
+    for (int i = 0; i < s; ++i) {
+      // (cx + offset(i)) - u with cx + offset(i) == x0 + i exactly
+      const double X = __dsub_rn(__dadd_rn(xd0, (double)i), u);
+      if (kValid && !rw.lq[(r0 + j) * rw.bp + x0 + i]) continue;
+      if (!(X >= 0.0 && X <= wm1)) continue;
+      const int xi = __double2int_rz(X);
+      if (kValid && !rw.rq[(r0 + j) * rw.bp + xi]) continue;
+      const double fx = __dsub_rn(X, (double)xi);
+      const double v = __dadd_rn(__dmul_rn(__dsub_rn(1.0, fx), rr[rw.s8(xi)]),
+                                 __dmul_rn(fx, rr[rw.s8(xi + 1)]));
+      sum = __dadd_rn(sum, v);
+      ++n;
+    }
+  }
+  ev.n = n;
+  ev.msq = CUDART_INF;
+  if (n == 0) return ev;
+  const double rmean = __ddiv_rn(sum, (double)n);
+  double ssr = 0.0, jr = 0.0;
+#pragma unroll 1
+  for (int j = 0; j < s; ++j) {
+    const double* rr = rw.R + (r0 + j) * rw.rp;
+    const float* lr = rw.Lf + (r0 + j) * rw.fp;
+    const float* gr = rw.Gf + (r0 + j) * rw.fp;
+    for (int i = 0; i < s; ++i) {
+      if (kValid && !rw.lq[(r0 + j) * rw.bp + x0 + i]) continue;
+      const double X = __dsub_rn(__dadd_rn(xd0, (double)i), u);
+      if (!(X >= 0.0 && X <= wm1)) continue;
+      const int xi = __double2int_rz(X);
+      if (kValid && !rw.rq[(r0 + j) * rw.bp + xi]) continue;
+      const double fx = __dsub_rn(X, (double)xi);
+      const double v = __dadd_rn(__dmul_rn(__dsub_rn(1.0, fx), rr[rw.s8(xi)]),
+                                 __dmul_rn(fx, rr[rw.s8(xi + 1)]));
+      const double t = __dsub_rn((double)lr[rw.s4(x0 + i)], mean);
+      const double r = __dsub_rn(__dsub_rn(v, rmean), t);
+      ssr = __dadd_rn(ssr, __dmul_rn(r, r));
+      jr = __dadd_rn(jr, __dmul_rn((double)gr[rw.s4(x0 + i)], r));
+    }
+  }
+  ev.msq = __ddiv_rn(ssr, (double)n);
+  ev.jr = jr;
+  return ev;
+}
+
+// estimate_patch_variance (src/depth_variance.cpp:94-170) on the window
+// priors. CUDA exp() may differ from glibc's by an ulp: sigma_k agrees to
+// ~1e-15 relative, which is why var_disp is held to 1e-3 rel, not bits.
+__device__ double variance_fit(const double* woff, int nwin, int wcenter, const double* res,
+                               const uint8_t* ok, double denom) {
+  double delta[kMaxWin], p[kMaxWin];
+  double center_prior = 0.0;
+  int n = 0;
+  for (int k = 0; k < nwin; ++k) {
+    if (!ok[k]) continue;
+    const double pr = fast_exp(__ddiv_rn(-res[k], denom));
+    delta[n] = woff[k];
+    p[n] = pr;
+    ++n;
+    if (k == wcenter) center_prior = pr;
+  }
+  const double fallback = 2.0;  // kSigmaFallback, inc/depth_variance.hpp:15
+  if (n < 3) return fallback;
+  for (int i = 0; i < n; ++i) {
+    if (delta[i] == 0.0) continue;
+    if (!(center_prior > p[i])) return fallback;
+  }
+  double c = 1.0;
+  double sigma = sqrt(0.1);
+  for (int iter = 0; iter < 10; ++iter) {  // kVarianceFitIterations
+    double a00 = 0.0, a01 = 0.0, a11 = 0.0, b0 = 0.0, b1 = 0.0;
+    for (int i = 0; i < n; ++i) {
+      const double d2 = __dmul_rn(delta[i], delta[i]);
+      const double g = exp(__ddiv_rn(-d2, __dmul_rn(__dmul_rn(2.0, sigma), sigma)));
+      const double r = __dsub_rn(__dmul_rn(c, g), p[i]);
+      const double js = __ddiv_rn(__dmul_rn(__dmul_rn(c, g), d2),
+                                  __dmul_rn(__dmul_rn(sigma, sigma), sigma));
+      a00 = __dadd_rn(a00, __dmul_rn(g, g));
+      a01 = __dadd_rn(a01, __dmul_rn(g, js));
+      a11 = __dadd_rn(a11, __dmul_rn(js, js));
+      b0 = __dsub_rn(b0, __dmul_rn(g, r));
+      b1 = __dsub_rn(b1, __dmul_rn(js, r));
+    }
+    if (!(a00 > 0.0)) return fallback;
+    const double l00 = __dsqrt_rn(a00);
+    const double l01 = __ddiv_rn(a01, l00);
+    const double d11 = __dsub_rn(a11, __dmul_rn(l01, l01));
+    if (!(d11 > 1e-300)) return fallback;
+    const double l11 = __dsqrt_rn(d11);
+    const double y0 = __ddiv_rn(b0, l00);
+    const double y1 = __ddiv_rn(__dsub_rn(b1, __dmul_rn(l01, y0)), l11);
+    const double xs = __ddiv_rn(y1, l11);
+    const double xc = __ddiv_rn(__dsub_rn(y0, __dmul_rn(l01, xs)), l00);
+    c = __dadd_rn(c, xc);
+    sigma = __dadd_rn(sigma, xs);
+    if (!isfinite(c) || !isfinite(sigma) || sigma <= 0.0) return fallback;
+  }
+  double ssr = 0.0;
+  for (int i = 0; i < n; ++i) {
+    const double g = exp(__ddiv_rn(__dmul_rn(-delta[i], delta[i]),
+                                   __dmul_rn(__dmul_rn(2.0, sigma), sigma)));
+    const double r = __dsub_rn(__dmul_rn(c, g), p[i]);
+    ssr = __dadd_rn(ssr, __dmul_rn(r, r));
+  }
+  const double fit = __dsqrt_rn(__ddiv_rn(ssr, (double)n));
+  if (!isfinite(fit)) return fallback;
+  if (fit > 0.1) return fallback;  // kVarianceFitMaxResidual
+  return sigma;
+}
+
+}  // namespace
+
+template <int S, bool kSmem, bool kValid>
+__global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams pp, BandPlan bp) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const Grid& g = L.g;
+  const int s = S > 0 ? S : g.size;
+  const int w = L.w, h = L.h;
+  const long long pair = blockIdx.y;
+  const int ky0 = blockIdx.x * bp.rb;
+  const int ky1 = min(ky0 + bp.rb, g.ny);
+  const int npb = (ky1 - ky0) * g.nx;
+  const int nwin = pp.nwin;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  auto row_start = [&](int ky) { return ky == g.ny - 1 ? g.lasty0 : ky * g.stride; };
+  const int ylo = row_start(ky0);
+  const int nrows = row_start(ky1 - 1) + s - ylo;
+
+  // ---- shared-memory carve-up (mirrors band_layout on the host)
+  const BandLayout lay = band_layout(bp.use_smem ? bp.smem_rows : 0, bp.rpitch, bp.fpitch,
+                                     bp.bpitch, bp.npb, nwin, kValid);
+  double* sR = (double*)(smem + lay.oR);
+  float* sL = (float*)(smem + lay.oL);
+  float* sG = (float*)(smem + lay.oG);
+  uint8_t* sLQ = smem + lay.oLQ;
+  uint8_t* sRQ = smem + lay.oRQ;
+  double* st_mean = (double*)(smem + lay.oMean);
+  double* st_hess = (double*)(smem + lay.oHess);
+  double* st_tmsq = (double*)(smem + lay.oTmsq);
+  double* st_u = (double*)(smem + lay.oU);
+  double* st_prev = (double*)(smem + lay.oPrev);
+  double* st_lastd = (double*)(smem + lay.oLastd);
+  double* st_wres = (double*)(smem + lay.oWres);
+  int* st_cnt = (int*)(smem + lay.oCnt);
+  uint8_t* st_iter = smem + lay.oIter;
+  uint8_t* st_stage = smem + lay.oStage;
+  uint8_t* st_wok = smem + lay.oWok;
+  uint32_t* list[2] = {(uint32_t*)(smem + lay.oList0), (uint32_t*)(smem + lay.oList1)};
+  int* counters = (int*)(smem + lay.oCounters);  // [0],[1]: list sizes
+
+  const long long pbase = pair * L.plane;
+  Rows<kSmem> rw;
+  int rofs;  // row index of image row y in rw: y - rofs
+  if (kSmem) {
+    // ---- stage the band (coalesced global reads, padded shared writes)
+    const double* gR = L.rd + pair * (long long)(w + 1) * h + (long long)ylo * (w + 1);
+    for (int r = 0; r < nrows; ++r) {
+      for (int x = tid; x <= w; x += nt) sR[r * bp.rpitch + Rows<true>::s8(x)] = gR[(long long)r * (w + 1) + x];
+      const float* gl = L.left + pbase + (long long)(ylo + r) * w;
+      const float* gg = L.grad + pbase + (long long)(ylo + r) * w;
+      for (int x = tid; x < w; x += nt) {
+        sL[r * bp.fpitch + Rows<true>::s4(x)] = gl[x];
+        sG[r * bp.fpitch + Rows<true>::s4(x)] = gg[x];
+      }
+      if (kValid) {
+        const uint8_t* lq = L.lq + pbase + (long long)(ylo + r) * w;
+        const uint8_t* rq = L.rq + pbase + (long long)(ylo + r) * w;
+        for (int x = tid; x < w; x += nt) {
+          sLQ[r * bp.bpitch + x] = lq[x];
+          sRQ[r * bp.bpitch + x] = rq[x];
+        }
+      }
+    }
+    rw.R = sR;
+    rw.Lf = sL;
+    rw.Gf = sG;
+    rw.lq = sLQ;
+    rw.rq = sRQ;
+    rw.rp = bp.rpitch;
+    rw.fp = bp.fpitch;
+    rw.bp = bp.bpitch;
+    rofs = ylo;
+  } else {
+    rw.R = L.rd + pair * (long long)(w + 1) * h;
+    rw.Lf = L.left + pbase;
+    rw.Gf = L.grad + pbase;
+    rw.lq = L.lq + pbase;
+    rw.rq = L.rq + pbase;
+    rw.rp = w + 1;
+    rw.fp = w;
+    rw.bp = w;
+    rofs = 0;
+  }
+  if (tid < 2) counters[tid] = 0;
+  __syncthreads();
+
+  // ---- setup: extract_patch + precompute_patch_system + u0 (:250-262)
+  for (int p = tid; p < npb; p += nt) {
+    const int kx = p % g.nx, ky = ky0 + p / g.nx;
+    const int x0 = kx == g.nx - 1 ? g.lastx0 : kx * g.stride;
+    const int r0 = row_start(ky) - rofs;
+    uint8_t stage = kSkipped;
+    double sum = 0.0;
+    int count = 0;
+    for (int j = 0; j < s; ++j) {
+      const float* lr = rw.Lf + (r0 + j) * rw.fp;
+      for (int i = 0; i < s; ++i) {
+        if (kValid && !rw.lq[(r0 + j) * rw.bp + x0 + i]) continue;
+        sum = __dadd_rn(sum, (double)lr[rw.s4(x0 + i)]);
+        ++count;
+      }
+    }
+    double mean = 0.0, hess = 0.0, tsq = 0.0;
+    bool ok = count > 0;
+    if (ok) {
+      mean = __ddiv_rn(sum, (double)count);
+      ok = !(__ddiv_rn((double)count, (double)(s * s)) < pp.vpr);  // :251
+    }
+    if (ok) {
+      for (int j = 0; j < s; ++j) {
+        const float* lr = rw.Lf + (r0 + j) * rw.fp;
+        const float* gr = rw.Gf + (r0 + j) * rw.fp;
+        for (int i = 0; i < s; ++i) {
+          if (kValid && !rw.lq[(r0 + j) * rw.bp + x0 + i]) continue;
+          const double gv = (double)gr[rw.s4(x0 + i)];
+          hess = __dadd_rn(hess, __dmul_rn(gv, gv));
+          const double t = __dsub_rn((double)lr[rw.s4(x0 + i)], mean);
+          tsq = __dadd_rn(tsq, __dmul_rn(t, t));
+        }
+      }
+      ok = (hess >= 1e-8) && isfinite(hess);  // degenerate (:254, lk_solver.cpp:33)
+    }
+    if (ok) {
+      stage = kSolved;
+      const double cx = kx == g.nx - 1 ? g.cmax_x : __dadd_rn(g.c0, (double)kx * g.stride);
+      const double cy = ky == g.ny - 1 ? g.cmax_y : __dadd_rn(g.c0, (double)ky * g.stride);
+      double u = 0.0;
+      if (pp.have_prev) {
+        const int ix = clampi(lround_i(cx), 0, w - 1);
+        const int iy = clampi(lround_i(cy), 0, h - 1);
+        const Fused f = gather<false, false>(P, pair, min(ix / 2, P.w - 1), min(iy / 2, P.h - 1),
+                                            pp.prev_mask);
+        if (!(f.sw <= 0.0)) u = __dmul_rn(2.0, __ddiv_rn(f.swu, f.sw));
+      }
+      st_mean[p] = mean;
+      st_hess[p] = hess;
+      st_tmsq[p] = __ddiv_rn(tsq, (double)count);
+      st_u[p] = u;
+      st_prev[p] = CUDART_INF;
+      st_lastd[p] = 0.0;
+      st_cnt[p] = count;
+      st_iter[p] = 0;
+      const double xc = __dsub_rn(cx, u);  // in_bounds(cx - u0, cy), lk_solver.cpp:89
+      if (xc >= 0.0 && xc <= (double)(w - 1)) {
+        const int q = atomicAdd(&counters[0], 1);
+        list[0][q] = (uint32_t)(p * (nwin + 1));
+      }
+    }
+    st_stage[p] = stage;
+  }
+  __syncthreads();
+
+  // ---- rounds of evaluation work items: (p, LK) and (p, window k)
+  int cur = 0;
+  for (;;) {
+    const int n_items = counters[cur];
+    if (n_items == 0) break;
+    for (int q = tid; q < n_items; q += nt) {
+      const int item = list[cur][q];
+      const int p = item / (nwin + 1), k = item % (nwin + 1) - 1;
+      const int kx = p % g.nx, ky = ky0 + p / g.nx;
+      const int x0 = kx == g.nx - 1 ? g.lastx0 : kx * g.stride;
+      const int r0 = row_start(ky) - rofs;
+      const double xd0 = (double)x0, xdl = (double)(x0 + s - 1);
+      const double u = k < 0 ? st_u[p] : __dadd_rn(st_u[p], pp.woff[k]);
+      const Ev ev = eval_patch<S, kSmem, kValid>(rw, w, s, x0, r0, xd0, xdl, st_mean[p], u);
+      if (k >= 0) {
+        // sample_window: valid iff every template pixel was sampled (:31-36)
+        st_wres[p * nwin + k] = ev.msq;
+        st_wok[p * nwin + k] = ev.n == st_cnt[p];
+        continue;
+      }
+      // one iteration of solve_patch_disparity (src/lk_solver.cpp:96-127)
+      const int it = st_iter[p] + 1;
+      st_iter[p] = (uint8_t)it;
+      bool done = false, conv = false;
+      if (ev.n == 0) {
+        done = true;
+      } else {
+        const double r = ev.msq;
+        const double prev = st_prev[p];
+        if (it >= pp.min_it) {
+          if (r < pp.stop_good) {
+            conv = done = true;
+          } else if (r > __dmul_rn(pp.stop_bad, st_tmsq[p])) {
+            done = true;
+          } else if (isfinite(prev) && __dsub_rn(prev, r) < __dmul_rn(pp.stop_improve, prev)) {
+            conv = it > 1 && fabs(st_lastd[p]) < 1e-2;
+            done = true;
+          }
+        }
+        if (!done) {
+          const double delta = __ddiv_rn(ev.jr, st_hess[p]);
+          st_u[p] = __dadd_rn(st_u[p], delta);
+          st_lastd[p] = delta;
+          st_prev[p] = r;
+          if (fabs(delta) < 1e-2) conv = done = true;  // kUpdateEpsilon
+          else if (it >= pp.max_it) done = true;
+        }
+      }
+      if (!done) {
+        list[cur ^ 1][atomicAdd(&counters[cur ^ 1], 1)] = (uint32_t)item;
+      } else if (conv) {
+        st_stage[p] = kConverged;
+        const int q2 = atomicAdd(&counters[cur ^ 1], nwin);
+        for (int kk = 0; kk < nwin; ++kk)
+          list[cur ^ 1][q2 + kk] = (uint32_t)(p * (nwin + 1) + kk + 1);
+      }
+    }
+    __syncthreads();
+    if (tid == 0) counters[cur] = 0;
+    cur ^= 1;
+    __syncthreads();
+  }
+
+  // ---- posterior, propagation, variance and the records (:268-299)
+  const long long rec0 = pair * (long long)g.nx * g.ny + (long long)ky0 * g.nx;
+  for (int p = tid; p < npb; p += nt) {
+    uint8_t stage = st_stage[p];
+    double u_out = 0.0, prob_out = 0.0, post_out = 0.0, sig_out = 0.0;
+    if (stage == kConverged) {
+      const double* res = st_wres + p * nwin;
+      const uint8_t* ok = st_wok + p * nwin;
+      int invalid = 0;
+      for (int q = 0; q < nwin; ++q) invalid += !ok[q];
+      bool accept = !(invalid > 1 || !ok[pp.wcenter]);
+      double sigma_r = 0.0, posterior = 0.0;
+      if (accept) {
+        // dynamic_sigma (src/window_posterior.cpp:42-59)
+        double ssum = 0.0;
+        int cnt = 0;
+        for (int q = 0; q < nwin; ++q) {
+          if (!ok[q]) continue;
+          ssum = __dadd_rn(ssum, res[q]);
+          ++cnt;
+        }
+        const double m = __ddiv_rn(ssum, (double)cnt);
+        double ss = 0.0;
+        for (int q = 0; q < nwin; ++q) {
+          if (!ok[q]) continue;
+          const double d = __dsub_rn(res[q], m);
+          ss = __dadd_rn(ss, __dmul_rn(d, d));
+        }
+        const double sd = __dsqrt_rn(__ddiv_rn(ss, (double)cnt));
+        sigma_r = (sd < 1e-4) ? 1e-4 : sd;
+        // window_priors + patch_posterior (:61-96)
+        const double denom = __dmul_rn(
+            __dmul_rn(__dmul_rn(__dmul_rn(2.0, sigma_r), sigma_r), (double)s), (double)s);
+        double psum = 0.0, pc = 0.0;
+        for (int q = 0; q < nwin; ++q) {
+          const double pr = ok[q] ? fast_exp(__ddiv_rn(-res[q], denom)) : 0.0;
+          psum = __dadd_rn(psum, pr);
+          if (q == pp.wcenter) pc = pr;
+        }
+        accept = !(psum <= 0.0);
+        if (accept) {
+          posterior = __ddiv_rn(pc, psum);
+          const double c = res[pp.wcenter];
+          for (int q = 0; q < nwin; ++q) {
+            if (q == pp.wcenter || !ok[q]) continue;
+            if (!(c < res[q])) {
+              accept = false;  // not a strict local minimum (:273)
+              break;
+            }
+          }
+        }
+        if (accept) {
+          const int kx = p % g.nx, ky = ky0 + p / g.nx;
+          const double cx = kx == g.nx - 1 ? g.cmax_x : __dadd_rn(g.c0, (double)kx * g.stride);
+          const double cy = ky == g.ny - 1 ? g.cmax_y : __dadd_rn(g.c0, (double)ky * g.stride);
+          double inherited = 0.0;
+          if (pp.have_prev) {
+            const int px = clampi(lround_i(__ddiv_rn(cx, 2.0)), 0, P.w - 1);
+            const int py = clampi(lround_i(__ddiv_rn(cy, 2.0)), 0, P.h - 1);
+            const Fused f = gather<true, false>(P, pair, px, py, pp.prev_mask);
+            if (!(f.sw <= 0.0)) inherited = __ddiv_rn(f.swp, f.sw);
+          }
+          double pr = __dadd_rn(inherited, __dmul_rn(L.level_w, posterior));
+          pr = (pr < 0.0) ? 0.0 : ((1.0 < pr) ? 1.0 : pr);
+          u_out = st_u[p];
+          prob_out = pr;
+          post_out = posterior;
+          if (pp.want_var) sig_out = variance_fit(pp.woff, nwin, pp.wcenter, res, ok, denom);
+          stage = kAccepted;
+        }
+      }
+    }
+    const long long rec = rec0 + p;
+    L.stage[rec] = stage;
+    L.u[rec] = u_out;
+    L.prob[rec] = prob_out;
+    L.post[rec] = post_out;
+    L.sigma[rec] = sig_out;
+  }
+}
+
+// ---------------------------------------------------------------------------
+
+BandPlan plan_bands(const Level& L, const PatchParams& pp, int max_smem_per_cta) {
+  const Grid& g = L.g;
+  BandPlan bp{};
+  const bool valid = !pp.all_valid;
+  bp.rpitch = (L.w + (L.w >> 4)) + 1;           // slots for x in [0, w]
+  bp.fpitch = (L.w - 1 + ((L.w - 1) >> 5)) + 1;  // slots for x in [0, w-1]
+  bp.bpitch = valid ? L.w : 0;
+  auto bytes_for = [&](int rb) {
+    const int rows = (rb - 1) * g.stride + g.size;
+    const int npb = rb * g.nx;
+    return band_layout(rows, bp.rpitch, bp.fpitch, bp.bpitch, npb, pp.nwin, valid).total;
+  };
+  // Largest band with <= 256 patches that still lets two CTAs share an SM.
+  const size_t two_per_sm = size_t(max_smem_per_cta) / 2 - 1024;
+  int rb = 1;
+  while (rb < g.ny && (rb + 1) * g.nx <= 256 && bytes_for(rb + 1) <= two_per_sm) ++rb;
+  bp.use_smem = bytes_for(rb) <= size_t(max_smem_per_cta);
+  bp.rb = rb;
+  bp.n_bands = (g.ny + rb - 1) / rb;
+  bp.npb = rb * g.nx;
+  bp.smem_rows = (rb - 1) * g.stride + g.size;
+  bp.smem_bytes = bp.use_smem ? bytes_for(rb)
+                              : band_layout(0, bp.rpitch, bp.fpitch, bp.bpitch, bp.npb, pp.nwin,
+                                            valid).total;
+  bp.threads = std::min(256, ((bp.npb + 31) / 32) * 32);
+  return bp;
+}
+
+template <int S, bool kSmem, bool kValid>
+static cudaError_t launch_t(const Level& L, const Level& P, const PatchParams& pp,
+                            const BandPlan& bp, cudaStream_t s) {
+  auto kern = k_patches<S, kSmem, kValid>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)bp.smem_bytes);
+  if (e != cudaSuccess) return e;
+  dim3 grid(bp.n_bands, pp.n_pairs);
+  kern<<<grid, bp.threads, bp.smem_bytes, s>>>(L, P, pp, bp);
+  return cudaGetLastError();
+}
+
+template <bool kSmem, bool kValid>
+static cudaError_t launch_s(const Level& L, const Level& P, const PatchParams& pp,
+                            const BandPlan& bp, cudaStream_t s) {
+  switch (L.g.size) {
+    case 8: return launch_t<8, kSmem, kValid>(L, P, pp, bp, s);
+    case 10: return launch_t<10, kSmem, kValid>(L, P, pp, bp, s);
+    case 12: return launch_t<12, kSmem, kValid>(L, P, pp, bp, s);
+    case 16: return launch_t<16, kSmem, kValid>(L, P, pp, bp, s);
+    default: return launch_t<0, kSmem, kValid>(L, P, pp, bp, s);
+  }
+}
+
+cudaError_t launch_patches(const Level& L, const Level& P, const PatchParams& pp,
+                           const BandPlan& bp, cudaStream_t s) {
+  const bool valid = !pp.all_valid;
+  if (bp.use_smem) return valid ? launch_s<true, true>(L, P, pp, bp, s)
+                                : launch_s<true, false>(L, P, pp, bp, s);
+  return valid ? launch_t<0, false, true>(L, P, pp, bp, s)
+               : launch_t<0, false, false>(L, P, pp, bp, s);
+}
+
+}  // namespace bdis
