@@ -184,6 +184,19 @@ int pstereo_gpu_set_profiling(pstereo_ctx* ctx, int enable);
 int pstereo_gpu_stage_times(pstereo_ctx* ctx, double* ms_total, int cap, int* n_calls);
 const char* pstereo_gpu_stage_name(const pstereo_ctx* ctx, int stage);
 
+/* ---- test hook ----
+ * eval_patch_residual (src/lk_solver.cpp:38-81) of size x size lattice
+ * patches with footprint origin (x0[q], y0[q]) at disparity u[q], on one
+ * width x height level, through the same device function k_patches uses.
+ * Host buffers; returns PSTEREO_OK or PSTEREO_EINTERNAL. Used by the parity
+ * tests to probe the evaluation at adversarial disparities. */
+int pstereo_debug_eval_residual(int device, int width, int height,
+                                const float* left, const uint8_t* left_valid,
+                                const float* right, const uint8_t* right_valid,
+                                int patch_size, int n_queries, const int* x0,
+                                const int* y0, const double* u, double* msq,
+                                double* jr, int* n);
+
 /* ---- deterministic synthetic pairs (BASELINE.json configs) ---- */
 typedef struct pstereo_synth_spec {
   int width, height, channels;

@@ -125,8 +125,36 @@ def lib() -> C.CDLL:
         L.pstereo_synth_pair.argtypes = [C.POINTER(SynthSpec), C.c_uint64, u8p, u8p, f32p]
         L.pstereo_synth_batch.argtypes = [C.POINTER(SynthSpec), C.c_int, C.c_uint64, u8p, u8p,
                                           C.c_int]
+        L.pstereo_debug_eval_residual.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p,
+                                                  C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
+                                                  C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                                                  C.c_void_p, C.c_void_p, C.c_void_p]
         _LIB = L
     return _LIB
+
+
+def debug_eval_residual(left, right, size, x0, y0, u, left_valid=None, right_valid=None,
+                        device=0):
+    """Test hook: (msq, jr, n) arrays of eval_patch_residual on the GPU."""
+    left = np.ascontiguousarray(left, np.float32)
+    right = np.ascontiguousarray(right, np.float32)
+    h, w = left.shape
+    x0 = np.ascontiguousarray(x0, np.int32)
+    y0 = np.ascontiguousarray(y0, np.int32)
+    u = np.ascontiguousarray(u, np.float64)
+    nq = len(u)
+    msq = np.zeros(nq, np.float64)
+    jr = np.zeros(nq, np.float64)
+    n = np.zeros(nq, np.int32)
+    lv = None if left_valid is None else np.ascontiguousarray(left_valid, np.uint8)
+    rv = None if right_valid is None else np.ascontiguousarray(right_valid, np.uint8)
+    rc = lib().pstereo_debug_eval_residual(
+        device, w, h, left.ctypes.data, None if lv is None else lv.ctypes.data, right.ctypes.data,
+        None if rv is None else rv.ctypes.data, size, nq, x0.ctypes.data, y0.ctypes.data,
+        u.ctypes.data, msq.ctypes.data, jr.ctypes.data, n.ctypes.data)
+    if rc:
+        raise GpuError("pstereo_debug_eval_residual failed")
+    return msq, jr, n
 
 
 # Exported symbols of include/pstereo_gpu.h (checked by tests/test_abi.py).
@@ -135,7 +163,7 @@ ABI_SYMBOLS = [
     "pstereo_gpu_destroy", "pstereo_gpu_last_error", "pstereo_gpu_match_u8",
     "pstereo_gpu_match_f32", "pstereo_gpu_last_launch_count", "pstereo_gpu_set_profiling",
     "pstereo_gpu_stage_times", "pstereo_gpu_stage_name", "pstereo_synth_default",
-    "pstereo_synth_pair", "pstereo_synth_batch",
+    "pstereo_synth_pair", "pstereo_synth_batch", "pstereo_debug_eval_residual",
 ]
 
 

@@ -811,3 +811,76 @@ int pstereo_gpu_match_f32(pstereo_ctx* ctx, int n_pairs, int width, int height,
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// test hook: one residual evaluation per query through the k_patches device
+// function (include/pstereo_gpu.h, pstereo_debug_eval_residual)
+
+extern "C" int pstereo_debug_eval_residual(int device, int width, int height, const float* left,
+                                           const uint8_t* left_valid, const float* right,
+                                           const uint8_t* right_valid, int patch_size,
+                                           int n_queries, const int* x0, const int* y0,
+                                           const double* u, double* msq, double* jr, int* n) {
+  if (width < 2 || height < 1 || patch_size < 1 || patch_size > PSTEREO_MAX_PATCH ||
+      n_queries < 0)
+    return PSTEREO_EINTERNAL;
+  for (int q = 0; q < n_queries; ++q)
+    if (x0[q] < 0 || y0[q] < 0 || x0[q] + patch_size > width || y0[q] + patch_size > height)
+      return PSTEREO_EINTERNAL;
+  if (cudaSetDevice(device) != cudaSuccess) return PSTEREO_EINTERNAL;
+  const size_t px = size_t(width) * height;
+  DevBuf<float> dl, dr, dg;
+  DevBuf<uint8_t> lv, rv, lq, rq;
+  DevBuf<double> rd, dq_u, d_msq, d_jr;
+  DevBuf<int> dqx, dqy, d_n;
+  const size_t nq = size_t(n_queries > 0 ? n_queries : 1);
+  bool ok = dl.ensure(px) == cudaSuccess && dr.ensure(px) == cudaSuccess &&
+            dg.ensure(px) == cudaSuccess && lv.ensure(px) == cudaSuccess &&
+            rv.ensure(px) == cudaSuccess && lq.ensure(px) == cudaSuccess &&
+            rq.ensure(px) == cudaSuccess && rd.ensure(size_t(width + 1) * height) == cudaSuccess &&
+            dq_u.ensure(nq) == cudaSuccess && d_msq.ensure(nq) == cudaSuccess &&
+            d_jr.ensure(nq) == cudaSuccess && dqx.ensure(nq) == cudaSuccess &&
+            dqy.ensure(nq) == cudaSuccess && d_n.ensure(nq) == cudaSuccess;
+  int rc = ok ? PSTEREO_OK : PSTEREO_EINTERNAL;
+  if (ok) {
+    cudaMemcpy(dl.p, left, px * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(dr.p, right, px * 4, cudaMemcpyHostToDevice);
+    if (left_valid) cudaMemcpy(lv.p, left_valid, px, cudaMemcpyHostToDevice);
+    else cudaMemset(lv.p, 1, px);
+    if (right_valid) cudaMemcpy(rv.p, right_valid, px, cudaMemcpyHostToDevice);
+    else cudaMemset(rv.p, 1, px);
+    cudaMemcpy(dqx.p, x0, size_t(n_queries) * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(dqy.p, y0, size_t(n_queries) * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(dq_u.p, u, size_t(n_queries) * 8, cudaMemcpyHostToDevice);
+    Level L;
+    std::memset(&L, 0, sizeof L);
+    L.w = width;
+    L.h = height;
+    L.plane = (long long)px;
+    L.left = dl.p;
+    L.right = dr.p;
+    L.lvalid = lv.p;
+    L.rvalid = rv.p;
+    L.grad = dg.p;
+    L.lq = lq.p;
+    L.rq = rq.p;
+    L.rd = rd.p;
+    launch_level_tables(L, 1, nullptr);
+    const int all_valid = left_valid == nullptr && right_valid == nullptr;
+    if (n_queries > 0 &&
+        launch_debug_eval(L, patch_size, all_valid, n_queries, dqx.p, dqy.p, dq_u.p, d_msq.p,
+                          d_jr.p, d_n.p, nullptr) != cudaSuccess)
+      rc = PSTEREO_EINTERNAL;
+    if (cudaDeviceSynchronize() != cudaSuccess) rc = PSTEREO_EINTERNAL;
+    if (rc == PSTEREO_OK && n_queries > 0) {
+      cudaMemcpy(msq, d_msq.p, size_t(n_queries) * 8, cudaMemcpyDeviceToHost);
+      cudaMemcpy(jr, d_jr.p, size_t(n_queries) * 8, cudaMemcpyDeviceToHost);
+      cudaMemcpy(n, d_n.p, size_t(n_queries) * 4, cudaMemcpyDeviceToHost);
+    }
+  }
+  for (auto* b : {&dl, &dr, &dg}) b->release();
+  for (auto* b : {&lv, &rv, &lq, &rq}) b->release();
+  for (auto* b : {&rd, &dq_u, &d_msq, &d_jr}) b->release();
+  for (auto* b : {&dqx, &dqy, &d_n}) b->release();
+  return rc;
+}

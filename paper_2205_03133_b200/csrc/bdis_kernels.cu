@@ -178,9 +178,13 @@ __device__ __forceinline__ void uf_union(Ptr lab, int* raw, int a, int b) {
   }
 }
 
+// Tile rows are warps (kTileW == 32): a pixel starts as the index of the first
+// pixel of its horizontal run (ballot bit tricks), then vertically adjacent
+// runs are merged with union-find (path halving) in shared memory.
 __global__ void __launch_bounds__(kTileW * kTileH) k_ccl_local(int w, int h, long long plane,
                                                              const uint8_t* __restrict__ mask,
                                                              int* __restrict__ lab) {
+  static_assert(kTileW == 32, "tile rows are warps");
   __shared__ int sl[kTileW * kTileH];
   const int tiles_x = (w + kTileW - 1) / kTileW;
   const int tx0 = (blockIdx.x % tiles_x) * kTileW, ty0 = (blockIdx.x / tiles_x) * kTileH;
@@ -188,12 +192,36 @@ __global__ void __launch_bounds__(kTileW * kTileH) k_ccl_local(int w, int h, lon
   const int x = tx0 + lx, y = ty0 + ly;
   const long long base = blockIdx.y * plane;
   const bool m = x < w && y < h && mask[base + (long long)y * w + x];
-  sl[t] = m ? t : -1;
+  const unsigned bits = __ballot_sync(0xffffffffu, m);
+  const unsigned starts = bits & ~(bits << 1);
+  const unsigned upto = starts & (0xffffffffu >> (31 - lx));  // run starts at lanes <= lx
+  sl[t] = m ? ly * kTileW + (31 - __clz(upto)) : -1;
   __syncthreads();
   volatile int* vl = sl;
-  if (m) {
-    if (lx > 0 && sl[t - 1] >= 0) uf_union(vl, sl, t, t - 1);
-    if (ly > 0 && sl[t - kTileW] >= 0) uf_union(vl, sl, t, t - kTileW);
+  // one union per vertically overlapping pixel pair; runs make chains short
+  if (m && ly > 0 && sl[t - kTileW] >= 0) {
+    int a = sl[t], b = sl[t - kTileW];
+    for (;;) {
+      while (vl[a] != a) {
+        const int g = vl[vl[a]];
+        vl[a] = g;
+        a = g;
+      }
+      while (vl[b] != b) {
+        const int g = vl[vl[b]];
+        vl[b] = g;
+        b = g;
+      }
+      if (a == b) break;
+      if (a < b) {
+        const int tmp = a;
+        a = b;
+        b = tmp;
+      }
+      const int old = atomicMin(&sl[a], b);
+      if (old == a) break;
+      a = old;
+    }
   }
   __syncthreads();
   if (m) {

@@ -138,6 +138,9 @@ void launch_fuse_finest(const Level& L, const FinestBufs& fb, const double* mask
                         int want_var, double threshold, int n_pairs, cudaStream_t s);
 void launch_ccl(int w, int h, long long plane, int full_w, int full_h, int e,
                 const uint8_t* mask, int* lab, int* area, int n_pairs, cudaStream_t s);
+cudaError_t launch_debug_eval(const Level& L, int size, int all_valid, int nq, const int* qx,
+                              const int* qy, const double* qu, double* msq, double* jr, int* n,
+                              cudaStream_t s);
 void launch_output(const OutputArgs& a, int f64, int n_pairs, cudaStream_t s);
 void launch_stats(const StatsArgs& a, int n_pairs, cudaStream_t s);
 

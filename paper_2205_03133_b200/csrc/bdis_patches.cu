@@ -48,6 +48,9 @@ struct Ev {
   int n;
 };
 
+// x in [0, 32 + w): at most {<1}, [1,2), [2,4), ... binades within 32 samples
+constexpr int kMaxSeg = 8;
+
 template <bool kSmem>
 struct Rows {
   const double* R;   // right view, fp64, rows of (w+1)
@@ -136,25 +139,75 @@ __device__ __forceinline__ Ev eval_patch(const Rows<kSmem>& rw, int w, int s_rt,
     ev.jr = jr;
     return ev;
   }
-  // General path: the literal per-sample arithmetic of sample_bilinear
-  // (inc/image.hpp:53-71) at integer rows -- bounds test, truncation, weight.
+  // Segment path (patch rows that leave the image or cross binades): the
+  // in-bounds samples [lo, hi] (x_i increases with i, so out-of-bounds samples
+  // -- invalid in sample_bilinear -- form a prefix and a suffix) split into
+  // runs whose x_i share a binade; within a run x_i = x_i0 + (i - i0) exactly
+  // (same argument as the fast path), so each run has one floor offset and
+  // one weight fx. Only a few x_i are probed per evaluation.
+  auto xat = [&](int i) { return __dsub_rn(__dadd_rn(xd0, (double)i), u); };
+  int lo, hi;
+  if (xf >= 0.0) {
+    lo = 0;
+  } else {
+    const double est = -xf;
+    lo = est >= (double)s ? s : __double2int_rz(est);
+    while (lo < s && xat(lo) < 0.0) ++lo;
+    while (lo > 0 && xat(lo - 1) >= 0.0) --lo;
+  }
+  if (xl <= wm1) {
+    hi = s - 1;
+  } else {
+    const double est = __dsub_rn(wm1, xf);
+    hi = !(est >= 0.0) ? -1 : (est >= (double)(s - 1) ? s - 1 : __double2int_rz(est));
+    while (hi >= 0 && xat(hi) > wm1) --hi;
+    while (hi + 1 < s && xat(hi + 1) <= wm1) ++hi;
+  }
+  if (!(xf == xf)) hi = -1;  // NaN disparity: every sample is outside the image
+  int seg_i0[kMaxSeg + 1], seg_base[kMaxSeg];
+  double seg_fx[kMaxSeg];
+  int ns = 0;
+  for (int i = lo; i <= hi && ns < kMaxSeg;) {
+    const double x = xat(i);
+    const int fl = __double2int_rz(x);
+    seg_i0[ns] = i;
+    seg_base[ns] = fl - i;
+    seg_fx[ns] = __dsub_rn(x, (double)fl);
+    ++ns;
+    if (x < 1.0) {  // only one sample can lie below 1
+      ++i;
+      continue;
+    }
+    const double B = __hiloint2double(((__double2hiint(x) >> 20) + 1) << 20, 0);  // next 2^k
+    const double d = __dsub_rn(B, x);                                              // exact
+    int k = d >= (double)(hi + 1 - i) ? hi + 1 : i + __double2int_rz(d);
+    if (k <= i) k = i + 1;
+    while (k <= hi && xat(k) < B) ++k;
+    while (k - 1 > i && xat(k - 1) >= B) --k;
+    i = k;
+  }
+  seg_i0[ns] = hi + 1;
 #pragma unroll 1
   for (int j = 0; j < s; ++j) {
     const double* rr = rw.R + (r0 + j) * rw.rp;
-    for (int i = 0; i < s; ++i) {
-      // (cx + offset(i)) - u with cx + offset(i) == x0 + i exactly
-      const double X = __dsub_rn(__dadd_rn(xd0, (double)i), u);
-      if (kValid && !rw.lq[(r0 + j) * rw.bp + x0 + i]) continue;
-      if (!(X >= 0.0 && X <= wm1)) continue;
-      const int xi = __double2int_rz(X);
-      if (kValid && !rw.rq[(r0 + j) * rw.bp + xi]) continue;
-      const double fx = __dsub_rn(X, (double)xi);
-      const double v = __dadd_rn(__dmul_rn(__dsub_rn(1.0, fx), rr[rw.s8(xi)]),
-                                 __dmul_rn(fx, rr[rw.s8(xi + 1)]));
-      sum = __dadd_rn(sum, v);
-      ++n;
+#pragma unroll 1
+    for (int gsg = 0; gsg < ns; ++gsg) {
+      const int base = seg_base[gsg];
+      const double fx = seg_fx[gsg], omf = __dsub_rn(1.0, fx);
+      double a = rr[rw.s8(base + seg_i0[gsg])];
+      for (int i = seg_i0[gsg]; i < seg_i0[gsg + 1]; ++i) {
+        const double b = rr[rw.s8(base + i + 1)];
+        const double v = __dadd_rn(__dmul_rn(omf, a), __dmul_rn(fx, b));
+        a = b;
+        if (kValid) {
+          if (!(rw.lq[(r0 + j) * rw.bp + x0 + i] && rw.rq[(r0 + j) * rw.bp + base + i])) continue;
+          ++n;
+        }
+        sum = __dadd_rn(sum, v);
+      }
     }
   }
+  if (!kValid) n = hi >= lo ? s * (hi - lo + 1) : 0;
   ev.n = n;
   ev.msq = CUDART_INF;
   if (n == 0) return ev;
@@ -165,19 +218,22 @@ __device__ __forceinline__ Ev eval_patch(const Rows<kSmem>& rw, int w, int s_rt,
     const double* rr = rw.R + (r0 + j) * rw.rp;
     const float* lr = rw.Lf + (r0 + j) * rw.fp;
     const float* gr = rw.Gf + (r0 + j) * rw.fp;
-    for (int i = 0; i < s; ++i) {
-      if (kValid && !rw.lq[(r0 + j) * rw.bp + x0 + i]) continue;
-      const double X = __dsub_rn(__dadd_rn(xd0, (double)i), u);
-      if (!(X >= 0.0 && X <= wm1)) continue;
-      const int xi = __double2int_rz(X);
-      if (kValid && !rw.rq[(r0 + j) * rw.bp + xi]) continue;
-      const double fx = __dsub_rn(X, (double)xi);
-      const double v = __dadd_rn(__dmul_rn(__dsub_rn(1.0, fx), rr[rw.s8(xi)]),
-                                 __dmul_rn(fx, rr[rw.s8(xi + 1)]));
-      const double t = __dsub_rn((double)lr[rw.s4(x0 + i)], mean);
-      const double r = __dsub_rn(__dsub_rn(v, rmean), t);
-      ssr = __dadd_rn(ssr, __dmul_rn(r, r));
-      jr = __dadd_rn(jr, __dmul_rn((double)gr[rw.s4(x0 + i)], r));
+#pragma unroll 1
+    for (int gsg = 0; gsg < ns; ++gsg) {
+      const int base = seg_base[gsg];
+      const double fx = seg_fx[gsg], omf = __dsub_rn(1.0, fx);
+      double a = rr[rw.s8(base + seg_i0[gsg])];
+      for (int i = seg_i0[gsg]; i < seg_i0[gsg + 1]; ++i) {
+        const double b = rr[rw.s8(base + i + 1)];
+        const double v = __dadd_rn(__dmul_rn(omf, a), __dmul_rn(fx, b));
+        a = b;
+        if (kValid && !(rw.lq[(r0 + j) * rw.bp + x0 + i] && rw.rq[(r0 + j) * rw.bp + base + i]))
+          continue;
+        const double t = __dsub_rn((double)lr[rw.s4(x0 + i)], mean);
+        const double r = __dsub_rn(__dsub_rn(v, rmean), t);
+        ssr = __dadd_rn(ssr, __dmul_rn(r, r));
+        jr = __dadd_rn(jr, __dmul_rn((double)gr[rw.s4(x0 + i)], r));
+      }
     }
   }
   ev.msq = __ddiv_rn(ssr, (double)n);
@@ -607,6 +663,52 @@ cudaError_t launch_patches(const Level& L, const Level& P, const PatchParams& pp
                                 : launch_s<true, false>(L, P, pp, bp, s);
   return valid ? launch_t<0, false, true>(L, P, pp, bp, s)
                : launch_t<0, false, false>(L, P, pp, bp, s);
+}
+
+// ---------------------------------------------------------------------------
+// Test hook: eval_patch_residual for arbitrary (x0, y0, u) queries on one level,
+// through exactly the device function k_patches uses (global-memory mode).
+template <bool kValid>
+__global__ void k_debug_eval(Level L, int size, int nq, const int* __restrict__ qx,
+                             const int* __restrict__ qy, const double* __restrict__ qu,
+                             double* __restrict__ msq, double* __restrict__ jr,
+                             int* __restrict__ n) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  Rows<false> rw;
+  rw.R = L.rd;
+  rw.Lf = L.left;
+  rw.Gf = L.grad;
+  rw.lq = L.lq;
+  rw.rq = L.rq;
+  rw.rp = L.w + 1;
+  rw.fp = L.w;
+  rw.bp = L.w;
+  const int x0 = qx[q], y0 = qy[q];
+  // template mean (extract_patch, src/patch.cpp:15-33)
+  double sum = 0.0;
+  int cnt = 0;
+  for (int j = 0; j < size; ++j)
+    for (int i = 0; i < size; ++i) {
+      if (kValid && !L.lq[(y0 + j) * L.w + x0 + i]) continue;
+      sum = __dadd_rn(sum, (double)L.left[(y0 + j) * L.w + x0 + i]);
+      ++cnt;
+    }
+  const double mean = cnt ? __ddiv_rn(sum, (double)cnt) : 0.0;
+  const Ev ev = eval_patch<0, false, kValid>(rw, L.w, size, x0, y0, (double)x0,
+                                             (double)(x0 + size - 1), mean, qu[q]);
+  msq[q] = ev.msq;
+  jr[q] = ev.jr;
+  n[q] = ev.n;
+}
+
+cudaError_t launch_debug_eval(const Level& L, int size, int all_valid, int nq, const int* qx,
+                              const int* qy, const double* qu, double* msq, double* jr, int* n,
+                              cudaStream_t s) {
+  const int t = 128;
+  if (all_valid) k_debug_eval<false><<<(nq + t - 1) / t, t, 0, s>>>(L, size, nq, qx, qy, qu, msq, jr, n);
+  else k_debug_eval<true><<<(nq + t - 1) / t, t, 0, s>>>(L, size, nq, qx, qy, qu, msq, jr, n);
+  return cudaGetLastError();
 }
 
 }  // namespace bdis

@@ -1,0 +1,22 @@
+"""Summarise an ncu --csv launch list (gpu__time_duration.sum) per kernel."""
+import collections
+import csv
+import sys
+
+rows = list(csv.reader(open(sys.argv[1])))
+hdr = None
+agg = collections.defaultdict(lambda: [0, 0.0])
+for r in rows:
+    if len(r) > 5 and r[0] == "ID":
+        hdr = r
+        continue
+    if hdr and len(r) == len(hdr):
+        d = dict(zip(hdr, r))
+        if d.get("Metric Name") == "gpu__time_duration.sum":
+            k = d["Kernel Name"].split("(")[0][:48]
+            agg[k][0] += 1
+            agg[k][1] += float(d["Metric Value"].replace(",", ""))
+tot = sum(t for _, t in agg.values())
+for k, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
+    print(f"{t / 1e3:10.1f} us  {100 * t / tot:5.1f}%  n={n:3d}  {k}")
+print(f"{tot / 1e3:10.1f} us total")

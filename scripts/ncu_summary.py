@@ -1,0 +1,39 @@
+"""Key metrics of an ncu --set full report (first kernel), for profiles/ notes."""
+import csv
+import io
+import subprocess
+import sys
+
+rep = sys.argv[1]
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                     text=True).stdout
+rows = list(csv.reader(io.StringIO(raw)))
+hdr, units, vals = rows[0], rows[1], rows[2]
+want = [
+    "Kernel Name", "gpu__time_duration.sum", "launch__grid_size", "launch__block_size",
+    "launch__registers_per_thread", "launch__shared_mem_per_block_dynamic",
+    "sm__warps_active.avg.pct_of_peak_sustained_active",
+    "smsp__thread_inst_executed_per_inst_executed.ratio",
+    "sm__inst_executed.sum", "smsp__issue_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+    "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum",
+    "dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_bytes.sum",
+    "smsp__average_warp_latency_issue_stalled_barrier",
+]
+for k in want:
+    for i, h in enumerate(hdr):
+        if h == k or h.endswith(k):
+            print(f"{h:70s} {vals[i]} {units[i]}")
+            break
+stalls = [(float(v.replace(",", "")), h) for h, v in zip(hdr, vals)
+          if h.startswith("smsp__pcsamp_warps_issue_stalled_") and not h.endswith("not_issued")
+          and v not in ("", "n/a")]
+tot = sum(s for s, _ in stalls) or 1
+print("stall samples (share):")
+for s, h in sorted(stalls, reverse=True)[:10]:
+    print(f"   {100 * s / tot:5.1f}%  {h.replace('smsp__pcsamp_warps_issue_stalled_', '')}")
