@@ -164,36 +164,50 @@ __device__ __forceinline__ Ev eval_patch(const Rows<kSmem>& rw, int w, int s_rt,
     while (hi + 1 < s && xat(hi + 1) <= wm1) ++hi;
   }
   if (!(xf == xf)) hi = -1;  // NaN disparity: every sample is outside the image
+  // segment table, fully unrolled so it stays in registers
   int seg_i0[kMaxSeg + 1], seg_base[kMaxSeg];
-  double seg_fx[kMaxSeg];
+  double seg_fx[kMaxSeg], seg_omf[kMaxSeg];
   int ns = 0;
-  for (int i = lo; i <= hi && ns < kMaxSeg;) {
-    const double x = xat(i);
-    const int fl = __double2int_rz(x);
-    seg_i0[ns] = i;
-    seg_base[ns] = fl - i;
-    seg_fx[ns] = __dsub_rn(x, (double)fl);
-    ++ns;
-    if (x < 1.0) {  // only one sample can lie below 1
-      ++i;
-      continue;
+  {
+    int i = lo;
+#pragma unroll
+    for (int g = 0; g < kMaxSeg; ++g) {
+      seg_i0[g] = i;
+      seg_base[g] = 0;
+      seg_fx[g] = 0.0;
+      seg_omf[g] = 1.0;
+      if (i <= hi) {
+        const double x = xat(i);
+        const int fl = __double2int_rz(x);
+        seg_base[g] = fl - i;
+        seg_fx[g] = __dsub_rn(x, (double)fl);
+        seg_omf[g] = __dsub_rn(1.0, seg_fx[g]);
+        ns = g + 1;
+        int k;
+        if (x < 1.0) {  // only one sample can lie below 1
+          k = i + 1;
+        } else {
+          // next power of two above x; d = B - x is exact (Sterbenz)
+          const double B = __hiloint2double(((__double2hiint(x) >> 20) + 1) << 20, 0);
+          const double d = __dsub_rn(B, x);
+          k = d >= (double)(hi + 1 - i) ? hi + 1 : i + __double2int_rz(d);
+          if (k <= i) k = i + 1;
+          while (k <= hi && xat(k) < B) ++k;
+          while (k - 1 > i && xat(k - 1) >= B) --k;
+        }
+        i = k;
+      }
     }
-    const double B = __hiloint2double(((__double2hiint(x) >> 20) + 1) << 20, 0);  // next 2^k
-    const double d = __dsub_rn(B, x);                                              // exact
-    int k = d >= (double)(hi + 1 - i) ? hi + 1 : i + __double2int_rz(d);
-    if (k <= i) k = i + 1;
-    while (k <= hi && xat(k) < B) ++k;
-    while (k - 1 > i && xat(k - 1) >= B) --k;
-    i = k;
+    seg_i0[kMaxSeg] = i;
   }
-  seg_i0[ns] = hi + 1;
 #pragma unroll 1
   for (int j = 0; j < s; ++j) {
     const double* rr = rw.R + (r0 + j) * rw.rp;
-#pragma unroll 1
-    for (int gsg = 0; gsg < ns; ++gsg) {
+#pragma unroll
+    for (int gsg = 0; gsg < kMaxSeg; ++gsg) {
+      if (gsg >= ns) break;
       const int base = seg_base[gsg];
-      const double fx = seg_fx[gsg], omf = __dsub_rn(1.0, fx);
+      const double fx = seg_fx[gsg], omf = seg_omf[gsg];
       double a = rr[rw.s8(base + seg_i0[gsg])];
       for (int i = seg_i0[gsg]; i < seg_i0[gsg + 1]; ++i) {
         const double b = rr[rw.s8(base + i + 1)];
@@ -218,10 +232,11 @@ __device__ __forceinline__ Ev eval_patch(const Rows<kSmem>& rw, int w, int s_rt,
     const double* rr = rw.R + (r0 + j) * rw.rp;
     const float* lr = rw.Lf + (r0 + j) * rw.fp;
     const float* gr = rw.Gf + (r0 + j) * rw.fp;
-#pragma unroll 1
-    for (int gsg = 0; gsg < ns; ++gsg) {
+#pragma unroll
+    for (int gsg = 0; gsg < kMaxSeg; ++gsg) {
+      if (gsg >= ns) break;
       const int base = seg_base[gsg];
-      const double fx = seg_fx[gsg], omf = __dsub_rn(1.0, fx);
+      const double fx = seg_fx[gsg], omf = seg_omf[gsg];
       double a = rr[rw.s8(base + seg_i0[gsg])];
       for (int i = seg_i0[gsg]; i < seg_i0[gsg + 1]; ++i) {
         const double b = rr[rw.s8(base + i + 1)];
@@ -344,7 +359,19 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
   uint8_t* st_stage = smem + lay.oStage;
   uint8_t* st_wok = smem + lay.oWok;
   uint32_t* list[2] = {(uint32_t*)(smem + lay.oList0), (uint32_t*)(smem + lay.oList1)};
-  int* counters = (int*)(smem + lay.oCounters);  // [0],[1]: list sizes
+  // two-ended work lists: items whose evaluation takes the fast path are
+  // appended at the front, the others at the back, so warps stay uniform
+  int* counters = (int*)(smem + lay.oCounters);  // [2*l]: front size, [2*l+1]: back size
+  const int cap = bp.npb * nwin;
+  auto fast_item = [&](int x0, double u) {
+    const double xf = __dsub_rn((double)x0, u), xl = __dsub_rn((double)(x0 + s - 1), u);
+    return xf >= 0.0 && xl <= (double)(w - 1) &&
+           (__double2hiint(xf) >> 20) == (__double2hiint(xl) >> 20);
+  };
+  auto push = [&](int l, uint32_t item, bool fast) {
+    if (fast) list[l][atomicAdd(&counters[2 * l], 1)] = item;
+    else list[l][cap - 1 - atomicAdd(&counters[2 * l + 1], 1)] = item;
+  };
 
   const long long pbase = pair * L.plane;
   Rows<kSmem> rw;
@@ -389,7 +416,7 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
     rw.bp = w;
     rofs = 0;
   }
-  if (tid < 2) counters[tid] = 0;
+  if (tid < 4) counters[tid] = 0;
   __syncthreads();
 
   // ---- setup: extract_patch + precompute_patch_system + u0 (:250-262)
@@ -450,8 +477,7 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
       st_iter[p] = 0;
       const double xc = __dsub_rn(cx, u);  // in_bounds(cx - u0, cy), lk_solver.cpp:89
       if (xc >= 0.0 && xc <= (double)(w - 1)) {
-        const int q = atomicAdd(&counters[0], 1);
-        list[0][q] = (uint32_t)(p * (nwin + 1));
+        push(0, (uint32_t)(p * (nwin + 1)), fast_item(kx == g.nx - 1 ? g.lastx0 : kx * g.stride, u));
       }
     }
     st_stage[p] = stage;
@@ -461,10 +487,11 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
   // ---- rounds of evaluation work items: (p, LK) and (p, window k)
   int cur = 0;
   for (;;) {
-    const int n_items = counters[cur];
+    const int n_front = counters[2 * cur];
+    const int n_items = n_front + counters[2 * cur + 1];
     if (n_items == 0) break;
     for (int q = tid; q < n_items; q += nt) {
-      const int item = list[cur][q];
+      const int item = q < n_front ? list[cur][q] : list[cur][cap - 1 - (q - n_front)];
       const int p = item / (nwin + 1), k = item % (nwin + 1) - 1;
       const int kx = p % g.nx, ky = ky0 + p / g.nx;
       const int x0 = kx == g.nx - 1 ? g.lastx0 : kx * g.stride;
@@ -507,16 +534,16 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
         }
       }
       if (!done) {
-        list[cur ^ 1][atomicAdd(&counters[cur ^ 1], 1)] = (uint32_t)item;
+        push(cur ^ 1, (uint32_t)item, fast_item(x0, st_u[p]));
       } else if (conv) {
         st_stage[p] = kConverged;
-        const int q2 = atomicAdd(&counters[cur ^ 1], nwin);
         for (int kk = 0; kk < nwin; ++kk)
-          list[cur ^ 1][q2 + kk] = (uint32_t)(p * (nwin + 1) + kk + 1);
+          push(cur ^ 1, (uint32_t)(p * (nwin + 1) + kk + 1),
+               fast_item(x0, __dadd_rn(st_u[p], pp.woff[kk])));
       }
     }
     __syncthreads();
-    if (tid == 0) counters[cur] = 0;
+    if (tid == 0) counters[2 * cur] = counters[2 * cur + 1] = 0;
     cur ^= 1;
     __syncthreads();
   }
