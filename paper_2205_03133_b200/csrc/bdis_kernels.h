@@ -43,9 +43,9 @@ struct BandPlan {
 // host planner and the kernel.
 struct BandLayout {
   size_t oR, oL, oG, oLQ, oRQ;
-  size_t oMean, oHess, oTmsq, oU, oPrev, oLastd, oWres;
-  size_t oCnt, oList0, oList1, oCounters;
-  size_t oIter, oStage, oWok;
+  size_t oMean, oHess, oTmsq, oU, oWres;
+  size_t oCnt, oPool, oCounters;
+  size_t oStage, oWok;
   size_t total;
 };
 
@@ -68,14 +68,10 @@ __host__ __device__ inline BandLayout band_layout(int rows, int rpitch, int fpit
   l.oHess = take(size_t(npb) * 8, 8);
   l.oTmsq = take(size_t(npb) * 8, 8);
   l.oU = take(size_t(npb) * 8, 8);
-  l.oPrev = take(size_t(npb) * 8, 8);
-  l.oLastd = take(size_t(npb) * 8, 8);
   l.oWres = take(size_t(npb) * nwin * 8, 8);
   l.oCnt = take(size_t(npb) * 4, 4);
-  l.oList0 = take(size_t(npb) * nwin * 4, 4);
-  l.oList1 = take(size_t(npb) * nwin * 4, 4);
+  l.oPool = take(size_t(npb) * 4, 4);
   l.oCounters = take(4 * 4, 4);
-  l.oIter = take(size_t(npb), 1);
   l.oStage = take(size_t(npb), 1);
   l.oWok = take(size_t(npb) * nwin, 1);
   l.total = (o + 15) / 16 * 16;

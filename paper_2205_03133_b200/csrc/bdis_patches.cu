@@ -11,24 +11,22 @@
 //     right view (fp64), left view and gradient (fp32) are staged in shared
 //     memory once, padded (x + x/16 for 8-byte, x + x/32 for 4-byte slots) so
 //     the stride-`stride` accesses of neighbouring patches hit distinct banks;
-//   * a thread owns a patch evaluation at a time and sums its samples in the
+//   * a thread owns one patch at a time and sums its samples in the
 //     reference's sequential row-major order -- that is what makes every sum
 //     bit-identical to the CPU (a warp tree reduction would reorder them);
-//   * the LK iterations and the window samples are scheduled as work items in
-//     rounds: after every round the still-active items are compacted, so the
-//     1..12 iteration spread between patches costs no idle lanes, and the
-//     window evaluations of a converged patch run in parallel in the next
-//     round;
-//   * per-evaluation constant-fraction fast path: for a lattice patch the
-//     right samples of one row are x_i = (x0 + i) - u. When x_first and
-//     x_last are inside [0, w-1] and share one binade, fl((x0+i) - u) =
-//     (x0+i) + c for one c (the integers x0+i are multiples of the binade's
-//     ulp, and round-to-nearest-even of (x0+i) + (-u) then only depends on
-//     -u), so floor(x_i) = floor(x_first) + i and the interpolation weight
-//     fx = x_i - floor(x_i) is the same double for every i. That removes the
-//     per-sample double->int->double conversions without changing a bit;
-//     every other evaluation falls back to the literal per-sample
-//     sample_bilinear arithmetic.
+//   * phases: (1) balanced setup of every band patch (extract, Hessian, u0
+//     gather from the coarser level's records); (2) persistent lanes: each
+//     lane runs one residual evaluation per loop trip for its current patch
+//     -- an LK iteration or one of the window samples -- and takes the next
+//     patch from the CTA's pool when it is done, so the 1..12 iteration spread
+//     between patches costs no lockstep waiting and there is no barrier until
+//     the pool is drained; (3) balanced finish (posterior, local-minimum test,
+//     inherited probability, variance fit, records);
+//   * the right-sample position x = (cx + offset(i)) - u of column i does not
+//     depend on the row, so each evaluation computes the exact per-column
+//     truncation x0_i and weight fx_i once (s conversions instead of s*s) and
+//     applies them to every row: the literal sample_bilinear arithmetic
+//     (inc/image.hpp:53-71) with no per-sample double<->int conversions.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -48,9 +46,6 @@ struct Ev {
   int n;
 };
 
-// x in [0, 32 + w): at most {<1}, [1,2), [2,4), ... binades within 32 samples
-constexpr int kMaxSeg = 8;
-
 template <bool kSmem>
 struct Rows {
   const double* R;   // right view, fp64, rows of (w+1)
@@ -64,166 +59,56 @@ struct Rows {
 };
 
 // eval_patch_residual (src/lk_solver.cpp:38-81) of a lattice patch whose
-// footprint starts at column x0 and row r0 of `rw`.
+// footprint starts at column x0 and row r0 of `rw`, at disparity u.
 template <int S, bool kSmem, bool kValid>
 __device__ __forceinline__ Ev eval_patch(const Rows<kSmem>& rw, int w, int s_rt, int x0, int r0,
-                                         double xd0, double xdl, double mean, double u) {
+                                         double mean, double u) {
+  constexpr int SA = S > 0 ? S : kMaxPatch;
   const int s = S > 0 ? S : s_rt;
-  const double xf = __dsub_rn(xd0, u);
-  const double xl = __dsub_rn(xdl, u);
   const double wm1 = (double)(w - 1);
-  const bool fast = xf >= 0.0 && xl <= wm1 &&
-                    (__double2hiint(xf) >> 20) == (__double2hiint(xl) >> 20);
-  double sum = 0.0;
+  const double xd0 = (double)x0;
+  // column table: sample_bilinear's clamp / truncation / weight per column
+  int cxi[SA];
+  double cfx[SA], comf[SA];
+  unsigned inb = 0, contig = 0;
+#pragma unroll
+  for (int i = 0; i < SA; ++i) {
+    if (S == 0 && i >= s) break;
+    const double X = __dsub_rn(__dadd_rn(xd0, (double)i), u);  // (cx + offset(i)) - u
+    const bool in = X >= 0.0 && X <= wm1;
+    const int xi = in ? __double2int_rz(X) : 0;
+    cxi[i] = xi;
+    cfx[i] = in ? __dsub_rn(X, (double)xi) : 0.0;
+    comf[i] = __dsub_rn(1.0, cfx[i]);
+    inb |= (unsigned)in << i;
+    if (i > 0 && xi == cxi[i - 1] + 1) contig |= 1u << i;  // tap reuse: a_i == b_{i-1}
+  }
   int n = 0;
-  Ev ev;
-  ev.jr = 0.0;
-  if (fast) {
-    const int base = __double2int_rz(xf);
-    const double fx = __dsub_rn(xf, (double)base);
-    const double omf = __dsub_rn(1.0, fx);
-    // pass 1: mean of the right samples over jointly valid pixels. Sample i
-    // reads taps (base+i, base+i+1); tap base+i+1 is sample i+1's first tap.
-#pragma unroll 1
-    for (int j = 0; j < s; ++j) {
-      const double* rr = rw.R + (r0 + j) * rw.rp;
-      double a = rr[rw.s8(base)];
-      auto body = [&](int i) {
-        const double b = rr[rw.s8(base + i + 1)];
-        const double v = __dadd_rn(__dmul_rn(omf, a), __dmul_rn(fx, b));
-        a = b;
-        if (kValid) {
-          if (!(rw.lq[(r0 + j) * rw.bp + x0 + i] && rw.rq[(r0 + j) * rw.bp + base + i])) return;
-          ++n;
-        }
-        sum = __dadd_rn(sum, v);
-      };
-      if (S > 0) {
-#pragma unroll
-        for (int i = 0; i < (S > 0 ? S : 1); ++i) body(i);
-      } else {
-        for (int i = 0; i < s; ++i) body(i);
-      }
-    }
-    if (!kValid) n = s * s;
-    ev.n = n;
-    ev.msq = CUDART_INF;
-    if (n == 0) return ev;
-    const double rmean = __ddiv_rn(sum, (double)n);
-    double ssr = 0.0, jr = 0.0;
-#pragma unroll 1
-    for (int j = 0; j < s; ++j) {
-      const double* rr = rw.R + (r0 + j) * rw.rp;
-      const float* lr = rw.Lf + (r0 + j) * rw.fp;
-      const float* gr = rw.Gf + (r0 + j) * rw.fp;
-      double a = rr[rw.s8(base)];
-      auto body = [&](int i) {
-        const double b = rr[rw.s8(base + i + 1)];
-        const double v = __dadd_rn(__dmul_rn(omf, a), __dmul_rn(fx, b));
-        a = b;
-        if (kValid && !(rw.lq[(r0 + j) * rw.bp + x0 + i] && rw.rq[(r0 + j) * rw.bp + base + i]))
-          return;
-        const double t = __dsub_rn((double)lr[rw.s4(x0 + i)], mean);
-        const double r = __dsub_rn(__dsub_rn(v, rmean), t);
-        ssr = __dadd_rn(ssr, __dmul_rn(r, r));
-        jr = __dadd_rn(jr, __dmul_rn((double)gr[rw.s4(x0 + i)], r));
-      };
-      if (S > 0) {
-#pragma unroll
-        for (int i = 0; i < (S > 0 ? S : 1); ++i) body(i);
-      } else {
-        for (int i = 0; i < s; ++i) body(i);
-      }
-    }
-    ev.msq = __ddiv_rn(ssr, (double)n);
-    ev.jr = jr;
-    return ev;
-  }
-  // Segment path (patch rows that leave the image or cross binades): the
-  // in-bounds samples [lo, hi] (x_i increases with i, so out-of-bounds samples
-  // -- invalid in sample_bilinear -- form a prefix and a suffix) split into
-  // runs whose x_i share a binade; within a run x_i = x_i0 + (i - i0) exactly
-  // (same argument as the fast path), so each run has one floor offset and
-  // one weight fx. Only a few x_i are probed per evaluation.
-  auto xat = [&](int i) { return __dsub_rn(__dadd_rn(xd0, (double)i), u); };
-  int lo, hi;
-  if (xf >= 0.0) {
-    lo = 0;
-  } else {
-    const double est = -xf;
-    lo = est >= (double)s ? s : __double2int_rz(est);
-    while (lo < s && xat(lo) < 0.0) ++lo;
-    while (lo > 0 && xat(lo - 1) >= 0.0) --lo;
-  }
-  if (xl <= wm1) {
-    hi = s - 1;
-  } else {
-    const double est = __dsub_rn(wm1, xf);
-    hi = !(est >= 0.0) ? -1 : (est >= (double)(s - 1) ? s - 1 : __double2int_rz(est));
-    while (hi >= 0 && xat(hi) > wm1) --hi;
-    while (hi + 1 < s && xat(hi + 1) <= wm1) ++hi;
-  }
-  if (!(xf == xf)) hi = -1;  // NaN disparity: every sample is outside the image
-  // segment table, fully unrolled so it stays in registers
-  int seg_i0[kMaxSeg + 1], seg_base[kMaxSeg];
-  double seg_fx[kMaxSeg], seg_omf[kMaxSeg];
-  int ns = 0;
-  {
-    int i = lo;
-#pragma unroll
-    for (int g = 0; g < kMaxSeg; ++g) {
-      seg_i0[g] = i;
-      seg_base[g] = 0;
-      seg_fx[g] = 0.0;
-      seg_omf[g] = 1.0;
-      if (i <= hi) {
-        const double x = xat(i);
-        const int fl = __double2int_rz(x);
-        seg_base[g] = fl - i;
-        seg_fx[g] = __dsub_rn(x, (double)fl);
-        seg_omf[g] = __dsub_rn(1.0, seg_fx[g]);
-        ns = g + 1;
-        int k;
-        if (x < 1.0) {  // only one sample can lie below 1
-          k = i + 1;
-        } else {
-          // next power of two above x; d = B - x is exact (Sterbenz)
-          const double B = __hiloint2double(((__double2hiint(x) >> 20) + 1) << 20, 0);
-          const double d = __dsub_rn(B, x);
-          k = d >= (double)(hi + 1 - i) ? hi + 1 : i + __double2int_rz(d);
-          if (k <= i) k = i + 1;
-          while (k <= hi && xat(k) < B) ++k;
-          while (k - 1 > i && xat(k - 1) >= B) --k;
-        }
-        i = k;
-      }
-    }
-    seg_i0[kMaxSeg] = i;
-  }
+  double sum = 0.0;
 #pragma unroll 1
   for (int j = 0; j < s; ++j) {
     const double* rr = rw.R + (r0 + j) * rw.rp;
+    double b = 0.0;
 #pragma unroll
-    for (int gsg = 0; gsg < kMaxSeg; ++gsg) {
-      if (gsg >= ns) break;
-      const int base = seg_base[gsg];
-      const double fx = seg_fx[gsg], omf = seg_omf[gsg];
-      double a = rr[rw.s8(base + seg_i0[gsg])];
-      for (int i = seg_i0[gsg]; i < seg_i0[gsg + 1]; ++i) {
-        const double b = rr[rw.s8(base + i + 1)];
-        const double v = __dadd_rn(__dmul_rn(omf, a), __dmul_rn(fx, b));
-        a = b;
-        if (kValid) {
-          if (!(rw.lq[(r0 + j) * rw.bp + x0 + i] && rw.rq[(r0 + j) * rw.bp + base + i])) continue;
-          ++n;
-        }
+    for (int i = 0; i < SA; ++i) {
+      if (S == 0 && i >= s) break;
+      const double a = (contig >> i) & 1u ? b : rr[rw.s8(cxi[i])];
+      b = rr[rw.s8(cxi[i] + 1)];
+      const double v = __dadd_rn(__dmul_rn(comf[i], a), __dmul_rn(cfx[i], b));
+      bool use = (inb >> i) & 1u;
+      if (kValid)
+        use = use && rw.lq[(r0 + j) * rw.bp + x0 + i] && rw.rq[(r0 + j) * rw.bp + cxi[i]];
+      if (use) {
         sum = __dadd_rn(sum, v);
+        if (kValid) ++n;
       }
     }
   }
-  if (!kValid) n = hi >= lo ? s * (hi - lo + 1) : 0;
+  if (!kValid) n = s * __popc(inb);
+  Ev ev;
   ev.n = n;
   ev.msq = CUDART_INF;
+  ev.jr = 0.0;
   if (n == 0) return ev;
   const double rmean = __ddiv_rn(sum, (double)n);
   double ssr = 0.0, jr = 0.0;
@@ -232,18 +117,17 @@ __device__ __forceinline__ Ev eval_patch(const Rows<kSmem>& rw, int w, int s_rt,
     const double* rr = rw.R + (r0 + j) * rw.rp;
     const float* lr = rw.Lf + (r0 + j) * rw.fp;
     const float* gr = rw.Gf + (r0 + j) * rw.fp;
+    double b = 0.0;
 #pragma unroll
-    for (int gsg = 0; gsg < kMaxSeg; ++gsg) {
-      if (gsg >= ns) break;
-      const int base = seg_base[gsg];
-      const double fx = seg_fx[gsg], omf = seg_omf[gsg];
-      double a = rr[rw.s8(base + seg_i0[gsg])];
-      for (int i = seg_i0[gsg]; i < seg_i0[gsg + 1]; ++i) {
-        const double b = rr[rw.s8(base + i + 1)];
-        const double v = __dadd_rn(__dmul_rn(omf, a), __dmul_rn(fx, b));
-        a = b;
-        if (kValid && !(rw.lq[(r0 + j) * rw.bp + x0 + i] && rw.rq[(r0 + j) * rw.bp + base + i]))
-          continue;
+    for (int i = 0; i < SA; ++i) {
+      if (S == 0 && i >= s) break;
+      const double a = (contig >> i) & 1u ? b : rr[rw.s8(cxi[i])];
+      b = rr[rw.s8(cxi[i] + 1)];
+      bool use = (inb >> i) & 1u;
+      if (kValid)
+        use = use && rw.lq[(r0 + j) * rw.bp + x0 + i] && rw.rq[(r0 + j) * rw.bp + cxi[i]];
+      if (use) {
+        const double v = __dadd_rn(__dmul_rn(comf[i], a), __dmul_rn(cfx[i], b));
         const double t = __dsub_rn((double)lr[rw.s4(x0 + i)], mean);
         const double r = __dsub_rn(__dsub_rn(v, rmean), t);
         ssr = __dadd_rn(ssr, __dmul_rn(r, r));
@@ -323,6 +207,7 @@ __device__ double variance_fit(const double* woff, int nwin, int wcenter, const 
 
 }  // namespace
 
+
 template <int S, bool kSmem, bool kValid>
 __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams pp, BandPlan bp) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -336,6 +221,7 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
   const int nwin = pp.nwin;
   const int tid = threadIdx.x, nt = blockDim.x;
   auto row_start = [&](int ky) { return ky == g.ny - 1 ? g.lasty0 : ky * g.stride; };
+  auto col_start = [&](int kx) { return kx == g.nx - 1 ? g.lastx0 : kx * g.stride; };
   const int ylo = row_start(ky0);
   const int nrows = row_start(ky1 - 1) + s - ylo;
 
@@ -351,36 +237,22 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
   double* st_hess = (double*)(smem + lay.oHess);
   double* st_tmsq = (double*)(smem + lay.oTmsq);
   double* st_u = (double*)(smem + lay.oU);
-  double* st_prev = (double*)(smem + lay.oPrev);
-  double* st_lastd = (double*)(smem + lay.oLastd);
   double* st_wres = (double*)(smem + lay.oWres);
   int* st_cnt = (int*)(smem + lay.oCnt);
-  uint8_t* st_iter = smem + lay.oIter;
+  int* pool = (int*)(smem + lay.oPool);
+  int* counters = (int*)(smem + lay.oCounters);  // [0]: pool size, [1]: next to take
   uint8_t* st_stage = smem + lay.oStage;
   uint8_t* st_wok = smem + lay.oWok;
-  uint32_t* list[2] = {(uint32_t*)(smem + lay.oList0), (uint32_t*)(smem + lay.oList1)};
-  // two-ended work lists: items whose evaluation takes the fast path are
-  // appended at the front, the others at the back, so warps stay uniform
-  int* counters = (int*)(smem + lay.oCounters);  // [2*l]: front size, [2*l+1]: back size
-  const int cap = bp.npb * nwin;
-  auto fast_item = [&](int x0, double u) {
-    const double xf = __dsub_rn((double)x0, u), xl = __dsub_rn((double)(x0 + s - 1), u);
-    return xf >= 0.0 && xl <= (double)(w - 1) &&
-           (__double2hiint(xf) >> 20) == (__double2hiint(xl) >> 20);
-  };
-  auto push = [&](int l, uint32_t item, bool fast) {
-    if (fast) list[l][atomicAdd(&counters[2 * l], 1)] = item;
-    else list[l][cap - 1 - atomicAdd(&counters[2 * l + 1], 1)] = item;
-  };
 
   const long long pbase = pair * L.plane;
   Rows<kSmem> rw;
-  int rofs;  // row index of image row y in rw: y - rofs
+  int rofs;  // row index of image row y in rw is y - rofs
   if (kSmem) {
     // ---- stage the band (coalesced global reads, padded shared writes)
     const double* gR = L.rd + pair * (long long)(w + 1) * h + (long long)ylo * (w + 1);
     for (int r = 0; r < nrows; ++r) {
-      for (int x = tid; x <= w; x += nt) sR[r * bp.rpitch + Rows<true>::s8(x)] = gR[(long long)r * (w + 1) + x];
+      for (int x = tid; x <= w; x += nt)
+        sR[r * bp.rpitch + Rows<true>::s8(x)] = gR[(long long)r * (w + 1) + x];
       const float* gl = L.left + pbase + (long long)(ylo + r) * w;
       const float* gg = L.grad + pbase + (long long)(ylo + r) * w;
       for (int x = tid; x < w; x += nt) {
@@ -416,13 +288,13 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
     rw.bp = w;
     rofs = 0;
   }
-  if (tid < 4) counters[tid] = 0;
+  if (tid < 2) counters[tid] = 0;
   __syncthreads();
 
-  // ---- setup: extract_patch + precompute_patch_system + u0 (:250-262)
+  // ---- phase 1: extract_patch + precompute_patch_system + u0 (:250-262)
   for (int p = tid; p < npb; p += nt) {
     const int kx = p % g.nx, ky = ky0 + p / g.nx;
-    const int x0 = kx == g.nx - 1 ? g.lastx0 : kx * g.stride;
+    const int x0 = col_start(kx);
     const int r0 = row_start(ky) - rofs;
     uint8_t stage = kSkipped;
     double sum = 0.0;
@@ -471,84 +343,89 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
       st_hess[p] = hess;
       st_tmsq[p] = __ddiv_rn(tsq, (double)count);
       st_u[p] = u;
-      st_prev[p] = CUDART_INF;
-      st_lastd[p] = 0.0;
       st_cnt[p] = count;
-      st_iter[p] = 0;
       const double xc = __dsub_rn(cx, u);  // in_bounds(cx - u0, cy), lk_solver.cpp:89
-      if (xc >= 0.0 && xc <= (double)(w - 1)) {
-        push(0, (uint32_t)(p * (nwin + 1)), fast_item(kx == g.nx - 1 ? g.lastx0 : kx * g.stride, u));
-      }
+      if (xc >= 0.0 && xc <= (double)(w - 1)) pool[atomicAdd(&counters[0], 1)] = p;
     }
     st_stage[p] = stage;
   }
   __syncthreads();
 
-  // ---- rounds of evaluation work items: (p, LK) and (p, window k)
-  int cur = 0;
-  for (;;) {
-    const int n_front = counters[2 * cur];
-    const int n_items = n_front + counters[2 * cur + 1];
-    if (n_items == 0) break;
-    for (int q = tid; q < n_items; q += nt) {
-      const int item = q < n_front ? list[cur][q] : list[cur][cap - 1 - (q - n_front)];
-      const int p = item / (nwin + 1), k = item % (nwin + 1) - 1;
-      const int kx = p % g.nx, ky = ky0 + p / g.nx;
-      const int x0 = kx == g.nx - 1 ? g.lastx0 : kx * g.stride;
-      const int r0 = row_start(ky) - rofs;
-      const double xd0 = (double)x0, xdl = (double)(x0 + s - 1);
-      const double u = k < 0 ? st_u[p] : __dadd_rn(st_u[p], pp.woff[k]);
-      const Ev ev = eval_patch<S, kSmem, kValid>(rw, w, s, x0, r0, xd0, xdl, st_mean[p], u);
+  // ---- phase 2: persistent lanes, one residual evaluation per loop trip
+  {
+    const int n_pool = counters[0];
+    auto take = [&]() {
+      const int q = atomicAdd(&counters[1], 1);
+      return q < n_pool ? pool[q] : -1;
+    };
+    int p = take();
+    int k = -1, it = 0, x0 = 0, r0 = 0;
+    double u = 0.0, prev = CUDART_INF, lastd = 0.0, mean = 0.0;
+    auto start = [&](int np) {
+      p = np;
+      if (p < 0) return;
+      x0 = col_start(p % g.nx);
+      r0 = row_start(ky0 + p / g.nx) - rofs;
+      u = st_u[p];
+      mean = st_mean[p];
+      k = -1;
+      it = 0;
+      prev = CUDART_INF;
+      lastd = 0.0;
+    };
+    start(p);
+    while (p >= 0) {
+      const double uu = k < 0 ? u : __dadd_rn(u, pp.woff[k]);
+      const Ev ev = eval_patch<S, kSmem, kValid>(rw, w, s, x0, r0, mean, uu);
+      bool next = false;
       if (k >= 0) {
         // sample_window: valid iff every template pixel was sampled (:31-36)
         st_wres[p * nwin + k] = ev.msq;
         st_wok[p * nwin + k] = ev.n == st_cnt[p];
-        continue;
-      }
-      // one iteration of solve_patch_disparity (src/lk_solver.cpp:96-127)
-      const int it = st_iter[p] + 1;
-      st_iter[p] = (uint8_t)it;
-      bool done = false, conv = false;
-      if (ev.n == 0) {
-        done = true;
+        next = ++k == nwin;
       } else {
-        const double r = ev.msq;
-        const double prev = st_prev[p];
-        if (it >= pp.min_it) {
-          if (r < pp.stop_good) {
-            conv = done = true;
-          } else if (r > __dmul_rn(pp.stop_bad, st_tmsq[p])) {
-            done = true;
-          } else if (isfinite(prev) && __dsub_rn(prev, r) < __dmul_rn(pp.stop_improve, prev)) {
-            conv = it > 1 && fabs(st_lastd[p]) < 1e-2;
-            done = true;
+        // one iteration of solve_patch_disparity (src/lk_solver.cpp:96-127)
+        ++it;
+        bool done = false, conv = false;
+        if (ev.n == 0) {
+          done = true;
+        } else {
+          const double r = ev.msq;
+          if (it >= pp.min_it) {
+            if (r < pp.stop_good) {
+              conv = done = true;
+            } else if (r > __dmul_rn(pp.stop_bad, st_tmsq[p])) {
+              done = true;
+            } else if (isfinite(prev) && __dsub_rn(prev, r) < __dmul_rn(pp.stop_improve, prev)) {
+              conv = it > 1 && fabs(lastd) < 1e-2;
+              done = true;
+            }
+          }
+          if (!done) {
+            const double delta = __ddiv_rn(ev.jr, st_hess[p]);
+            u = __dadd_rn(u, delta);
+            lastd = delta;
+            prev = r;
+            if (fabs(delta) < 1e-2) conv = done = true;  // kUpdateEpsilon
+            else if (it >= pp.max_it) done = true;
           }
         }
-        if (!done) {
-          const double delta = __ddiv_rn(ev.jr, st_hess[p]);
-          st_u[p] = __dadd_rn(st_u[p], delta);
-          st_lastd[p] = delta;
-          st_prev[p] = r;
-          if (fabs(delta) < 1e-2) conv = done = true;  // kUpdateEpsilon
-          else if (it >= pp.max_it) done = true;
+        if (done) {
+          if (conv) {
+            st_stage[p] = kConverged;
+            st_u[p] = u;
+            k = 0;  // window samples next
+          } else {
+            next = true;
+          }
         }
       }
-      if (!done) {
-        push(cur ^ 1, (uint32_t)item, fast_item(x0, st_u[p]));
-      } else if (conv) {
-        st_stage[p] = kConverged;
-        for (int kk = 0; kk < nwin; ++kk)
-          push(cur ^ 1, (uint32_t)(p * (nwin + 1) + kk + 1),
-               fast_item(x0, __dadd_rn(st_u[p], pp.woff[kk])));
-      }
+      if (next) start(take());
     }
-    __syncthreads();
-    if (tid == 0) counters[2 * cur] = counters[2 * cur + 1] = 0;
-    cur ^= 1;
-    __syncthreads();
   }
+  __syncthreads();
 
-  // ---- posterior, propagation, variance and the records (:268-299)
+  // ---- phase 3: posterior, propagation, variance and the records (:268-299)
   const long long rec0 = pair * (long long)g.nx * g.ny + (long long)ky0 * g.nx;
   for (int p = tid; p < npb; p += nt) {
     uint8_t stage = st_stage[p];
@@ -640,13 +517,13 @@ BandPlan plan_bands(const Level& L, const PatchParams& pp, int max_smem_per_cta)
   bp.bpitch = valid ? L.w : 0;
   auto bytes_for = [&](int rb) {
     const int rows = (rb - 1) * g.stride + g.size;
-    const int npb = rb * g.nx;
-    return band_layout(rows, bp.rpitch, bp.fpitch, bp.bpitch, npb, pp.nwin, valid).total;
+    return band_layout(rows, bp.rpitch, bp.fpitch, bp.bpitch, rb * g.nx, pp.nwin, valid).total;
   };
-  // Largest band with <= 256 patches that still lets two CTAs share an SM.
+  // ~1.5 patches per lane of a 128-thread CTA, while two CTAs fit an SM
+  const int threads = 128;
   const size_t two_per_sm = size_t(max_smem_per_cta) / 2 - 1024;
-  int rb = 1;
-  while (rb < g.ny && (rb + 1) * g.nx <= 256 && bytes_for(rb + 1) <= two_per_sm) ++rb;
+  int rb = std::max(1, std::min(g.ny, (3 * threads / 2 + g.nx / 2) / g.nx));
+  while (rb > 1 && bytes_for(rb) > two_per_sm) --rb;
   bp.use_smem = bytes_for(rb) <= size_t(max_smem_per_cta);
   bp.rb = rb;
   bp.n_bands = (g.ny + rb - 1) / rb;
@@ -655,7 +532,7 @@ BandPlan plan_bands(const Level& L, const PatchParams& pp, int max_smem_per_cta)
   bp.smem_bytes = bp.use_smem ? bytes_for(rb)
                               : band_layout(0, bp.rpitch, bp.fpitch, bp.bpitch, bp.npb, pp.nwin,
                                             valid).total;
-  bp.threads = std::min(256, ((bp.npb + 31) / 32) * 32);
+  bp.threads = std::min(threads, std::max(32, ((bp.npb + 31) / 32) * 32));
   return bp;
 }
 
@@ -722,8 +599,7 @@ __global__ void k_debug_eval(Level L, int size, int nq, const int* __restrict__ 
       ++cnt;
     }
   const double mean = cnt ? __ddiv_rn(sum, (double)cnt) : 0.0;
-  const Ev ev = eval_patch<0, false, kValid>(rw, L.w, size, x0, y0, (double)x0,
-                                             (double)(x0 + size - 1), mean, qu[q]);
+  const Ev ev = eval_patch<0, false, kValid>(rw, L.w, size, x0, y0, mean, qu[q]);
   msq[q] = ev.msq;
   jr[q] = ev.jr;
   n[q] = ev.n;
@@ -737,5 +613,6 @@ cudaError_t launch_debug_eval(const Level& L, int size, int all_valid, int nq, c
   else k_debug_eval<true><<<(nq + t - 1) / t, t, 0, s>>>(L, size, nq, qx, qy, qu, msq, jr, n);
   return cudaGetLastError();
 }
+
 
 }  // namespace bdis
