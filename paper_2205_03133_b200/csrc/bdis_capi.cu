@@ -138,7 +138,7 @@ struct DevBuf {
 struct LevelBufs {
   DevBuf<float> left, right, grad;
   DevBuf<uint8_t> lvalid, rvalid, lq, rq, stage;
-  DevBuf<double> rd;
+  DevBuf<float> rpad;
   DevBuf<double> u, prob, post, sigma;
 };
 
@@ -372,7 +372,7 @@ void pstereo_gpu_destroy(pstereo_ctx* ctx) {
     L.lq.release();
     L.rq.release();
     L.stage.release();
-    L.rd.release();
+    L.rpad.release();
     L.u.release();
     L.prob.release();
     L.post.release();
@@ -494,59 +494,65 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
   const long long n_full = (long long)W * H;
   const long long npx = n_full * n;
 
-  // ---- inputs -> full-resolution fp32 planes
-  for (int v = 0; v < 2; ++v) {
-    CK(ctx->full[v].ensure(size_t(npx)));
-    CK(ctx->full_valid[v].ensure(size_t(npx)));
-  }
-  if (left_u8) {
-    const size_t bytes = size_t(npx) * channels;
-    const uint8_t* src[2] = {left_u8, right_u8};
-    for (int v = 0; v < 2; ++v) {
-      if (!inputs_on_device) {
-        CK(ctx->in_u8[v].ensure(bytes));
-        CK(cudaMemcpyAsync(ctx->in_u8[v].p, src[v], bytes, cudaMemcpyHostToDevice, s));
-        src[v] = ctx->in_u8[v].p;
-      }
-    }
-    CK(mark());
-    for (int v = 0; v < 2; ++v) {
-      launch_gray_u8(src[v], channels, npx, ctx->full[v].p, ctx->full_valid[v].p, s);
-      ++ctx->launches;
-    }
-  } else {
-    const float* fsrc[2] = {left_f, right_f};
-    const uint8_t* vsrc[2] = {left_v, right_v};
-    const cudaMemcpyKind kind = inputs_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-    for (int v = 0; v < 2; ++v) {
-      CK(cudaMemcpyAsync(ctx->full[v].p, fsrc[v], size_t(npx) * sizeof(float), kind, s));
-      if (vsrc[v]) CK(cudaMemcpyAsync(ctx->full_valid[v].p, vsrc[v], size_t(npx), kind, s));
-      else CK(cudaMemsetAsync(ctx->full_valid[v].p, 1, size_t(npx), s));
-    }
-    CK(mark());
-  }
-
-  // ---- pyramid cascade (src/pyramid.cpp:59-81)
+  // every input pixel is valid for gray/RGB rasters and for float planes
+  // without masks: the fused pyramid applies and the patch kernel skips the
+  // 4-tap validity tests
+  const bool all_valid = left_u8 ? (channels != 4) : (left_v == nullptr && right_v == nullptr);
   std::vector<int> ws(ce + 1), hs(ce + 1);
   ws[0] = W;
   hs[0] = H;
   for (int e = 1; e <= ce; ++e) {
     ws[e] = (ws[e - 1] + 1) / 2;
     hs[e] = (hs[e - 1] + 1) / 2;
-    LevelBufs& B = ctx->levels[e];
-    const size_t np = size_t(ws[e]) * hs[e] * n;
-    CK(B.left.ensure(np));
-    CK(B.right.ensure(np));
-    CK(B.lvalid.ensure(np));
-    CK(B.rvalid.ensure(np));
-    const float* sl = e == 1 ? ctx->full[0].p : ctx->levels[e - 1].left.p;
-    const float* sr = e == 1 ? ctx->full[1].p : ctx->levels[e - 1].right.p;
-    const uint8_t* slv = e == 1 ? ctx->full_valid[0].p : ctx->levels[e - 1].lvalid.p;
-    const uint8_t* srv = e == 1 ? ctx->full_valid[1].p : ctx->levels[e - 1].rvalid.p;
-    launch_downsample(sl, slv, sr, srv, ws[e - 1], hs[e - 1], B.left.p, B.lvalid.p, B.right.p,
-                      B.rvalid.p, ws[e], hs[e], n, s);
-    ++ctx->launches;
   }
+  PyrArgs pa;
+  std::memset(&pa, 0, sizeof pa);
+  pa.n_pairs = n;
+  pa.W = W;
+  pa.H = H;
+  pa.C = channels;
+  pa.ce = ce;
+  pa.fe = fe;
+  for (int e = 0; e <= ce; ++e) {
+    pa.ws[e] = ws[e];
+    pa.hs[e] = hs[e];
+  }
+  pa.buf_floats = ce >= 1 ? (1 << (ce - 1)) * ws[1] : 0;
+  const bool fused = all_valid && pyramid_smem_bytes(pa) <= size_t(ctx->max_smem);
+
+  // ---- inputs
+  const uint8_t* src_u8[2] = {left_u8, right_u8};
+  if (left_u8) {
+    const size_t bytes = size_t(npx) * channels;
+    for (int v = 0; v < 2; ++v) {
+      if (!inputs_on_device) {
+        CK(ctx->in_u8[v].ensure(bytes));
+        CK(cudaMemcpyAsync(ctx->in_u8[v].p, src_u8[v], bytes, cudaMemcpyHostToDevice, s));
+        src_u8[v] = ctx->in_u8[v].p;
+      }
+    }
+  }
+  if (!left_u8 || !fused) {
+    for (int v = 0; v < 2; ++v) {
+      CK(ctx->full[v].ensure(size_t(npx)));
+      CK(ctx->full_valid[v].ensure(size_t(npx)));
+    }
+  }
+  if (!left_u8) {
+    const float* fsrc[2] = {left_f, right_f};
+    const uint8_t* vsrc[2] = {left_v, right_v};
+    const cudaMemcpyKind kind = inputs_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    for (int v = 0; v < 2; ++v) {
+      CK(cudaMemcpyAsync(ctx->full[v].p, fsrc[v], size_t(npx) * sizeof(float), kind, s));
+      if (!fused) {
+        if (vsrc[v]) CK(cudaMemcpyAsync(ctx->full_valid[v].p, vsrc[v], size_t(npx), kind, s));
+        else CK(cudaMemsetAsync(ctx->full_valid[v].p, 1, size_t(npx), s));
+      }
+    }
+  }
+  CK(mark());
+
+  // ---- pyramid (src/pyramid.cpp:44-96) and per-level tables
   std::vector<Level> lv(geo.size());
   for (size_t li = 0; li < geo.size(); ++li) {
     const LevelGeom& G = geo[li];
@@ -558,21 +564,23 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
     L.h = G.h;
     L.plane = (long long)G.w * G.h;
     const size_t np = size_t(L.plane) * n;
-    if (G.e == 0) {
+    CK(B.grad.ensure(np));
+    CK(B.rpad.ensure(size_t(G.w + 1) * G.h * n));
+    if (G.e == 0 && !fused) {
       L.left = ctx->full[0].p;
       L.right = ctx->full[1].p;
       L.lvalid = ctx->full_valid[0].p;
       L.rvalid = ctx->full_valid[1].p;
     } else {
+      CK(B.left.ensure(np));
       L.left = B.left.p;
-      L.right = B.right.p;
-      L.lvalid = B.lvalid.p;
-      L.rvalid = B.rvalid.p;
     }
-    CK(B.grad.ensure(np));
-    CK(B.lq.ensure(np));
-    CK(B.rq.ensure(np));
-    CK(B.rd.ensure(size_t(G.w + 1) * G.h * n));
+    if (!fused) {
+      CK(B.lq.ensure(np));
+      CK(B.rq.ensure(np));
+      L.lq = B.lq.p;
+      L.rq = B.rq.p;
+    }
     const size_t nrec = size_t(G.g.nx) * G.g.ny * n;
     CK(B.stage.ensure(nrec));
     CK(B.u.ensure(nrec));
@@ -580,9 +588,7 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
     CK(B.post.ensure(nrec));
     CK(B.sigma.ensure(nrec));
     L.grad = B.grad.p;
-    L.lq = B.lq.p;
-    L.rq = B.rq.p;
-    L.rd = B.rd.p;
+    L.rpad = B.rpad.p;
     L.g = G.g;
     L.u = B.u.p;
     L.prob = B.prob.p;
@@ -590,8 +596,52 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
     L.sigma = B.sigma.p;
     L.stage = B.stage.p;
     L.level_w = G.level_w;
-    launch_level_tables(L, n, s);
+    pa.L[G.e] = B.left.p;
+    pa.G[G.e] = B.grad.p;
+    pa.Rp[G.e] = B.rpad.p;
+  }
+  if (fused) {
+    pa.u8l = src_u8[0];
+    pa.u8r = src_u8[1];
+    pa.f0l = left_u8 ? nullptr : ctx->full[0].p;
+    pa.f0r = left_u8 ? nullptr : ctx->full[1].p;
+    CK(launch_pyramid(pa, left_u8 != nullptr, s));
     ++ctx->launches;
+  } else {
+    // general path (masked inputs): grayscale, cascade, then the tables
+    if (left_u8) {
+      for (int v = 0; v < 2; ++v) {
+        launch_gray_u8(src_u8[v], channels, npx, ctx->full[v].p, ctx->full_valid[v].p, s);
+        ++ctx->launches;
+      }
+    }
+    for (int e = 1; e <= ce; ++e) {
+      LevelBufs& B = ctx->levels[e];
+      const size_t np = size_t(ws[e]) * hs[e] * n;
+      CK(B.left.ensure(np));
+      CK(B.right.ensure(np));
+      CK(B.lvalid.ensure(np));
+      CK(B.rvalid.ensure(np));
+      const float* sl = e == 1 ? ctx->full[0].p : ctx->levels[e - 1].left.p;
+      const float* sr = e == 1 ? ctx->full[1].p : ctx->levels[e - 1].right.p;
+      const uint8_t* slv = e == 1 ? ctx->full_valid[0].p : ctx->levels[e - 1].lvalid.p;
+      const uint8_t* srv = e == 1 ? ctx->full_valid[1].p : ctx->levels[e - 1].rvalid.p;
+      launch_downsample(sl, slv, sr, srv, ws[e - 1], hs[e - 1], B.left.p, B.lvalid.p, B.right.p,
+                        B.rvalid.p, ws[e], hs[e], n, s);
+      ++ctx->launches;
+    }
+    for (size_t li = 0; li < geo.size(); ++li) {
+      Level& L = lv[li];
+      if (L.e != 0) {
+        LevelBufs& B = ctx->levels[L.e];
+        L.left = B.left.p;
+        L.right = B.right.p;
+        L.lvalid = B.lvalid.p;
+        L.rvalid = B.rvalid.p;
+      }
+      launch_level_tables(L, n, s);
+      ++ctx->launches;
+    }
   }
   CK(mark());
 
@@ -610,9 +660,7 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
   pp.wcenter = ctx->wcenter;
   for (int q = 0; q < ctx->nwin; ++q) pp.woff[q] = ctx->woff[q];
   pp.prev_mask = ctx->mask.p;
-  // every input pixel is valid for gray/RGB rasters and for float planes
-  // without masks: the kernels then skip the 4-tap validity tests
-  pp.all_valid = left_u8 ? (channels != 4) : (left_v == nullptr && right_v == nullptr);
+  pp.all_valid = all_valid;
   for (size_t li = 0; li < lv.size(); ++li) {
     pp.want_var = prm.estimate_variance && lv[li].e == fe;
     pp.have_prev = li > 0;
@@ -831,7 +879,8 @@ extern "C" int pstereo_debug_eval_residual(int device, int width, int height, co
   const size_t px = size_t(width) * height;
   DevBuf<float> dl, dr, dg;
   DevBuf<uint8_t> lv, rv, lq, rq;
-  DevBuf<double> rd, dq_u, d_msq, d_jr;
+  DevBuf<float> rd;
+  DevBuf<double> dq_u, d_msq, d_jr;
   DevBuf<int> dqx, dqy, d_n;
   const size_t nq = size_t(n_queries > 0 ? n_queries : 1);
   bool ok = dl.ensure(px) == cudaSuccess && dr.ensure(px) == cudaSuccess &&
@@ -864,7 +913,7 @@ extern "C" int pstereo_debug_eval_residual(int device, int width, int height, co
     L.grad = dg.p;
     L.lq = lq.p;
     L.rq = rq.p;
-    L.rd = rd.p;
+    L.rpad = rd.p;
     launch_level_tables(L, 1, nullptr);
     const int all_valid = left_valid == nullptr && right_valid == nullptr;
     if (n_queries > 0 &&
@@ -880,7 +929,8 @@ extern "C" int pstereo_debug_eval_residual(int device, int width, int height, co
   }
   for (auto* b : {&dl, &dr, &dg}) b->release();
   for (auto* b : {&lv, &rv, &lq, &rq}) b->release();
-  for (auto* b : {&rd, &dq_u, &d_msq, &d_jr}) b->release();
+  rd.release();
+  for (auto* b : {&dq_u, &d_msq, &d_jr}) b->release();
   for (auto* b : {&dqx, &dqy, &d_n}) b->release();
   return rc;
 }

@@ -36,7 +36,7 @@ struct Level {
   float* grad;     // gradient_x of left (src/pyramid.cpp:30-42)
   uint8_t* lq;     // 4-tap validity of left at (x,y) (inc/image.hpp:68-69)
   uint8_t* rq;     // 4-tap validity of right at (x,y)
-  double* rd;      // right view as double, rows of w+1 (rd[w] = rd[w-1]: the
+  float* rpad;     // right view, rows of w+1 (rpad[w] = rpad[w-1]: the
                    // x1 = min(x0+1, w-1) clamp of inc/image.hpp:60)
   Grid g;
   // per-patch records [pair][ny][nx] (PatchEstimate, inc/coarse_to_fine.hpp:39-47)

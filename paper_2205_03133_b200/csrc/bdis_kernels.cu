@@ -105,9 +105,148 @@ __global__ void k_level_tables(Level L) {
   L.lq[base + i] = (lv[p00] && lv[p10] && lv[p01] && lv[p11]) ? 1 : 0;
   L.rq[base + i] = (rv[p00] && rv[p10] && rv[p01] && rv[p11]) ? 1 : 0;
   const float* r = L.right + base;
-  double* rd = L.rd + blockIdx.y * (long long)(w + 1) * h + (long long)y * (w + 1);
-  rd[x] = (double)r[p00];
-  if (x == w - 1) rd[w] = (double)r[p00];
+  float* rp = L.rpad + blockIdx.y * (long long)(w + 1) * h + (long long)y * (w + 1);
+  rp[x] = r[p00];
+  if (x == w - 1) rp[w] = r[p00];
+}
+
+// Fused pyramid for fully valid inputs: one CTA per (row of the coarsest
+// level, pair) builds every level's rows of that band -- to_grayscale on the
+// fly from the uint8 raster (or the fp32 plane), then the cascade of
+// downsample_half (src/pyramid.cpp:9-28, same ceil dims and edge clamps at
+// every level) in shared memory -- and writes, for each stored level, the left
+// view, its gradient_x (src/pyramid.cpp:30-42) and the padded right view.
+// Replaces k_gray_u8 + k_downsample + k_level_tables: the full-resolution fp32
+// planes never touch HBM.
+template <bool kU8>
+__device__ __forceinline__ float src_px(const PyrArgs& a, int view, long long pair, int x,
+                                        int y) {
+  const long long i = pair * (long long)a.W * a.H + (long long)y * a.W + x;
+  if (kU8) {
+    const uint8_t* p = (view ? a.u8r : a.u8l) + i * a.C;
+    const double inv255 = 1.0 / 255.0;
+    if (a.C == 1) return __double2float_rn(__dmul_rn((double)p[0], inv255));
+    const double s = __dadd_rn(__dadd_rn(__dmul_rn(0.299, (double)p[0]), __dmul_rn(0.587, (double)p[1])),
+                               __dmul_rn(0.114, (double)p[2]));
+    return __double2float_rn(__dmul_rn(s, inv255));
+  }
+  return (view ? a.f0r : a.f0l)[i];
+}
+
+__device__ __forceinline__ float down4(float a, float b, float c, float d) {
+  return __fmul_rn(0.25f, __fadd_rn(__fadd_rn(__fadd_rn(a, b), c), d));
+}
+
+template <bool kU8>
+__global__ void __launch_bounds__(256) k_pyramid(PyrArgs a) {
+  extern __shared__ __align__(16) float sbuf[];
+  const int band = blockIdx.x;
+  const long long pair = blockIdx.y;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int ce = a.ce, fe = a.fe;
+  // level-1 rows of this band live in buf0 (L then R), level e >= 2 alternate
+  float* buf[2] = {sbuf, sbuf + 2 * a.buf_floats};
+  auto store = [&](int e, int y0, int rows, const float* Lb, const float* Rb) {
+    const int w = a.ws[e];
+    const long long pl = pair * (long long)w * a.hs[e];
+    const long long pr = pair * (long long)(w + 1) * a.hs[e];
+    for (int q = tid; q < rows * w; q += nt) {
+      const int r = q / w, x = q % w;
+      const float* lr = Lb + r * w;
+      const float l = lr[x];
+      float g = 0.0f;
+      if (w >= 2) {
+        if (x == 0) g = __fsub_rn(lr[1], lr[0]);
+        else if (x == w - 1) g = __fsub_rn(lr[w - 1], lr[w - 2]);
+        else g = __fmul_rn(0.5f, __fsub_rn(lr[x + 1], lr[x - 1]));
+      }
+      const long long o = pl + (long long)(y0 + r) * w + x;
+      a.L[e][o] = l;
+      a.G[e][o] = g;
+      const float rv = Rb[r * w + x];
+      float* rp = a.Rp[e] + pr + (long long)(y0 + r) * (w + 1);
+      rp[x] = rv;
+      if (x == w - 1) rp[w] = rv;
+    }
+  };
+  // ---- level 0 rows of the band (stored only when finest_exp == 0)
+  if (fe == 0) {
+    const int r0 = band << ce, r1 = min(r0 + (1 << ce), a.H);
+    const int W = a.W;
+    const long long pl = pair * (long long)W * a.H, pr = pair * (long long)(W + 1) * a.H;
+    for (int q = tid; q < (r1 - r0) * W; q += nt) {
+      const int y = r0 + q / W, x = q % W;
+      const float l = src_px<kU8>(a, 0, pair, x, y);
+      float g = 0.0f;
+      if (W >= 2) {
+        if (x == 0) g = __fsub_rn(src_px<kU8>(a, 0, pair, 1, y), l);
+        else if (x == W - 1) g = __fsub_rn(l, src_px<kU8>(a, 0, pair, W - 2, y));
+        else g = __fmul_rn(0.5f, __fsub_rn(src_px<kU8>(a, 0, pair, x + 1, y),
+                                           src_px<kU8>(a, 0, pair, x - 1, y)));
+      }
+      const long long o = pl + (long long)y * W + x;
+      a.L[0][o] = l;
+      a.G[0][o] = g;
+      const float rv = src_px<kU8>(a, 1, pair, x, y);
+      float* rp = a.Rp[0] + pr + (long long)y * (W + 1);
+      rp[x] = rv;
+      if (x == W - 1) rp[W] = rv;
+    }
+  }
+  if (ce == 0) return;
+  // ---- level 1 from the source
+  {
+    const int w = a.ws[1], h = a.hs[1];
+    const int y0 = band << (ce - 1), rows = min(1 << (ce - 1), h - y0);
+    float* Lb = buf[0];
+    float* Rb = buf[0] + a.buf_floats;
+    for (int q = tid; q < rows * w; q += nt) {
+      const int y = y0 + q / w, x = q % w;
+      const int sx0 = 2 * x, sx1 = min(2 * x + 1, a.W - 1);
+      const int sy0 = 2 * y, sy1 = min(2 * y + 1, a.H - 1);
+      Lb[q] = down4(src_px<kU8>(a, 0, pair, sx0, sy0), src_px<kU8>(a, 0, pair, sx1, sy0),
+                    src_px<kU8>(a, 0, pair, sx0, sy1), src_px<kU8>(a, 0, pair, sx1, sy1));
+      Rb[q] = down4(src_px<kU8>(a, 1, pair, sx0, sy0), src_px<kU8>(a, 1, pair, sx1, sy0),
+                    src_px<kU8>(a, 1, pair, sx0, sy1), src_px<kU8>(a, 1, pair, sx1, sy1));
+    }
+    __syncthreads();
+    if (1 >= fe) store(1, y0, rows, Lb, Rb);
+  }
+  // ---- levels 2..ce from the previous level in shared memory
+  for (int e = 2; e <= ce; ++e) {
+    const int pw = a.ws[e - 1], ph = a.hs[e - 1];
+    const int py0 = band << (ce - e + 1);
+    const float* PL = buf[(e - 2) & 1];
+    const float* PR = PL + a.buf_floats;
+    const int w = a.ws[e], h = a.hs[e];
+    const int y0 = band << (ce - e), rows = min(1 << (ce - e), h - y0);
+    float* Lb = buf[(e - 1) & 1];
+    float* Rb = Lb + a.buf_floats;
+    for (int q = tid; q < rows * w; q += nt) {
+      const int y = y0 + q / w, x = q % w;
+      const int x0 = 2 * x, x1 = min(2 * x + 1, pw - 1);
+      const int r0 = 2 * y - py0, r1 = min(2 * y + 1, ph - 1) - py0;
+      Lb[q] = down4(PL[r0 * pw + x0], PL[r0 * pw + x1], PL[r1 * pw + x0], PL[r1 * pw + x1]);
+      Rb[q] = down4(PR[r0 * pw + x0], PR[r0 * pw + x1], PR[r1 * pw + x0], PR[r1 * pw + x1]);
+    }
+    __syncthreads();
+    if (e >= fe) store(e, y0, rows, Lb, Rb);
+  }
+}
+
+size_t pyramid_smem_bytes(const PyrArgs& a) { return a.ce >= 1 ? 4 * a.buf_floats * sizeof(float) : 0; }
+
+cudaError_t launch_pyramid(const PyrArgs& a, bool u8, cudaStream_t s) {
+  const size_t smem = pyramid_smem_bytes(a);
+  dim3 grid(a.hs[a.ce], a.n_pairs);
+  if (u8) {
+    cudaFuncSetAttribute(k_pyramid<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_pyramid<true><<<grid, 256, smem, s>>>(a);
+  } else {
+    cudaFuncSetAttribute(k_pyramid<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_pyramid<false><<<grid, 256, smem, s>>>(a);
+  }
+  return cudaGetLastError();
 }
 
 // --------------------------------------------------------------------------

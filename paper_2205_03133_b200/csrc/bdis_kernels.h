@@ -31,7 +31,7 @@ struct BandPlan {
   int n_bands;     // ceil(ny / rb)
   int threads;     // CTA size
   int smem_rows;   // (rb - 1) * stride + size
-  int rpitch;      // smem slots per right-view row (doubles)
+  int rpitch;      // smem slots per right-view row
   int fpitch;      // smem slots per left/gradient row (floats)
   int bpitch;      // bytes per validity row
   int use_smem;    // 0: read the level tables from global memory
@@ -59,7 +59,7 @@ __host__ __device__ inline BandLayout band_layout(int rows, int rpitch, int fpit
     o += bytes;
     return r;
   };
-  l.oR = take(size_t(rows) * rpitch * 8, 16);
+  l.oR = take(size_t(rows) * rpitch * 4, 16);
   l.oL = take(size_t(rows) * fpitch * 4, 16);
   l.oG = take(size_t(rows) * fpitch * 4, 16);
   l.oLQ = take(valid ? size_t(rows) * bpitch : 0, 16);
@@ -79,6 +79,22 @@ __host__ __device__ inline BandLayout band_layout(int rows, int rpitch, int fpit
 }
 
 BandPlan plan_bands(const Level& L, const PatchParams& pp, int max_smem_per_cta);
+
+// Fused pyramid (all-valid inputs): levels are indexed by exponent.
+struct PyrArgs {
+  int n_pairs, W, H, C, ce, fe;
+  const uint8_t* u8l;
+  const uint8_t* u8r;
+  const float* f0l;
+  const float* f0r;
+  int ws[kMaxLevels], hs[kMaxLevels];
+  float* L[kMaxLevels];
+  float* G[kMaxLevels];
+  float* Rp[kMaxLevels];
+  int buf_floats;  // floats per view in one shared buffer: 2^(ce-1) * ws[1]
+};
+size_t pyramid_smem_bytes(const PyrArgs& a);
+cudaError_t launch_pyramid(const PyrArgs& a, bool u8, cudaStream_t s);
 
 struct FinestBufs {
   double* disp;

@@ -8,9 +8,9 @@
 //
 // B200 mapping
 //   * one CTA per (pair, band of `rb` patch rows); the band's rows of the
-//     right view (fp64), left view and gradient (fp32) are staged in shared
-//     memory once, padded (x + x/16 for 8-byte, x + x/32 for 4-byte slots) so
-//     the stride-`stride` accesses of neighbouring patches hit distinct banks;
+//     right view, left view and gradient (fp32) are staged in shared memory
+//     once, padded (x + x/32) so the stride-`stride` accesses of neighbouring
+//     patches hit distinct banks;
 //   * a thread owns one patch at a time and sums its samples in the
 //     reference's sequential row-major order -- that is what makes every sum
 //     bit-identical to the CPU (a warp tree reduction would reorder them);
@@ -48,13 +48,12 @@ struct Ev {
 
 template <bool kSmem>
 struct Rows {
-  const double* R;   // right view, fp64, rows of (w+1)
+  const float* R;    // right view, rows of (w+1)
   const float* Lf;   // left view
   const float* Gf;   // gradient of the left view
   const uint8_t* lq; // 4-tap validity (kValid only)
   const uint8_t* rq;
   int rp, fp, bp;    // row pitches (slots)
-  __device__ __forceinline__ static int s8(int x) { return kSmem ? x + (x >> 4) : x; }
   __device__ __forceinline__ static int s4(int x) { return kSmem ? x + (x >> 5) : x; }
 };
 
@@ -87,13 +86,13 @@ __device__ __forceinline__ Ev eval_patch(const Rows<kSmem>& rw, int w, int s_rt,
   double sum = 0.0;
 #pragma unroll 1
   for (int j = 0; j < s; ++j) {
-    const double* rr = rw.R + (r0 + j) * rw.rp;
+    const float* rr = rw.R + (r0 + j) * rw.rp;
     double b = 0.0;
 #pragma unroll
     for (int i = 0; i < SA; ++i) {
       if (S == 0 && i >= s) break;
-      const double a = (contig >> i) & 1u ? b : rr[rw.s8(cxi[i])];
-      b = rr[rw.s8(cxi[i] + 1)];
+      const double a = (contig >> i) & 1u ? b : (double)rr[rw.s4(cxi[i])];
+      b = (double)rr[rw.s4(cxi[i] + 1)];
       const double v = __dadd_rn(__dmul_rn(comf[i], a), __dmul_rn(cfx[i], b));
       bool use = (inb >> i) & 1u;
       if (kValid)
@@ -114,15 +113,15 @@ __device__ __forceinline__ Ev eval_patch(const Rows<kSmem>& rw, int w, int s_rt,
   double ssr = 0.0, jr = 0.0;
 #pragma unroll 1
   for (int j = 0; j < s; ++j) {
-    const double* rr = rw.R + (r0 + j) * rw.rp;
+    const float* rr = rw.R + (r0 + j) * rw.rp;
     const float* lr = rw.Lf + (r0 + j) * rw.fp;
     const float* gr = rw.Gf + (r0 + j) * rw.fp;
     double b = 0.0;
 #pragma unroll
     for (int i = 0; i < SA; ++i) {
       if (S == 0 && i >= s) break;
-      const double a = (contig >> i) & 1u ? b : rr[rw.s8(cxi[i])];
-      b = rr[rw.s8(cxi[i] + 1)];
+      const double a = (contig >> i) & 1u ? b : (double)rr[rw.s4(cxi[i])];
+      b = (double)rr[rw.s4(cxi[i] + 1)];
       bool use = (inb >> i) & 1u;
       if (kValid)
         use = use && rw.lq[(r0 + j) * rw.bp + x0 + i] && rw.rq[(r0 + j) * rw.bp + cxi[i]];
@@ -228,7 +227,7 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
   // ---- shared-memory carve-up (mirrors band_layout on the host)
   const BandLayout lay = band_layout(bp.use_smem ? bp.smem_rows : 0, bp.rpitch, bp.fpitch,
                                      bp.bpitch, bp.npb, nwin, kValid);
-  double* sR = (double*)(smem + lay.oR);
+  float* sR = (float*)(smem + lay.oR);
   float* sL = (float*)(smem + lay.oL);
   float* sG = (float*)(smem + lay.oG);
   uint8_t* sLQ = smem + lay.oLQ;
@@ -249,10 +248,10 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
   int rofs;  // row index of image row y in rw is y - rofs
   if (kSmem) {
     // ---- stage the band (coalesced global reads, padded shared writes)
-    const double* gR = L.rd + pair * (long long)(w + 1) * h + (long long)ylo * (w + 1);
+    const float* gR = L.rpad + pair * (long long)(w + 1) * h + (long long)ylo * (w + 1);
     for (int r = 0; r < nrows; ++r) {
       for (int x = tid; x <= w; x += nt)
-        sR[r * bp.rpitch + Rows<true>::s8(x)] = gR[(long long)r * (w + 1) + x];
+        sR[r * bp.rpitch + Rows<true>::s4(x)] = gR[(long long)r * (w + 1) + x];
       const float* gl = L.left + pbase + (long long)(ylo + r) * w;
       const float* gg = L.grad + pbase + (long long)(ylo + r) * w;
       for (int x = tid; x < w; x += nt) {
@@ -278,7 +277,7 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
     rw.bp = bp.bpitch;
     rofs = ylo;
   } else {
-    rw.R = L.rd + pair * (long long)(w + 1) * h;
+    rw.R = L.rpad + pair * (long long)(w + 1) * h;
     rw.Lf = L.left + pbase;
     rw.Gf = L.grad + pbase;
     rw.lq = L.lq + pbase;
@@ -512,7 +511,7 @@ BandPlan plan_bands(const Level& L, const PatchParams& pp, int max_smem_per_cta)
   const Grid& g = L.g;
   BandPlan bp{};
   const bool valid = !pp.all_valid;
-  bp.rpitch = (L.w + (L.w >> 4)) + 1;           // slots for x in [0, w]
+  bp.rpitch = (L.w + (L.w >> 5)) + 1;           // slots for x in [0, w]
   bp.fpitch = (L.w - 1 + ((L.w - 1) >> 5)) + 1;  // slots for x in [0, w-1]
   bp.bpitch = valid ? L.w : 0;
   auto bytes_for = [&](int rb) {
@@ -580,7 +579,7 @@ __global__ void k_debug_eval(Level L, int size, int nq, const int* __restrict__ 
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= nq) return;
   Rows<false> rw;
-  rw.R = L.rd;
+  rw.R = L.rpad;
   rw.Lf = L.left;
   rw.Gf = L.grad;
   rw.lq = L.lq;
