@@ -30,6 +30,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <math.h>
 #include <math_constants.h>
 #include <stdint.h>
@@ -82,6 +83,57 @@ __device__ __forceinline__ Ev eval_patch(const Rows<kSmem>& rw, int w, int s_rt,
     inb |= (unsigned)in << i;
     if (i > 0 && xi == cxi[i - 1] + 1) contig |= 1u << i;  // tap reuse: a_i == b_{i-1}
   }
+  Ev ev;
+  ev.jr = 0.0;
+  ev.msq = CUDART_INF;
+  // Fast path (all valid, every column inside the image, taps contiguous:
+  // x0_i = x0_0 + i): no predicates, slot offsets hoisted out of the rows.
+  const unsigned full = S > 0 ? ((S >= 32) ? 0xffffffffu : ((1u << SA) - 1u)) : 0u;
+  if (S > 0 && !kValid && inb == full && contig == (full & ~1u)) {
+    int offR[SA + 1], offT[SA];
+#pragma unroll
+    for (int i = 0; i <= SA; ++i) offR[i] = rw.s4(cxi[0] + i);
+#pragma unroll
+    for (int i = 0; i < SA; ++i) offT[i] = rw.s4(x0 + i);
+    double sum = 0.0;
+    const float* rr = rw.R + r0 * rw.rp;
+#pragma unroll 1
+    for (int j = 0; j < SA; ++j, rr += rw.rp) {
+      double a = (double)rr[offR[0]];
+#pragma unroll
+      for (int i = 0; i < SA; ++i) {
+        const double b = (double)rr[offR[i + 1]];
+        sum = __dadd_rn(sum, __dadd_rn(__dmul_rn(comf[i], a), __dmul_rn(cfx[i], b)));
+        a = b;
+      }
+    }
+    const int n = SA * SA;
+    ev.n = n;
+    const double rmean = __ddiv_rn(sum, (double)n);
+    double ssr = 0.0, jr = 0.0;
+    rr = rw.R + r0 * rw.rp;
+    const float* lr = rw.Lf + r0 * rw.fp;
+    const float* gr = rw.Gf + r0 * rw.fp;
+#pragma unroll 1
+    for (int j = 0; j < SA; ++j, rr += rw.rp, lr += rw.fp, gr += rw.fp) {
+      double a = (double)rr[offR[0]];
+#pragma unroll
+      for (int i = 0; i < SA; ++i) {
+        const double b = (double)rr[offR[i + 1]];
+        const double v = __dadd_rn(__dmul_rn(comf[i], a), __dmul_rn(cfx[i], b));
+        a = b;
+        const double t = __dsub_rn((double)lr[offT[i]], mean);
+        const double r = __dsub_rn(__dsub_rn(v, rmean), t);
+        ssr = __dadd_rn(ssr, __dmul_rn(r, r));
+        jr = __dadd_rn(jr, __dmul_rn((double)gr[offT[i]], r));
+      }
+    }
+    ev.msq = __ddiv_rn(ssr, (double)n);
+    ev.jr = jr;
+    return ev;
+  }
+  // General path: per-sample predicates (out-of-image columns, validity masks,
+  // non-contiguous taps).
   int n = 0;
   double sum = 0.0;
 #pragma unroll 1
@@ -104,10 +156,7 @@ __device__ __forceinline__ Ev eval_patch(const Rows<kSmem>& rw, int w, int s_rt,
     }
   }
   if (!kValid) n = s * __popc(inb);
-  Ev ev;
   ev.n = n;
-  ev.msq = CUDART_INF;
-  ev.jr = 0.0;
   if (n == 0) return ev;
   const double rmean = __ddiv_rn(sum, (double)n);
   double ssr = 0.0, jr = 0.0;
@@ -518,11 +567,18 @@ BandPlan plan_bands(const Level& L, const PatchParams& pp, int max_smem_per_cta)
     const int rows = (rb - 1) * g.stride + g.size;
     return band_layout(rows, bp.rpitch, bp.fpitch, bp.bpitch, rb * g.nx, pp.nwin, valid).total;
   };
-  // ~1.5 patches per lane of a 128-thread CTA, while two CTAs fit an SM
-  const int threads = 128;
-  const size_t two_per_sm = size_t(max_smem_per_cta) / 2 - 1024;
-  int rb = std::max(1, std::min(g.ny, (3 * threads / 2 + g.nx / 2) / g.nx));
-  while (rb > 1 && bytes_for(rb) > two_per_sm) --rb;
+  // ~1.5 patches per lane of a 128-thread CTA, while `ctas` CTAs fit an SM
+  // (PSTEREO_TUNE_THREADS / _PPL10 / _CTAS override, for tuning runs only)
+  auto env = [](const char* k, int d) {
+    const char* v = getenv(k);
+    return v ? atoi(v) : d;
+  };
+  const int threads = env("PSTEREO_TUNE_THREADS", 128);
+  const int ppl10 = env("PSTEREO_TUNE_PPL10", 15);
+  const int ctas = env("PSTEREO_TUNE_CTAS", 2);
+  const size_t per_sm = size_t(max_smem_per_cta) / ctas - 1024;
+  int rb = std::max(1, std::min(g.ny, (ppl10 * threads / 10 + g.nx / 2) / g.nx));
+  while (rb > 1 && bytes_for(rb) > per_sm) --rb;
   bp.use_smem = bytes_for(rb) <= size_t(max_smem_per_cta);
   bp.rb = rb;
   bp.n_bands = (g.ny + rb - 1) / rb;
