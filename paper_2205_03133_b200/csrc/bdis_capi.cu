@@ -665,8 +665,13 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
     pp.want_var = prm.estimate_variance && lv[li].e == fe;
     pp.have_prev = li > 0;
     const Level& P = li > 0 ? lv[li - 1] : lv[li];
-    const BandPlan bp = plan_bands(lv[li], pp, ctx->max_smem);
-    CK(launch_patches(lv[li], P, pp, bp, s));
+    BandPlan bp;
+    if (plan_bands_rt(lv[li], pp, ctx->max_smem, &bp)) {
+      CK(launch_patches_rt(lv[li], P, pp, bp, s));
+    } else {
+      bp = plan_bands(lv[li], pp, ctx->max_smem);
+      CK(launch_patches(lv[li], P, pp, bp, s));
+    }
     ++ctx->launches;
     CK(mark());
   }

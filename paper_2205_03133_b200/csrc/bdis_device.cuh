@@ -107,4 +107,69 @@ __device__ __forceinline__ Fused gather(const Level& P, long long pair, int x,
   return f;
 }
 
+// estimate_patch_variance (src/depth_variance.cpp:94-170) on the window
+// priors. CUDA exp() may differ from glibc's by an ulp: sigma_k agrees to
+// ~1e-15 relative, which is why var_disp is held to 1e-3 rel, not bits.
+__device__ inline double variance_fit(const double* woff, int nwin, int wcenter, const double* res,
+                               const uint8_t* ok, double denom) {
+  double delta[kMaxWin], p[kMaxWin];
+  double center_prior = 0.0;
+  int n = 0;
+  for (int k = 0; k < nwin; ++k) {
+    if (!ok[k]) continue;
+    const double pr = fast_exp(__ddiv_rn(-res[k], denom));
+    delta[n] = woff[k];
+    p[n] = pr;
+    ++n;
+    if (k == wcenter) center_prior = pr;
+  }
+  const double fallback = 2.0;  // kSigmaFallback, inc/depth_variance.hpp:15
+  if (n < 3) return fallback;
+  for (int i = 0; i < n; ++i) {
+    if (delta[i] == 0.0) continue;
+    if (!(center_prior > p[i])) return fallback;
+  }
+  double c = 1.0;
+  double sigma = sqrt(0.1);
+  for (int iter = 0; iter < 10; ++iter) {  // kVarianceFitIterations
+    double a00 = 0.0, a01 = 0.0, a11 = 0.0, b0 = 0.0, b1 = 0.0;
+    for (int i = 0; i < n; ++i) {
+      const double d2 = __dmul_rn(delta[i], delta[i]);
+      const double g = exp(__ddiv_rn(-d2, __dmul_rn(__dmul_rn(2.0, sigma), sigma)));
+      const double r = __dsub_rn(__dmul_rn(c, g), p[i]);
+      const double js = __ddiv_rn(__dmul_rn(__dmul_rn(c, g), d2),
+                                  __dmul_rn(__dmul_rn(sigma, sigma), sigma));
+      a00 = __dadd_rn(a00, __dmul_rn(g, g));
+      a01 = __dadd_rn(a01, __dmul_rn(g, js));
+      a11 = __dadd_rn(a11, __dmul_rn(js, js));
+      b0 = __dsub_rn(b0, __dmul_rn(g, r));
+      b1 = __dsub_rn(b1, __dmul_rn(js, r));
+    }
+    if (!(a00 > 0.0)) return fallback;
+    const double l00 = __dsqrt_rn(a00);
+    const double l01 = __ddiv_rn(a01, l00);
+    const double d11 = __dsub_rn(a11, __dmul_rn(l01, l01));
+    if (!(d11 > 1e-300)) return fallback;
+    const double l11 = __dsqrt_rn(d11);
+    const double y0 = __ddiv_rn(b0, l00);
+    const double y1 = __ddiv_rn(__dsub_rn(b1, __dmul_rn(l01, y0)), l11);
+    const double xs = __ddiv_rn(y1, l11);
+    const double xc = __ddiv_rn(__dsub_rn(y0, __dmul_rn(l01, xs)), l00);
+    c = __dadd_rn(c, xc);
+    sigma = __dadd_rn(sigma, xs);
+    if (!isfinite(c) || !isfinite(sigma) || sigma <= 0.0) return fallback;
+  }
+  double ssr = 0.0;
+  for (int i = 0; i < n; ++i) {
+    const double g = exp(__ddiv_rn(__dmul_rn(-delta[i], delta[i]),
+                                   __dmul_rn(__dmul_rn(2.0, sigma), sigma)));
+    const double r = __dsub_rn(__dmul_rn(c, g), p[i]);
+    ssr = __dadd_rn(ssr, __dmul_rn(r, r));
+  }
+  const double fit = __dsqrt_rn(__ddiv_rn(ssr, (double)n));
+  if (!isfinite(fit)) return fallback;
+  if (fit > 0.1) return fallback;  // kVarianceFitMaxResidual
+  return sigma;
+}
+
 }  // namespace bdis

@@ -79,6 +79,10 @@ __host__ __device__ inline BandLayout band_layout(int rows, int rpitch, int fpit
 }
 
 BandPlan plan_bands(const Level& L, const PatchParams& pp, int max_smem_per_cta);
+// register-template variant for 8x8 patches of fully valid inputs (bdis_patches_rt.cu)
+bool plan_bands_rt(const Level& L, const PatchParams& pp, int max_smem_per_cta, BandPlan* out);
+cudaError_t launch_patches_rt(const Level& L, const Level& P, const PatchParams& pp,
+                              const BandPlan& bp, cudaStream_t s);
 
 // Fused pyramid (all-valid inputs): levels are indexed by exponent.
 struct PyrArgs {
