@@ -371,17 +371,30 @@ __global__ void __launch_bounds__(kTileW * kTileH) k_ccl_local(int w, int h, lon
 
 __global__ void k_ccl_border(int w, int h, long long plane, const uint8_t* __restrict__ mask,
                              int* lab) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= w * h) return;
-  const int x = i % w, y = i / w;
-  const bool left_edge = x > 0 && x % kTileW == 0, top_edge = y > 0 && y % kTileH == 0;
-  if (!left_edge && !top_edge) return;
+  // threads enumerate tile-border pixels only: vertical borders first
+  // (x = k*kTileW, k >= 1, every row), then horizontal ones
+  const int tiles_x = (w + kTileW - 1) / kTileW, tiles_y = (h + kTileH - 1) / kTileH;
+  const int nv = (tiles_x - 1) * h, nh = (tiles_y - 1) * w;
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nv + nh) return;
+  int x, y;
+  bool left;
+  if (q < nv) {
+    x = (q / h + 1) * kTileW;
+    y = q % h;
+    left = true;
+  } else {
+    x = (q - nv) % w;
+    y = ((q - nv) / w + 1) * kTileH;
+    left = false;
+  }
   const long long base = blockIdx.y * plane;
+  const int i = y * w + x;
   if (!mask[base + i]) return;
   int* l = lab + base;
   volatile int* vl = l;
-  if (left_edge && mask[base + i - 1]) uf_union(vl, l, i, i - 1);
-  if (top_edge && mask[base + i - w]) uf_union(vl, l, i, i - w);
+  const int j = left ? i - 1 : i - w;
+  if (mask[base + j]) uf_union(vl, l, i, j);
 }
 
 __global__ void k_ccl_final(int w, int h, long long plane, int full_w, int full_h, int e,
@@ -414,40 +427,49 @@ __global__ void k_ccl_final(int w, int h, long long plane, int full_w, int full_
 // sharing (src/pipeline.cpp:21-22) and disparity_to_depth (:9-41).
 template <typename T>
 __global__ void k_output(OutputArgs a) {
+  // one thread per finest-level pixel: values are computed once and written
+  // to its 2^e x 2^e full-resolution block (nearest upsampling)
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= a.W * a.H) return;
+  if (i >= a.fw * a.fh) return;
   const long long pair = blockIdx.y;
-  const int X = i % a.W, Y = i / a.W;
-  const int fx = min(X >> a.e, a.fw - 1), fy = min(Y >> a.e, a.fh - 1);
-  const long long f = pair * a.fplane + (long long)fy * a.fw + fx;
+  const int fx = i % a.fw, fy = i / a.fw;
+  const long long f = pair * a.fplane + i;
   const bool mv = a.mvalid[f] != 0;
   bool keep = false;
   if (a.fmask[f]) keep = a.area[pair * a.fplane + a.label[f]] >= a.min_px;
   const double d = mv ? __dmul_rn(a.scale_d, a.disp[f]) : 0.0;
   const double p = mv ? __dmul_rn(1.0, a.prob[f]) : 0.0;
-  const long long o = pair * (long long)a.W * a.H + i;
-  T* disp = (T*)a.out_disp;
-  if (disp) disp[o] = (T)d;
-  if (a.out_dvalid) a.out_dvalid[o] = keep ? 1 : 0;
-  if (a.out_prob) ((T*)a.out_prob)[o] = (T)p;
-  if (a.out_mdisp) ((T*)a.out_mdisp)[o] = (T)d;
-  if (a.out_mvalid) a.out_mvalid[o] = mv ? 1 : 0;
   const bool dv = keep && (d >= 0.1);  // kMinDisparity, inc/depth_variance.hpp:13
-  if (a.out_depth) ((T*)a.out_depth)[o] = (T)(dv ? __ddiv_rn(a.fb, d) : 0.0);
-  if (a.out_depth_valid) a.out_depth_valid[o] = dv ? 1 : 0;
+  const double depth = dv ? __ddiv_rn(a.fb, d) : 0.0;
+  double v = 0.0, sg = 0.0;
+  bool sv = false;
   if (a.has_var) {
-    const double v = mv ? __dmul_rn(a.scale_v, a.var[f]) : 0.0;
-    if (a.out_var) ((T*)a.out_var)[o] = (T)v;
-    const bool sv = dv && mv;
-    if (a.out_sigma) {
-      double sg = 0.0;
-      if (sv) {
-        const double vv = (v < 0.0) ? 0.0 : v;  // std::max(var, 0.0)
-        sg = __dmul_rn(__ddiv_rn(a.fb, __dmul_rn(d, d)), __dsqrt_rn(vv));
-      }
-      ((T*)a.out_sigma)[o] = (T)sg;
+    v = mv ? __dmul_rn(a.scale_v, a.var[f]) : 0.0;
+    sv = dv && mv;
+    if (sv) {
+      const double vv = (v < 0.0) ? 0.0 : v;  // std::max(var, 0.0)
+      sg = __dmul_rn(__ddiv_rn(a.fb, __dmul_rn(d, d)), __dsqrt_rn(vv));
     }
-    if (a.out_sigma_valid) a.out_sigma_valid[o] = sv ? 1 : 0;
+  }
+  const int x0 = fx << a.e, x1 = min((fx + 1) << a.e, a.W);
+  const int y0 = fy << a.e, y1 = min((fy + 1) << a.e, a.H);
+  const long long pbase = pair * (long long)a.W * a.H;
+  for (int y = y0; y < y1; ++y) {
+    for (int x = x0; x < x1; ++x) {
+      const long long o = pbase + (long long)y * a.W + x;
+      if (a.out_disp) ((T*)a.out_disp)[o] = (T)d;
+      if (a.out_dvalid) a.out_dvalid[o] = keep ? 1 : 0;
+      if (a.out_prob) ((T*)a.out_prob)[o] = (T)p;
+      if (a.out_mdisp) ((T*)a.out_mdisp)[o] = (T)d;
+      if (a.out_mvalid) a.out_mvalid[o] = mv ? 1 : 0;
+      if (a.out_depth) ((T*)a.out_depth)[o] = (T)depth;
+      if (a.out_depth_valid) a.out_depth_valid[o] = dv ? 1 : 0;
+      if (a.has_var) {
+        if (a.out_var) ((T*)a.out_var)[o] = (T)v;
+        if (a.out_sigma) ((T*)a.out_sigma)[o] = (T)sg;
+        if (a.out_sigma_valid) a.out_sigma_valid[o] = sv ? 1 : 0;
+      }
+    }
   }
 }
 
@@ -522,13 +544,15 @@ void launch_ccl(int w, int h, long long plane, int full_w, int full_h, int e,
                 const uint8_t* mask, int* lab, int* area, int n_pairs, cudaStream_t s) {
   const int tiles = ((w + kTileW - 1) / kTileW) * ((h + kTileH - 1) / kTileH);
   k_ccl_local<<<dim3(tiles, n_pairs), kTileW * kTileH, 0, s>>>(w, h, plane, mask, lab);
+  const int tx = (w + kTileW - 1) / kTileW, ty = (h + kTileH - 1) / kTileH;
+  const long long nb = (long long)(tx - 1) * h + (long long)(ty - 1) * w;
+  if (nb > 0) k_ccl_border<<<dim3(blocks_for(nb, 256), n_pairs), 256, 0, s>>>(w, h, plane, mask, lab);
   dim3 grid(blocks_for((long long)w * h, 256), n_pairs);
-  k_ccl_border<<<grid, 256, 0, s>>>(w, h, plane, mask, lab);
   k_ccl_final<<<grid, 256, 0, s>>>(w, h, plane, full_w, full_h, e, mask, lab, area);
 }
 
 void launch_output(const OutputArgs& a, int f64, int n_pairs, cudaStream_t s) {
-  dim3 grid(blocks_for((long long)a.W * a.H, 256), n_pairs);
+  dim3 grid(blocks_for((long long)a.fw * a.fh, 256), n_pairs);
   if (f64) k_output<double><<<grid, 256, 0, s>>>(a);
   else k_output<float><<<grid, 256, 0, s>>>(a);
 }

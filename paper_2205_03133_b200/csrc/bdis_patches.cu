@@ -86,29 +86,34 @@ __device__ __forceinline__ Ev eval_patch(const Rows<kSmem>& rw, int w, int s_rt,
   Ev ev;
   ev.jr = 0.0;
   ev.msq = CUDART_INF;
-  // Fast path (all valid, every column inside the image, taps contiguous:
-  // x0_i = x0_0 + i): no predicates, slot offsets hoisted out of the rows.
-  const unsigned full = S > 0 ? ((S >= 32) ? 0xffffffffu : ((1u << SA) - 1u)) : 0u;
-  if (S > 0 && !kValid && inb == full && contig == (full & ~1u)) {
-    int offR[SA + 1], offT[SA];
+  // Fully valid inputs: ONE predicated path for every lane -- columns outside
+  // the image are skipped (invalid samples, inc/image.hpp:55,68), the left tap
+  // is reused from the previous column when contiguous -- so lanes of a warp
+  // never split between code paths. Slot offsets are hoisted out of the rows.
+  if (S > 0 && !kValid) {
+    int offA[SA], offB[SA], offT[SA];
 #pragma unroll
-    for (int i = 0; i <= SA; ++i) offR[i] = rw.s4(cxi[0] + i);
-#pragma unroll
-    for (int i = 0; i < SA; ++i) offT[i] = rw.s4(x0 + i);
+    for (int i = 0; i < SA; ++i) {
+      offA[i] = rw.s4(cxi[i]);
+      offB[i] = rw.s4(cxi[i] + 1);
+      offT[i] = rw.s4(x0 + i);
+    }
+    const int n = SA * __popc(inb);
+    ev.n = n;
+    if (n == 0) return ev;
     double sum = 0.0;
     const float* rr = rw.R + r0 * rw.rp;
 #pragma unroll 1
     for (int j = 0; j < SA; ++j, rr += rw.rp) {
-      double a = (double)rr[offR[0]];
+      double b = 0.0;
 #pragma unroll
       for (int i = 0; i < SA; ++i) {
-        const double b = (double)rr[offR[i + 1]];
-        sum = __dadd_rn(sum, __dadd_rn(__dmul_rn(comf[i], a), __dmul_rn(cfx[i], b)));
-        a = b;
+        const double a = ((contig >> i) & 1u) ? b : (double)rr[offA[i]];
+        b = (double)rr[offB[i]];
+        const double v = __dadd_rn(__dmul_rn(comf[i], a), __dmul_rn(cfx[i], b));
+        if ((inb >> i) & 1u) sum = __dadd_rn(sum, v);
       }
     }
-    const int n = SA * SA;
-    ev.n = n;
     const double rmean = __ddiv_rn(sum, (double)n);
     double ssr = 0.0, jr = 0.0;
     rr = rw.R + r0 * rw.rp;
@@ -116,24 +121,26 @@ __device__ __forceinline__ Ev eval_patch(const Rows<kSmem>& rw, int w, int s_rt,
     const float* gr = rw.Gf + r0 * rw.fp;
 #pragma unroll 1
     for (int j = 0; j < SA; ++j, rr += rw.rp, lr += rw.fp, gr += rw.fp) {
-      double a = (double)rr[offR[0]];
+      double b = 0.0;
 #pragma unroll
       for (int i = 0; i < SA; ++i) {
-        const double b = (double)rr[offR[i + 1]];
+        const double a = ((contig >> i) & 1u) ? b : (double)rr[offA[i]];
+        b = (double)rr[offB[i]];
         const double v = __dadd_rn(__dmul_rn(comf[i], a), __dmul_rn(cfx[i], b));
-        a = b;
         const double t = __dsub_rn((double)lr[offT[i]], mean);
         const double r = __dsub_rn(__dsub_rn(v, rmean), t);
-        ssr = __dadd_rn(ssr, __dmul_rn(r, r));
-        jr = __dadd_rn(jr, __dmul_rn((double)gr[offT[i]], r));
+        const double gv = (double)gr[offT[i]];
+        if ((inb >> i) & 1u) {
+          ssr = __dadd_rn(ssr, __dmul_rn(r, r));
+          jr = __dadd_rn(jr, __dmul_rn(gv, r));
+        }
       }
     }
     ev.msq = __ddiv_rn(ssr, (double)n);
     ev.jr = jr;
     return ev;
   }
-  // General path: per-sample predicates (out-of-image columns, validity masks,
-  // non-contiguous taps).
+  // Validity masks (or a runtime patch size): per-sample predicates.
   int n = 0;
   double sum = 0.0;
 #pragma unroll 1

@@ -393,7 +393,9 @@ __global__ void __launch_bounds__(128, 2) k_patches_rt(Level L, Level P, PatchPa
 
 bool plan_bands_rt(const Level& L, const PatchParams& pp, int max_smem_per_cta, BandPlan* out) {
   const Grid& g = L.g;
-  if (!pp.all_valid || g.size != 8 || getenv("PSTEREO_TUNE_NO_RT")) return false;
+  // opt-in (PSTEREO_TUNE_RT=1): at 255 registers it runs 8 warps/SM and measured
+  // slower than k_patches on config 2 (see profiles/)
+  if (!pp.all_valid || g.size != 8 || !getenv("PSTEREO_TUNE_RT")) return false;
   BandPlan bp{};
   bp.rpitch = pad4_host(L.w) + 1;
   bp.fpitch = pad4_host(L.w - 1) + 1;
