@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -180,6 +181,10 @@ struct pstereo_ctx {
   DevBuf<int> stats;
   // staging for host outputs
   DevBuf<uint8_t> out_stage[10];
+  // host-buffer pipeline (chunked H2D / compute / D2H)
+  int chunk_pairs = 0;
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  std::vector<cudaEvent_t> chunk_events;
 };
 
 namespace {
@@ -351,6 +356,7 @@ int pstereo_gpu_create(int device, const pstereo_params* p, int max_width, int m
     return PSTEREO_EINTERNAL;
   }
   ctx->levels.resize(size_t(p->coarsest_exp) + 1);
+  if (const char* v = getenv("PSTEREO_CHUNK_PAIRS")) ctx->chunk_pairs = atoi(v);
   *out = ctx;
   return PSTEREO_OK;
 }
@@ -387,6 +393,9 @@ void pstereo_gpu_destroy(pstereo_ctx* ctx) {
   ctx->farea.release();
   ctx->stats.release();
   for (auto& b : ctx->out_stage) b.release();
+  for (auto e : ctx->chunk_events) cudaEventDestroy(e);
+  if (ctx->s_in) cudaStreamDestroy(ctx->s_in);
+  if (ctx->s_out) cudaStreamDestroy(ctx->s_out);
   for (auto* pool : {&ctx->ev_pending, &ctx->ev_free})
     for (auto& set : *pool)
       for (auto ev : set.ev) cudaEventDestroy(ev);
@@ -446,25 +455,27 @@ const char* pstereo_gpu_stage_name(const pstereo_ctx* ctx, int stage) {
 
 namespace {
 
-int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left_u8,
-        const uint8_t* right_u8, const float* left_f, const uint8_t* left_v,
-        const float* right_f, const uint8_t* right_v, int inputs_on_device, double focal,
-        double baseline, const pstereo_outputs* out, cudaStream_t stream) {
+// Device-resident batched run_pipeline: `n` pairs whose inputs are already in
+// device memory (uint8 rasters, or fp32 planes already in ctx->full at pair
+// offset `f32_offset` with validity in ctx->full_valid), outputs written to the
+// device planes in `dev_ptr` (already offset). Host-side stats / finest-level
+// records are copied asynchronously into `hs` and finished by the caller after
+// the stream completes.
+struct HostCopies {
+  int* stats = nullptr;      // [n][levels][3]
+  uint8_t* fst = nullptr;    // finest records [n][np]
+  double* fu = nullptr;
+  double* fpr = nullptr;
+  double* fpo = nullptr;
+  double* fsg = nullptr;
+};
+
+int run_device(pstereo_ctx* ctx, const std::vector<LevelGeom>& geo, int n, int W, int H,
+               int channels, const uint8_t* const src_u8_in[2], long long f32_offset,
+               bool have_f32_valid, double focal, double baseline, int f64,
+               void* const dev_ptr[10], const HostCopies& hc, cudaStream_t s) {
   const pstereo_params& prm = ctx->params;
-  ctx->launches = 0;
-  if (n < 0) return fail(ctx, PSTEREO_EINTERNAL, "n_pairs must be >= 0");
-  if (n == 0) return PSTEREO_OK;
-  if (!out) return fail(ctx, PSTEREO_EINTERNAL, "outputs must not be NULL");
-  std::vector<LevelGeom> geo;
-  std::string m;
-  int rc = level_geometry(&prm, W, H, &geo, &m);
-  if (rc) return fail(ctx, rc, m);
-  if (W > ctx->max_w || H > ctx->max_h || n > ctx->max_pairs)
-    return fail(ctx, PSTEREO_EINTERNAL, "batch exceeds the context's max_width/max_height/max_pairs");
-  if (left_u8 && channels != 1 && channels != 3 && channels != 4)
-    return fail(ctx, PSTEREO_EINTERNAL, "to_grayscale: unsupported channel count");
-  CK(cudaSetDevice(ctx->device));
-  const cudaStream_t s = stream ? stream : ctx->stream;
+  const uint8_t* left_u8 = src_u8_in[0];
   const bool prof = ctx->profiling;
   EvSet evs;
   if (prof) {
@@ -493,11 +504,15 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
   const int ce = prm.coarsest_exp, fe = prm.finest_exp, S = prm.patch_size;
   const long long n_full = (long long)W * H;
   const long long npx = n_full * n;
+  // fp32 inputs live in ctx->full at this pair offset (the chunked host path)
+  const float* fsrc[2] = {ctx->full[0].p + f32_offset * n_full, ctx->full[1].p + f32_offset * n_full};
+  const uint8_t* fval[2] = {ctx->full_valid[0].p + f32_offset * n_full,
+                            ctx->full_valid[1].p + f32_offset * n_full};
 
   // every input pixel is valid for gray/RGB rasters and for float planes
   // without masks: the fused pyramid applies and the patch kernel skips the
   // 4-tap validity tests
-  const bool all_valid = left_u8 ? (channels != 4) : (left_v == nullptr && right_v == nullptr);
+  const bool all_valid = left_u8 ? (channels != 4) : !have_f32_valid;
   std::vector<int> ws(ce + 1), hs(ce + 1);
   ws[0] = W;
   hs[0] = H;
@@ -520,34 +535,14 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
   pa.buf_floats = ce >= 1 ? (1 << (ce - 1)) * ws[1] : 0;
   const bool fused = all_valid && pyramid_smem_bytes(pa) <= size_t(ctx->max_smem);
 
-  // ---- inputs
-  const uint8_t* src_u8[2] = {left_u8, right_u8};
-  if (left_u8) {
-    const size_t bytes = size_t(npx) * channels;
-    for (int v = 0; v < 2; ++v) {
-      if (!inputs_on_device) {
-        CK(ctx->in_u8[v].ensure(bytes));
-        CK(cudaMemcpyAsync(ctx->in_u8[v].p, src_u8[v], bytes, cudaMemcpyHostToDevice, s));
-        src_u8[v] = ctx->in_u8[v].p;
-      }
-    }
-  }
-  if (!left_u8 || !fused) {
+  // ---- inputs (already on the device)
+  const uint8_t* src_u8[2] = {src_u8_in[0], src_u8_in[1]};
+  if (!left_u8 && !fused && !have_f32_valid)
+    for (int v = 0; v < 2; ++v) CK(cudaMemsetAsync((void*)fval[v], 1, size_t(npx), s));
+  if (left_u8 && !fused) {
     for (int v = 0; v < 2; ++v) {
       CK(ctx->full[v].ensure(size_t(npx)));
       CK(ctx->full_valid[v].ensure(size_t(npx)));
-    }
-  }
-  if (!left_u8) {
-    const float* fsrc[2] = {left_f, right_f};
-    const uint8_t* vsrc[2] = {left_v, right_v};
-    const cudaMemcpyKind kind = inputs_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-    for (int v = 0; v < 2; ++v) {
-      CK(cudaMemcpyAsync(ctx->full[v].p, fsrc[v], size_t(npx) * sizeof(float), kind, s));
-      if (!fused) {
-        if (vsrc[v]) CK(cudaMemcpyAsync(ctx->full_valid[v].p, vsrc[v], size_t(npx), kind, s));
-        else CK(cudaMemsetAsync(ctx->full_valid[v].p, 1, size_t(npx), s));
-      }
     }
   }
   CK(mark());
@@ -567,10 +562,10 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
     CK(B.grad.ensure(np));
     CK(B.rpad.ensure(size_t(G.w + 1) * G.h * n));
     if (G.e == 0 && !fused) {
-      L.left = ctx->full[0].p;
-      L.right = ctx->full[1].p;
-      L.lvalid = ctx->full_valid[0].p;
-      L.rvalid = ctx->full_valid[1].p;
+      L.left = left_u8 ? ctx->full[0].p : fsrc[0];
+      L.right = left_u8 ? ctx->full[1].p : fsrc[1];
+      L.lvalid = left_u8 ? ctx->full_valid[0].p : fval[0];
+      L.rvalid = left_u8 ? ctx->full_valid[1].p : fval[1];
     } else {
       CK(B.left.ensure(np));
       L.left = B.left.p;
@@ -603,8 +598,8 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
   if (fused) {
     pa.u8l = src_u8[0];
     pa.u8r = src_u8[1];
-    pa.f0l = left_u8 ? nullptr : ctx->full[0].p;
-    pa.f0r = left_u8 ? nullptr : ctx->full[1].p;
+    pa.f0l = left_u8 ? nullptr : fsrc[0];
+    pa.f0r = left_u8 ? nullptr : fsrc[1];
     CK(launch_pyramid(pa, left_u8 != nullptr, s));
     ++ctx->launches;
   } else {
@@ -622,10 +617,12 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
       CK(B.right.ensure(np));
       CK(B.lvalid.ensure(np));
       CK(B.rvalid.ensure(np));
-      const float* sl = e == 1 ? ctx->full[0].p : ctx->levels[e - 1].left.p;
-      const float* sr = e == 1 ? ctx->full[1].p : ctx->levels[e - 1].right.p;
-      const uint8_t* slv = e == 1 ? ctx->full_valid[0].p : ctx->levels[e - 1].lvalid.p;
-      const uint8_t* srv = e == 1 ? ctx->full_valid[1].p : ctx->levels[e - 1].rvalid.p;
+      const float* sl = e == 1 ? (left_u8 ? ctx->full[0].p : fsrc[0]) : ctx->levels[e - 1].left.p;
+      const float* sr = e == 1 ? (left_u8 ? ctx->full[1].p : fsrc[1]) : ctx->levels[e - 1].right.p;
+      const uint8_t* slv =
+          e == 1 ? (left_u8 ? ctx->full_valid[0].p : fval[0]) : ctx->levels[e - 1].lvalid.p;
+      const uint8_t* srv =
+          e == 1 ? (left_u8 ? ctx->full_valid[1].p : fval[1]) : ctx->levels[e - 1].rvalid.p;
       launch_downsample(sl, slv, sr, srv, ws[e - 1], hs[e - 1], B.left.p, B.lvalid.p, B.right.p,
                         B.rvalid.p, ws[e], hs[e], n, s);
       ++ctx->launches;
@@ -694,23 +691,6 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
   launch_ccl(F.w, F.h, F.plane, W, H, fe, ctx->fmask.p, ctx->flabel.p, ctx->farea.p, n, s);
   ctx->launches += 3;
 
-  // outputs: device pointers directly, or device staging + D2H
-  const int f64 = out->dtype == PSTEREO_F64;
-  const size_t esz = f64 ? sizeof(double) : sizeof(float);
-  const size_t nout = size_t(n_full) * n;
-  void* host_ptr[10] = {out->disparity, out->disparity_valid, out->probability, out->depth,
-                        out->depth_valid, out->depth_sigma, out->sigma_valid,
-                        out->match_disparity, out->match_valid, out->var_disp};
-  const size_t sizes[10] = {esz, 1, esz, esz, 1, esz, 1, esz, 1, esz};
-  void* dev_ptr[10];
-  for (int q = 0; q < 10; ++q) {
-    dev_ptr[q] = host_ptr[q];
-    if (!prm.estimate_variance && (q == 5 || q == 6 || q == 9)) dev_ptr[q] = nullptr;
-    if (host_ptr[q] && dev_ptr[q] && !out->on_device) {
-      CK(ctx->out_stage[q].ensure(nout * sizes[q]));
-      dev_ptr[q] = ctx->out_stage[q].p;
-    }
-  }
   OutputArgs oa;
   std::memset(&oa, 0, sizeof oa);
   oa.W = W;
@@ -747,7 +727,7 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
   launch_output(oa, f64, n, s);
   ++ctx->launches;
 
-  const bool want_stats = out->stats != nullptr;
+  const bool want_stats = hc.stats != nullptr;
   if (want_stats) {
     StatsArgs sa;
     std::memset(&sa, 0, sizeof sa);
@@ -764,57 +744,177 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
   CK(cudaGetLastError());
   CK(mark());
 
-  // ---- device -> host
-  bool need_sync = false;
-  if (!out->on_device) {
-    for (int q = 0; q < 10; ++q) {
-      if (!host_ptr[q] || !dev_ptr[q]) continue;
-      CK(cudaMemcpyAsync(host_ptr[q], dev_ptr[q], nout * sizes[q], cudaMemcpyDeviceToHost, s));
-      need_sync = true;
-    }
-  }
-  std::vector<int> hstats;
-  if (want_stats) {
-    hstats.resize(size_t(n) * lv.size() * 3);
-    CK(cudaMemcpyAsync(hstats.data(), ctx->stats.p, hstats.size() * sizeof(int),
+  if (want_stats)
+    CK(cudaMemcpyAsync(hc.stats, ctx->stats.p, size_t(n) * lv.size() * 3 * sizeof(int),
                        cudaMemcpyDeviceToHost, s));
-    need_sync = true;
-  }
-  // finest-level accepted patches (diagnostics; MatchResult::finest.patches)
-  std::vector<uint8_t> fst;
-  std::vector<double> fu, fpr, fpo, fsg;
-  const bool want_finest = out->finest && out->finest_count && out->finest_cap > 0;
-  if (want_finest) {
+  if (hc.fst) {
     const size_t nrec = size_t(F.g.nx) * F.g.ny * n;
-    fst.resize(nrec);
-    fu.resize(nrec);
-    fpr.resize(nrec);
-    fpo.resize(nrec);
-    fsg.resize(nrec);
-    CK(cudaMemcpyAsync(fst.data(), F.stage, nrec, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(fu.data(), F.u, nrec * 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(fpr.data(), F.prob, nrec * 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(fpo.data(), F.post, nrec * 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(fsg.data(), F.sigma, nrec * 8, cudaMemcpyDeviceToHost, s));
-    need_sync = true;
+    CK(cudaMemcpyAsync(hc.fst, F.stage, nrec, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hc.fu, F.u, nrec * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hc.fpr, F.prob, nrec * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hc.fpo, F.post, nrec * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hc.fsg, F.sigma, nrec * 8, cudaMemcpyDeviceToHost, s));
   }
   CK(mark());
   if (prof) ctx->ev_pending.push_back(std::move(evs));
+  return PSTEREO_OK;
+}
+
+// Public entry: validates, then either runs the device path directly or --
+// with host buffers -- pipelines chunks of pairs over three streams (H2D of
+// chunk c+1 and D2H of chunk c-1 overlap the kernels of chunk c).
+int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left_u8,
+        const uint8_t* right_u8, const float* left_f, const uint8_t* left_v,
+        const float* right_f, const uint8_t* right_v, int inputs_on_device, double focal,
+        double baseline, const pstereo_outputs* out, cudaStream_t stream) {
+  const pstereo_params& prm = ctx->params;
+  ctx->launches = 0;
+  if (n < 0) return fail(ctx, PSTEREO_EINTERNAL, "n_pairs must be >= 0");
+  if (n == 0) return PSTEREO_OK;
+  if (!out) return fail(ctx, PSTEREO_EINTERNAL, "outputs must not be NULL");
+  std::vector<LevelGeom> geo;
+  std::string m;
+  int rc = level_geometry(&prm, W, H, &geo, &m);
+  if (rc) return fail(ctx, rc, m);
+  if (W > ctx->max_w || H > ctx->max_h || n > ctx->max_pairs)
+    return fail(ctx, PSTEREO_EINTERNAL, "batch exceeds the context's max_width/max_height/max_pairs");
+  if (left_u8 && channels != 1 && channels != 3 && channels != 4)
+    return fail(ctx, PSTEREO_EINTERNAL, "to_grayscale: unsupported channel count");
+  CK(cudaSetDevice(ctx->device));
+  const cudaStream_t s = stream ? stream : ctx->stream;
+  const long long n_full = (long long)W * H;
+  const int f64 = out->dtype == PSTEREO_F64;
+  const size_t esz = f64 ? sizeof(double) : sizeof(float);
+  void* user_ptr[10] = {out->disparity, out->disparity_valid, out->probability, out->depth,
+                        out->depth_valid, out->depth_sigma, out->sigma_valid,
+                        out->match_disparity, out->match_valid, out->var_disp};
+  const size_t sizes[10] = {esz, 1, esz, esz, 1, esz, 1, esz, 1, esz};
+  for (int q : {5, 6, 9})
+    if (!prm.estimate_variance) user_ptr[q] = nullptr;
+  const bool host_in = !inputs_on_device, host_out = !out->on_device;
+  const bool pipelined = host_in || host_out;
+  const int n_levels = int(geo.size());
+  const Grid& fg = geo.back().g;
+  const size_t np_f = size_t(fg.nx) * fg.ny;
+  const bool want_finest = out->finest && out->finest_count && out->finest_cap > 0;
+  std::vector<int> hstats(out->stats ? size_t(n) * n_levels * 3 : 0);
+  std::vector<uint8_t> fst(want_finest ? np_f * n : 0);
+  std::vector<double> fu(fst.size()), fpr(fst.size()), fpo(fst.size()), fsg(fst.size());
+  const bool have_f32_valid = !left_u8 && (left_v || right_v);
+
+  // chunking: one chunk for the device path, else pairs per chunk
+  int chunk = n;
+  if (pipelined) {
+    chunk = ctx->chunk_pairs > 0 ? ctx->chunk_pairs : 32;
+    if (chunk > n) chunk = n;
+  }
+  // device input regions
+  const uint8_t* dev_u8[2] = {left_u8, right_u8};
+  if (left_u8 && host_in)
+    for (int v = 0; v < 2; ++v) {
+      CK(ctx->in_u8[v].ensure(size_t(n_full) * n * channels));
+      dev_u8[v] = ctx->in_u8[v].p;
+    }
+  if (!left_u8)
+    for (int v = 0; v < 2; ++v) {
+      CK(ctx->full[v].ensure(size_t(n_full) * n));
+      CK(ctx->full_valid[v].ensure(size_t(n_full) * n));
+    }
+  // device output regions
+  void* dev_out[10];
+  for (int q = 0; q < 10; ++q) {
+    dev_out[q] = user_ptr[q];
+    if (user_ptr[q] && host_out) {
+      CK(ctx->out_stage[q].ensure(size_t(n_full) * n * sizes[q]));
+      dev_out[q] = ctx->out_stage[q].p;
+    }
+  }
+  if (pipelined && !ctx->s_in) {
+    CK(cudaStreamCreateWithFlags(&ctx->s_in, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&ctx->s_out, cudaStreamNonBlocking));
+  }
+  const int n_chunks = (n + chunk - 1) / chunk;
+  while ((int)ctx->chunk_events.size() < 2 * n_chunks) {
+    cudaEvent_t e;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ctx->chunk_events.push_back(e);
+  }
+  for (int c = 0; c < n_chunks; ++c) {
+    const int c0 = c * chunk, nc = std::min(chunk, n - c0);
+    const size_t px0 = size_t(n_full) * c0, pxc = size_t(n_full) * nc;
+    if (pipelined) {
+      cudaStream_t sc = host_in ? ctx->s_in : s;
+      if (left_u8) {
+        if (host_in)
+          for (int v = 0; v < 2; ++v)
+            CK(cudaMemcpyAsync(ctx->in_u8[v].p + px0 * channels, (v ? right_u8 : left_u8) + px0 * channels,
+                               pxc * channels, cudaMemcpyHostToDevice, sc));
+      } else {
+        const cudaMemcpyKind kind = host_in ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+        for (int v = 0; v < 2; ++v) {
+          CK(cudaMemcpyAsync(ctx->full[v].p + px0, (v ? right_f : left_f) + px0, pxc * 4, kind, sc));
+          const uint8_t* vv = v ? right_v : left_v;
+          if (vv) CK(cudaMemcpyAsync(ctx->full_valid[v].p + px0, vv + px0, pxc, kind, sc));
+          else if (have_f32_valid) CK(cudaMemsetAsync(ctx->full_valid[v].p + px0, 1, pxc, sc));
+        }
+      }
+      if (sc != s) {
+        CK(cudaEventRecord(ctx->chunk_events[2 * c], sc));
+        CK(cudaStreamWaitEvent(s, ctx->chunk_events[2 * c], 0));
+      }
+    } else if (!left_u8) {
+      for (int v = 0; v < 2; ++v) {
+        CK(cudaMemcpyAsync(ctx->full[v].p, v ? right_f : left_f, pxc * 4, cudaMemcpyDeviceToDevice, s));
+        const uint8_t* vv = v ? right_v : left_v;
+        if (vv) CK(cudaMemcpyAsync(ctx->full_valid[v].p, vv, pxc, cudaMemcpyDeviceToDevice, s));
+        else if (have_f32_valid) CK(cudaMemsetAsync(ctx->full_valid[v].p, 1, pxc, s));
+      }
+    }
+    const uint8_t* cu8[2] = {left_u8 ? dev_u8[0] + px0 * channels : nullptr,
+                             left_u8 ? dev_u8[1] + px0 * channels : nullptr};
+    void* cout[10];
+    for (int q = 0; q < 10; ++q)
+      cout[q] = dev_out[q] ? (uint8_t*)dev_out[q] + px0 * sizes[q] : nullptr;
+    HostCopies hc;
+    if (!hstats.empty()) hc.stats = hstats.data() + size_t(c0) * n_levels * 3;
+    if (want_finest) {
+      hc.fst = fst.data() + np_f * c0;
+      hc.fu = fu.data() + np_f * c0;
+      hc.fpr = fpr.data() + np_f * c0;
+      hc.fpo = fpo.data() + np_f * c0;
+      hc.fsg = fsg.data() + np_f * c0;
+    }
+    const int launches0 = ctx->launches;
+    rc = run_device(ctx, geo, nc, W, H, channels, cu8, left_u8 ? 0 : c0, have_f32_valid, focal,
+                    baseline, f64, cout, hc, s);
+    if (rc) return rc;
+    (void)launches0;
+    if (host_out) {
+      CK(cudaEventRecord(ctx->chunk_events[2 * c + 1], s));
+      CK(cudaStreamWaitEvent(ctx->s_out, ctx->chunk_events[2 * c + 1], 0));
+      for (int q = 0; q < 10; ++q)
+        if (user_ptr[q])
+          CK(cudaMemcpyAsync((uint8_t*)user_ptr[q] + px0 * sizes[q], cout[q], pxc * sizes[q],
+                             cudaMemcpyDeviceToHost, ctx->s_out));
+    }
+  }
+  const bool need_sync = host_out || !hstats.empty() || want_finest;
+  if (host_out) CK(cudaStreamSynchronize(ctx->s_out));
   if (need_sync) CK(cudaStreamSynchronize(s));
-  if (want_stats) {
+  if (!hstats.empty()) {
     for (int p = 0; p < n; ++p)
-      for (size_t li = 0; li < lv.size(); ++li) {
-        pstereo_level_stats& st = out->stats[size_t(p) * lv.size() + li];
-        const int* c = &hstats[(size_t(p) * lv.size() + li) * 3];
-        st.exp = lv[li].e;
-        st.grid_patches = lv[li].g.nx * lv[li].g.ny;
-        st.extracted = c[0];
-        st.converged = c[1];
-        st.accepted = c[2];
+      for (int li = 0; li < n_levels; ++li) {
+        pstereo_level_stats& st = out->stats[size_t(p) * n_levels + li];
+        const int* cc = &hstats[(size_t(p) * n_levels + li) * 3];
+        st.exp = geo[size_t(li)].e;
+        st.grid_patches = geo[size_t(li)].g.nx * geo[size_t(li)].g.ny;
+        st.extracted = cc[0];
+        st.converged = cc[1];
+        st.accepted = cc[2];
       }
   }
   if (want_finest) {
-    const Grid& g = F.g;
+    const Grid& g = fg;
     const int np = g.nx * g.ny;
     for (int p = 0; p < n; ++p) {
       int cnt = 0;

@@ -138,3 +138,20 @@ def test_errors(gpu):
     with pytest.raises(P.DegenerateInputError):
         m.run_batch(l, l)  # 64x48 at 1/32 is 2x2 < 10 px (tests/test_pyramid.cpp:90-92)
     m.close()
+
+
+def test_chunked_host_pipeline(gpu, monkeypatch):
+    """Host buffers are pipelined in chunks over three streams; the result must
+    not depend on the chunking."""
+    P = gpu
+    left, right = P.synth_batch(0, 7, seed0=20, width=160, height=120)
+    cfg = P.PipelineConfig(coarsest_exp=2, finest_exp=1, patch_size=8, overlap=0.5,
+                           estimate_variance=True)
+    want = ["disparity", "disparity_valid", "depth", "depth_valid", "var_disp"]
+    with P.Matcher(cfg, 160, 120, 7) as m:
+        whole = m.run_batch(left, right, dtype=P.F64, want=want, stats=True)
+    monkeypatch.setenv("PSTEREO_CHUNK_PAIRS", "3")
+    with P.Matcher(cfg, 160, 120, 7) as m:
+        parts = m.run_batch(left, right, dtype=P.F64, want=want, stats=True)
+    for k in want + ["stats"]:
+        assert np.array_equal(whole[k], parts[k]), k
