@@ -13,6 +13,7 @@ namespace bdis {
 
 constexpr int kMaxPatch = 32;
 constexpr int kMaxWin = 33;  // 2 * PSTEREO_MAX_OFFSETS + 1
+constexpr int kRowPad = 32;  // zero slots either side of a staged right-view row
 
 enum Stage : uint8_t { kSkipped = 0, kSolved = 1, kConverged = 2, kAccepted = 3 };
 

@@ -86,31 +86,42 @@ __device__ __forceinline__ Ev eval_patch(const Rows<kSmem>& rw, int w, int s_rt,
   Ev ev;
   ev.jr = 0.0;
   ev.msq = CUDART_INF;
-  // Fully valid inputs: ONE predicated path for every lane -- columns outside
-  // the image are skipped (invalid samples, inc/image.hpp:55,68), the left tap
-  // is reused from the previous column when contiguous -- so lanes of a warp
-  // never split between code paths. Slot offsets are hoisted out of the rows.
-  if (S > 0 && !kValid) {
-    int offA[SA], offB[SA], offT[SA];
+  // Fully valid inputs, shared-memory rows: one predicated path. The in-bounds
+  // columns form a run [lo, hi] (x grows with i); when their taps are
+  // contiguous (x0_i = base + i -- always, unless x sits within rounding of an
+  // integer) sample i reads taps base+i, base+i+1 and reuses the left tap of
+  // column i+1. Out-of-image columns (invalid samples, inc/image.hpp:55,68)
+  // read the zero padding kRowPad slots either side of the row and are masked
+  // out of the sums. Lanes therefore never split between code paths.
+  int base = 0;
+  bool ctg = kSmem && !kValid && S > 0 && inb != 0;
+  if (ctg) {
+    const int lo = __ffs(inb) - 1;
+    base = cxi[0] - 0;
 #pragma unroll
-    for (int i = 0; i < SA; ++i) {
-      offA[i] = rw.s4(cxi[i]);
-      offB[i] = rw.s4(cxi[i] + 1);
-      offT[i] = rw.s4(x0 + i);
-    }
+    for (int i = 0; i < SA; ++i)
+      if (i == lo) base = cxi[i] - i;
+#pragma unroll
+    for (int i = 0; i < SA; ++i)
+      if (((inb >> i) & 1u) && cxi[i] != base + i) ctg = false;
+  }
+  if (ctg) {
+    int offT[SA];
+#pragma unroll
+    for (int i = 0; i < SA; ++i) offT[i] = rw.s4(x0 + i);
     const int n = SA * __popc(inb);
     ev.n = n;
-    if (n == 0) return ev;
+    const int xb = base + kRowPad;  // smem column of tap `base`
     double sum = 0.0;
     const float* rr = rw.R + r0 * rw.rp;
 #pragma unroll 1
     for (int j = 0; j < SA; ++j, rr += rw.rp) {
-      double b = 0.0;
+      double a = (double)rr[rw.s4(xb)];
 #pragma unroll
       for (int i = 0; i < SA; ++i) {
-        const double a = ((contig >> i) & 1u) ? b : (double)rr[offA[i]];
-        b = (double)rr[offB[i]];
+        const double b = (double)rr[rw.s4(xb + i + 1)];
         const double v = __dadd_rn(__dmul_rn(comf[i], a), __dmul_rn(cfx[i], b));
+        a = b;
         if ((inb >> i) & 1u) sum = __dadd_rn(sum, v);
       }
     }
@@ -121,12 +132,12 @@ __device__ __forceinline__ Ev eval_patch(const Rows<kSmem>& rw, int w, int s_rt,
     const float* gr = rw.Gf + r0 * rw.fp;
 #pragma unroll 1
     for (int j = 0; j < SA; ++j, rr += rw.rp, lr += rw.fp, gr += rw.fp) {
-      double b = 0.0;
+      double a = (double)rr[rw.s4(xb)];
 #pragma unroll
       for (int i = 0; i < SA; ++i) {
-        const double a = ((contig >> i) & 1u) ? b : (double)rr[offA[i]];
-        b = (double)rr[offB[i]];
+        const double b = (double)rr[rw.s4(xb + i + 1)];
         const double v = __dadd_rn(__dmul_rn(comf[i], a), __dmul_rn(cfx[i], b));
+        a = b;
         const double t = __dsub_rn((double)lr[offT[i]], mean);
         const double r = __dsub_rn(__dsub_rn(v, rmean), t);
         const double gv = (double)gr[offT[i]];
@@ -140,7 +151,9 @@ __device__ __forceinline__ Ev eval_patch(const Rows<kSmem>& rw, int w, int s_rt,
     ev.jr = jr;
     return ev;
   }
-  // Validity masks (or a runtime patch size): per-sample predicates.
+  // Validity masks, a runtime patch size, non-contiguous taps or global rows:
+  // per-sample predicates.
+  const int xo = kSmem ? kRowPad : 0;
   int n = 0;
   double sum = 0.0;
 #pragma unroll 1
@@ -150,8 +163,8 @@ __device__ __forceinline__ Ev eval_patch(const Rows<kSmem>& rw, int w, int s_rt,
 #pragma unroll
     for (int i = 0; i < SA; ++i) {
       if (S == 0 && i >= s) break;
-      const double a = (contig >> i) & 1u ? b : (double)rr[rw.s4(cxi[i])];
-      b = (double)rr[rw.s4(cxi[i] + 1)];
+      const double a = (double)rr[rw.s4(xo + cxi[i])];
+      b = (double)rr[rw.s4(xo + cxi[i] + 1)];
       const double v = __dadd_rn(__dmul_rn(comf[i], a), __dmul_rn(cfx[i], b));
       bool use = (inb >> i) & 1u;
       if (kValid)
@@ -176,8 +189,8 @@ __device__ __forceinline__ Ev eval_patch(const Rows<kSmem>& rw, int w, int s_rt,
 #pragma unroll
     for (int i = 0; i < SA; ++i) {
       if (S == 0 && i >= s) break;
-      const double a = (contig >> i) & 1u ? b : (double)rr[rw.s4(cxi[i])];
-      b = (double)rr[rw.s4(cxi[i] + 1)];
+      const double a = (double)rr[rw.s4(xo + cxi[i])];
+      b = (double)rr[rw.s4(xo + cxi[i] + 1)];
       bool use = (inb >> i) & 1u;
       if (kValid)
         use = use && rw.lq[(r0 + j) * rw.bp + x0 + i] && rw.rq[(r0 + j) * rw.bp + cxi[i]];
@@ -241,8 +254,10 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
     // ---- stage the band (coalesced global reads, padded shared writes)
     const float* gR = L.rpad + pair * (long long)(w + 1) * h + (long long)ylo * (w + 1);
     for (int r = 0; r < nrows; ++r) {
-      for (int x = tid; x <= w; x += nt)
-        sR[r * bp.rpitch + Rows<true>::s4(x)] = gR[(long long)r * (w + 1) + x];
+      // right row with kRowPad zero slots either side (x in [-kRowPad, w + kRowPad])
+      for (int x = tid - kRowPad; x <= w + kRowPad; x += nt)
+        sR[r * bp.rpitch + Rows<true>::s4(x + kRowPad)] =
+            (x >= 0 && x <= w) ? gR[(long long)r * (w + 1) + x] : 0.0f;
       const float* gl = L.left + pbase + (long long)(ylo + r) * w;
       const float* gg = L.grad + pbase + (long long)(ylo + r) * w;
       for (int x = tid; x < w; x += nt) {
@@ -498,11 +513,13 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
 
 // ---------------------------------------------------------------------------
 
+static inline int pad4_host(int x) { return x + (x >> 5); }
+
 BandPlan plan_bands(const Level& L, const PatchParams& pp, int max_smem_per_cta) {
   const Grid& g = L.g;
   BandPlan bp{};
   const bool valid = !pp.all_valid;
-  bp.rpitch = (L.w + (L.w >> 5)) + 1;           // slots for x in [0, w]
+  bp.rpitch = pad4_host(L.w + 2 * kRowPad) + 1;   // slots for x in [-kRowPad, w + kRowPad]
   bp.fpitch = (L.w - 1 + ((L.w - 1) >> 5)) + 1;  // slots for x in [0, w-1]
   bp.bpitch = valid ? L.w : 0;
   auto bytes_for = [&](int rb) {
