@@ -107,8 +107,15 @@ __device__ __forceinline__ Ev eval_patch(const Rows<kSmem>& rw, int w, int s_rt,
   }
   if (ctg) {
     int offT[SA];
+    double mo[SA], mf[SA], mk[SA];  // weights (1-fx, fx) and column mask, 0 when masked
 #pragma unroll
-    for (int i = 0; i < SA; ++i) offT[i] = rw.s4(x0 + i);
+    for (int i = 0; i < SA; ++i) {
+      offT[i] = rw.s4(x0 + i);
+      const bool in = (inb >> i) & 1u;
+      mo[i] = in ? comf[i] : 0.0;
+      mf[i] = in ? cfx[i] : 0.0;
+      mk[i] = in ? 1.0 : 0.0;
+    }
     const int n = SA * __popc(inb);
     ev.n = n;
     const int xb = base + kRowPad;  // smem column of tap `base`
@@ -120,9 +127,9 @@ __device__ __forceinline__ Ev eval_patch(const Rows<kSmem>& rw, int w, int s_rt,
 #pragma unroll
       for (int i = 0; i < SA; ++i) {
         const double b = (double)rr[rw.s4(xb + i + 1)];
-        const double v = __dadd_rn(__dmul_rn(comf[i], a), __dmul_rn(cfx[i], b));
+        // masked columns have cfx = comf = 0: v = +-0 leaves the sum unchanged
+        sum = __dadd_rn(sum, __dadd_rn(__dmul_rn(mo[i], a), __dmul_rn(mf[i], b)));
         a = b;
-        if ((inb >> i) & 1u) sum = __dadd_rn(sum, v);
       }
     }
     const double rmean = __ddiv_rn(sum, (double)n);
@@ -136,15 +143,13 @@ __device__ __forceinline__ Ev eval_patch(const Rows<kSmem>& rw, int w, int s_rt,
 #pragma unroll
       for (int i = 0; i < SA; ++i) {
         const double b = (double)rr[rw.s4(xb + i + 1)];
-        const double v = __dadd_rn(__dmul_rn(comf[i], a), __dmul_rn(cfx[i], b));
+        const double v = __dadd_rn(__dmul_rn(mo[i], a), __dmul_rn(mf[i], b));
         a = b;
         const double t = __dsub_rn((double)lr[offT[i]], mean);
-        const double r = __dsub_rn(__dsub_rn(v, rmean), t);
-        const double gv = (double)gr[offT[i]];
-        if ((inb >> i) & 1u) {
-          ssr = __dadd_rn(ssr, __dmul_rn(r, r));
-          jr = __dadd_rn(jr, __dmul_rn(gv, r));
-        }
+        // r * 1 == r; masked columns: r * 0 = +-0 adds nothing to ssr / jr
+        const double r = __dmul_rn(__dsub_rn(__dsub_rn(v, rmean), t), mk[i]);
+        ssr = __dadd_rn(ssr, __dmul_rn(r, r));
+        jr = __dadd_rn(jr, __dmul_rn((double)gr[offT[i]], r));
       }
     }
     ev.msq = __ddiv_rn(ssr, (double)n);
@@ -253,17 +258,23 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
   if (kSmem) {
     // ---- stage the band (coalesced global reads, padded shared writes)
     const float* gR = L.rpad + pair * (long long)(w + 1) * h + (long long)ylo * (w + 1);
+    // right rows with kRowPad zero slots either side (x in [-kRowPad, w + kRowPad])
+    const int rw2 = w + 1 + 2 * kRowPad;
+#pragma unroll 4
+    for (int q = tid; q < nrows * rw2; q += nt) {
+      const int r = q / rw2, x = q - r * rw2 - kRowPad;
+      sR[r * bp.rpitch + Rows<true>::s4(x + kRowPad)] =
+          (x >= 0 && x <= w) ? __ldg(gR + (long long)r * (w + 1) + x) : 0.0f;
+    }
+    const float* gl0 = L.left + pbase + (long long)ylo * w;
+    const float* gg0 = L.grad + pbase + (long long)ylo * w;
+#pragma unroll 4
+    for (int q = tid; q < nrows * w; q += nt) {
+      const int r = q / w, x = q - r * w;
+      sL[r * bp.fpitch + Rows<true>::s4(x)] = __ldg(gl0 + q);
+      sG[r * bp.fpitch + Rows<true>::s4(x)] = __ldg(gg0 + q);
+    }
     for (int r = 0; r < nrows; ++r) {
-      // right row with kRowPad zero slots either side (x in [-kRowPad, w + kRowPad])
-      for (int x = tid - kRowPad; x <= w + kRowPad; x += nt)
-        sR[r * bp.rpitch + Rows<true>::s4(x + kRowPad)] =
-            (x >= 0 && x <= w) ? gR[(long long)r * (w + 1) + x] : 0.0f;
-      const float* gl = L.left + pbase + (long long)(ylo + r) * w;
-      const float* gg = L.grad + pbase + (long long)(ylo + r) * w;
-      for (int x = tid; x < w; x += nt) {
-        sL[r * bp.fpitch + Rows<true>::s4(x)] = gl[x];
-        sG[r * bp.fpitch + Rows<true>::s4(x)] = gg[x];
-      }
       if (kValid) {
         const uint8_t* lq = L.lq + pbase + (long long)(ylo + r) * w;
         const uint8_t* rq = L.rq + pbase + (long long)(ylo + r) * w;
