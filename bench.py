@@ -209,7 +209,11 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     B = args.batch
     cfg = P.PipelineConfig.baseline(0)
-    left, right = P.synth_batch(0, B, seed0=rank * B, threads=max(1, host_cores() // max(world, 1)))
+    from paper_2205_03133_b200.shard import max_over_ranks, weak_shard
+
+    shard = weak_shard(B, rank, world)  # pairs are independent: no exchange
+    left, right = P.synth_batch(0, shard.count, seed0=shard.start,
+                                threads=max(1, host_cores() // max(world, 1)))
     dev = torch.device("cuda", local)
     dl = torch.from_numpy(left).to(dev)
     dr = torch.from_numpy(right).to(dev)
@@ -251,10 +255,7 @@ def run_ours(args):
     ms = e0.elapsed_time(e1)
     stages, calls = m.stage_times()
     m.set_profiling(False)
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    ms_max = max_over_ranks(ms, device=dev)
     value = world * B * args.steps / (ms_max / 1e3)
 
     # ---- e2e through the public ABI with pinned host buffers
@@ -278,10 +279,8 @@ def run_ours(args):
         step_e2e()
     torch.cuda.synchronize(dev)
     e2e_s = time.perf_counter() - t0
-    te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = world * B * e2e_steps / float(te.item()) if e2e_steps else None
+    e2e_s = max_over_ranks(e2e_s, device=dev)
+    e2e_value = world * B * e2e_steps / e2e_s if e2e_steps else None
     # parity spot check of the e2e output against the device-resident run
     if e2e_steps:
         assert torch.equal(hd, disp.cpu()) and torch.equal(hv, valid.cpu()), "e2e output differs"
