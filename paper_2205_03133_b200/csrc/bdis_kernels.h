@@ -59,7 +59,7 @@ __host__ __device__ inline BandLayout band_layout(int rows, int rpitch, int fpit
     o += bytes;
     return r;
   };
-  l.oR = take(size_t(rows) * rpitch * 4, 16);
+  l.oR = take(size_t(rows) * rpitch * 8, 16);
   l.oL = take(size_t(rows) * fpitch * 4, 16);
   l.oG = take(size_t(rows) * fpitch * 4, 16);
   l.oLQ = take(valid ? size_t(rows) * bpitch : 0, 16);

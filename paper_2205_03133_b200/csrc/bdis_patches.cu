@@ -8,9 +8,10 @@
 //
 // B200 mapping
 //   * one CTA per (pair, band of `rb` patch rows); the band's rows of the
-//     right view, left view and gradient (fp32) are staged in shared memory
-//     once, padded (x + x/32) so the stride-`stride` accesses of neighbouring
-//     patches hit distinct banks;
+//     right view (converted to fp64 once), left view and gradient (fp32) are
+//     staged in shared memory, padded (x + x/16 for 8-byte, x + x/32 for
+//     4-byte slots) so the stride-`stride` accesses of neighbouring patches hit
+//     distinct banks;
 //   * a thread owns one patch at a time and sums its samples in the
 //     reference's sequential row-major order -- that is what makes every sum
 //     bit-identical to the CPU (a warp tree reduction would reorder them);
@@ -30,6 +31,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cstdlib>
 #include <math.h>
 #include <math_constants.h>
@@ -49,13 +51,17 @@ struct Ev {
 
 template <bool kSmem>
 struct Rows {
-  const float* R;    // right view, rows of (w+1)
+  // right view rows: fp64 in shared memory (converted once at staging, padded
+  // x + x/16 for 8-byte slots), fp32 rows of (w+1) in global memory
+  using RT = typename std::conditional<kSmem, double, float>::type;
+  const RT* R;
   const float* Lf;   // left view
   const float* Gf;   // gradient of the left view
   const uint8_t* lq; // 4-tap validity (kValid only)
   const uint8_t* rq;
   int rp, fp, bp;    // row pitches (slots)
   __device__ __forceinline__ static int s4(int x) { return kSmem ? x + (x >> 5) : x; }
+  __device__ __forceinline__ static int s8(int x) { return kSmem ? x + (x >> 4) : x; }
 };
 
 // eval_patch_residual (src/lk_solver.cpp:38-81) of a lattice patch whose
@@ -120,13 +126,13 @@ __device__ __forceinline__ Ev eval_patch(const Rows<kSmem>& rw, int w, int s_rt,
     ev.n = n;
     const int xb = base + kRowPad;  // smem column of tap `base`
     double sum = 0.0;
-    const float* rr = rw.R + r0 * rw.rp;
+    const auto* rr = rw.R + r0 * rw.rp;
 #pragma unroll 1
     for (int j = 0; j < SA; ++j, rr += rw.rp) {
-      double a = (double)rr[rw.s4(xb)];
+      double a = (double)rr[rw.s8(xb)];
 #pragma unroll
       for (int i = 0; i < SA; ++i) {
-        const double b = (double)rr[rw.s4(xb + i + 1)];
+        const double b = (double)rr[rw.s8(xb + i + 1)];
         // masked columns have cfx = comf = 0: v = +-0 leaves the sum unchanged
         sum = __dadd_rn(sum, __dadd_rn(__dmul_rn(mo[i], a), __dmul_rn(mf[i], b)));
         a = b;
@@ -139,10 +145,10 @@ __device__ __forceinline__ Ev eval_patch(const Rows<kSmem>& rw, int w, int s_rt,
     const float* gr = rw.Gf + r0 * rw.fp;
 #pragma unroll 1
     for (int j = 0; j < SA; ++j, rr += rw.rp, lr += rw.fp, gr += rw.fp) {
-      double a = (double)rr[rw.s4(xb)];
+      double a = (double)rr[rw.s8(xb)];
 #pragma unroll
       for (int i = 0; i < SA; ++i) {
-        const double b = (double)rr[rw.s4(xb + i + 1)];
+        const double b = (double)rr[rw.s8(xb + i + 1)];
         const double v = __dadd_rn(__dmul_rn(mo[i], a), __dmul_rn(mf[i], b));
         a = b;
         const double t = __dsub_rn((double)lr[offT[i]], mean);
@@ -163,13 +169,13 @@ __device__ __forceinline__ Ev eval_patch(const Rows<kSmem>& rw, int w, int s_rt,
   double sum = 0.0;
 #pragma unroll 1
   for (int j = 0; j < s; ++j) {
-    const float* rr = rw.R + (r0 + j) * rw.rp;
+    const auto* rr = rw.R + (r0 + j) * rw.rp;
     double b = 0.0;
 #pragma unroll
     for (int i = 0; i < SA; ++i) {
       if (S == 0 && i >= s) break;
-      const double a = (double)rr[rw.s4(xo + cxi[i])];
-      b = (double)rr[rw.s4(xo + cxi[i] + 1)];
+      const double a = (double)rr[rw.s8(xo + cxi[i])];
+      b = (double)rr[rw.s8(xo + cxi[i] + 1)];
       const double v = __dadd_rn(__dmul_rn(comf[i], a), __dmul_rn(cfx[i], b));
       bool use = (inb >> i) & 1u;
       if (kValid)
@@ -187,15 +193,15 @@ __device__ __forceinline__ Ev eval_patch(const Rows<kSmem>& rw, int w, int s_rt,
   double ssr = 0.0, jr = 0.0;
 #pragma unroll 1
   for (int j = 0; j < s; ++j) {
-    const float* rr = rw.R + (r0 + j) * rw.rp;
+    const auto* rr = rw.R + (r0 + j) * rw.rp;
     const float* lr = rw.Lf + (r0 + j) * rw.fp;
     const float* gr = rw.Gf + (r0 + j) * rw.fp;
     double b = 0.0;
 #pragma unroll
     for (int i = 0; i < SA; ++i) {
       if (S == 0 && i >= s) break;
-      const double a = (double)rr[rw.s4(xo + cxi[i])];
-      b = (double)rr[rw.s4(xo + cxi[i] + 1)];
+      const double a = (double)rr[rw.s8(xo + cxi[i])];
+      b = (double)rr[rw.s8(xo + cxi[i] + 1)];
       bool use = (inb >> i) & 1u;
       if (kValid)
         use = use && rw.lq[(r0 + j) * rw.bp + x0 + i] && rw.rq[(r0 + j) * rw.bp + cxi[i]];
@@ -236,7 +242,7 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
   // ---- shared-memory carve-up (mirrors band_layout on the host)
   const BandLayout lay = band_layout(bp.use_smem ? bp.smem_rows : 0, bp.rpitch, bp.fpitch,
                                      bp.bpitch, bp.npb, nwin, kValid);
-  float* sR = (float*)(smem + lay.oR);
+  double* sR = (double*)(smem + lay.oR);
   float* sL = (float*)(smem + lay.oL);
   float* sG = (float*)(smem + lay.oG);
   uint8_t* sLQ = smem + lay.oLQ;
@@ -255,7 +261,7 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
   const long long pbase = pair * L.plane;
   Rows<kSmem> rw;
   int rofs;  // row index of image row y in rw is y - rofs
-  if (kSmem) {
+  if constexpr (kSmem) {
     // ---- stage the band (coalesced global reads, padded shared writes)
     const float* gR = L.rpad + pair * (long long)(w + 1) * h + (long long)ylo * (w + 1);
     // right rows with kRowPad zero slots either side (x in [-kRowPad, w + kRowPad])
@@ -263,8 +269,8 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
 #pragma unroll 4
     for (int q = tid; q < nrows * rw2; q += nt) {
       const int r = q / rw2, x = q - r * rw2 - kRowPad;
-      sR[r * bp.rpitch + Rows<true>::s4(x + kRowPad)] =
-          (x >= 0 && x <= w) ? __ldg(gR + (long long)r * (w + 1) + x) : 0.0f;
+      sR[r * bp.rpitch + Rows<true>::s8(x + kRowPad)] =
+          (x >= 0 && x <= w) ? (double)__ldg(gR + (long long)r * (w + 1) + x) : 0.0;
     }
     const float* gl0 = L.left + pbase + (long long)ylo * w;
     const float* gg0 = L.grad + pbase + (long long)ylo * w;
@@ -525,12 +531,13 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
 // ---------------------------------------------------------------------------
 
 static inline int pad4_host(int x) { return x + (x >> 5); }
+static inline int pad8_host(int x) { return x + (x >> 4); }
 
 BandPlan plan_bands(const Level& L, const PatchParams& pp, int max_smem_per_cta) {
   const Grid& g = L.g;
   BandPlan bp{};
   const bool valid = !pp.all_valid;
-  bp.rpitch = pad4_host(L.w + 2 * kRowPad) + 1;   // slots for x in [-kRowPad, w + kRowPad]
+  bp.rpitch = pad8_host(L.w + 2 * kRowPad) + 1;   // slots for x in [-kRowPad, w + kRowPad]
   bp.fpitch = (L.w - 1 + ((L.w - 1) >> 5)) + 1;  // slots for x in [0, w-1]
   bp.bpitch = valid ? L.w : 0;
   auto bytes_for = [&](int rb) {
