@@ -685,10 +685,9 @@ int run_device(pstereo_ctx* ctx, const std::vector<LevelGeom>& geo, int n, int W
   CK(ctx->farea.ensure(fnp));
   FinestBufs fb{ctx->fdisp.p, ctx->fprob.p, prm.estimate_variance ? ctx->fvar.p : nullptr,
                 ctx->fmvalid.p, ctx->fmask.p, ctx->flabel.p};
-  launch_fuse_finest(F, fb, ctx->mask.p, prm.estimate_variance, prm.pixel_threshold, n, s);
-  ++ctx->launches;
   CK(cudaMemsetAsync(ctx->farea.p, 0, fnp * sizeof(int), s));
-  launch_ccl(F.w, F.h, F.plane, W, H, fe, ctx->fmask.p, ctx->flabel.p, ctx->farea.p, n, s);
+  launch_fuse_ccl(F, fb, ctx->mask.p, prm.estimate_variance, prm.pixel_threshold, W, H, fe,
+                  ctx->farea.p, n, s);
   ctx->launches += 3;
 
   OutputArgs oa;

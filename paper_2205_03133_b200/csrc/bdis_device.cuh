@@ -13,7 +13,6 @@ namespace bdis {
 
 constexpr int kMaxPatch = 32;
 constexpr int kMaxWin = 33;  // 2 * PSTEREO_MAX_OFFSETS + 1
-constexpr int kRowPad = 32;  // zero slots either side of a staged right-view row
 
 enum Stage : uint8_t { kSkipped = 0, kSolved = 1, kConverged = 2, kAccepted = 3 };
 
@@ -72,40 +71,70 @@ struct Fused {
   double sw, swu, swp, sw2s;
 };
 
-template <bool kProb, bool kVar>
-__device__ __forceinline__ Fused gather(const Level& P, long long pair, int x,
-                                        int y, const double* __restrict__ mask) {
-  const Grid& g = P.g;
+// Global-memory records of one level (the default accessor of gather_with).
+struct GlobalRecords {
+  const Level& P;
+  long long base;
+  __device__ __forceinline__ uint8_t stage(int ky, int kx) const {
+    return P.stage[base + (long long)ky * P.g.nx + kx];
+  }
+  __device__ __forceinline__ double prob(int ky, int kx) const {
+    return P.prob[base + (long long)ky * P.g.nx + kx];
+  }
+  __device__ __forceinline__ double u(int ky, int kx) const {
+    return P.u[base + (long long)ky * P.g.nx + kx];
+  }
+  __device__ __forceinline__ double sigma(int ky, int kx) const {
+    return P.sigma[base + (long long)ky * P.g.nx + kx];
+  }
+};
+
+template <bool kProb, bool kVar, typename Rec>
+__device__ __forceinline__ Fused gather_with(const Grid& g, const Rec& rec, int x, int y,
+                                             const double* __restrict__ mask) {
   const int s = g.size, st = g.stride;
-  const long long base = pair * (long long)g.nx * g.ny;
   Fused f{0.0, 0.0, 0.0, 0.0};
   const int ky_lo = (y - s + 1 <= 0) ? 0 : (y - s + 1 + st - 1) / st;
   const int ky_hi = min(g.ny - 2, y / st);
   const int kx_lo = (x - s + 1 <= 0) ? 0 : (x - s + 1 + st - 1) / st;
   const int kx_hi = min(g.nx - 2, x / st);
   const bool last_x = x >= g.lastx0;
-  auto add = [&](long long idx, double m) {
-    if (P.stage[idx] != kAccepted) return;
-    const double pr = P.prob[idx];
+  auto add = [&](int ky, int kx, double m) {
+    if (rec.stage(ky, kx) != kAccepted) return;
+    const double pr = rec.prob(ky, kx);
     const double w = __dmul_rn(pr, m);
     f.sw = __dadd_rn(f.sw, w);
-    f.swu = __dadd_rn(f.swu, __dmul_rn(w, P.u[idx]));
+    f.swu = __dadd_rn(f.swu, __dmul_rn(w, rec.u(ky, kx)));
     if (kProb) f.swp = __dadd_rn(f.swp, __dmul_rn(w, pr));
     if (kVar) {
-      const double sk = P.sigma[idx];
+      const double sk = rec.sigma(ky, kx);
       f.sw2s = __dadd_rn(f.sw2s, __dmul_rn(__dmul_rn(__dmul_rn(w, w), sk), sk));
     }
   };
   auto row = [&](int ky, int y0) {
-    const int j = y - y0;
-    const double* mrow = mask + j * s;
-    const long long rbase = base + (long long)ky * g.nx;
-    for (int kx = kx_lo; kx <= kx_hi; ++kx) add(rbase + kx, mrow[x - kx * st]);
-    if (last_x) add(rbase + g.nx - 1, mrow[x - g.lastx0]);
+    const double* mrow = mask + (y - y0) * s;
+    for (int kx = kx_lo; kx <= kx_hi; ++kx) add(ky, kx, mrow[x - kx * st]);
+    if (last_x) add(ky, g.nx - 1, mrow[x - g.lastx0]);
   };
   for (int ky = ky_lo; ky <= ky_hi; ++ky) row(ky, ky * st);
   if (y >= g.lasty0) row(g.ny - 1, g.lasty0);
   return f;
+}
+
+// Patches of a level covering pixel columns [xa, xb] form one contiguous index
+// range (the clamped last patch has the largest start); same for rows.
+__device__ __forceinline__ void covering_range(int a, int b, int n, int s, int st, int last0,
+                                               int* k0, int* k1) {
+  *k0 = (a - s + 1 <= 0) ? 0 : min(n - 1, (a - s + 1 + st - 1) / st);
+  *k1 = b >= last0 ? n - 1 : min(n - 2, b / st);
+  if (*k1 < *k0) *k1 = *k0;
+}
+
+template <bool kProb, bool kVar>
+__device__ __forceinline__ Fused gather(const Level& P, long long pair, int x, int y,
+                                        const double* __restrict__ mask) {
+  const GlobalRecords rec{P, pair * (long long)P.g.nx * P.g.ny};
+  return gather_with<kProb, kVar>(P.g, rec, x, y, mask);
 }
 
 // estimate_patch_variance (src/depth_variance.cpp:94-170) on the window

@@ -10,7 +10,7 @@
 //                                                      k_patches
 //   fuse_level (finest) + filter threshold
 //                           src/coarse_to_fine.cpp:101-150,
-//                           src/depth_variance.cpp:78-86  k_fuse_finest
+//                           src/depth_variance.cpp:78-86  k_fuse_ccl_local
 //   remove_small_components src/depth_variance.cpp:43-76  k_ccl_*
 //   upsample_to_full + disparity_to_depth
 //                           src/coarse_to_fine.cpp:166-180,328-337,
@@ -252,37 +252,10 @@ cudaError_t launch_pyramid(const PyrArgs& a, bool u8, cudaStream_t s) {
 // --------------------------------------------------------------------------
 // finest level: fusion, filter, components, output
 
-// fuse_level at the finest level (src/coarse_to_fine.cpp:101-150) plus the
-// probability threshold of filter_validity (src/depth_variance.cpp:81-86).
-__global__ void k_fuse_finest(Level L, FinestBufs fb, const double* __restrict__ mask,
-                              int want_var, double threshold) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= L.w * L.h) return;
-  const long long pair = blockIdx.y;
-  const int x = i % L.w, y = i / L.w;
-  Fused f;
-  if (want_var) f = gather<true, true>(L, pair, x, y, mask);
-  else f = gather<true, false>(L, pair, x, y, mask);
-  const long long o = pair * L.plane + i;
-  const bool valid = !(f.sw <= 0.0);
-  double d = 0.0, p = 0.0, v = 0.0;
-  if (valid) {
-    d = __ddiv_rn(f.swu, f.sw);
-    p = __ddiv_rn(f.swp, f.sw);
-    if (want_var) v = __ddiv_rn(f.sw2s, __dmul_rn(f.sw, f.sw));
-  }
-  fb.disp[o] = d;
-  fb.prob[o] = p;
-  if (want_var) fb.var[o] = v;
-  fb.mvalid[o] = valid ? 1 : 0;
-  const bool keep = valid && !(p < threshold);
-  fb.mask[o] = keep ? 1 : 0;
-}
-
 // 4-connected components of the thresholded finest mask (the full-resolution
 // mask is its block replication, so components and areas carry over with
 // per-pixel area weights, src/depth_variance.cpp:43-92). Three passes:
-//   k_ccl_local  -- union-find inside a 32x16 tile in shared memory, every
+//   k_fuse_ccl_local -- (after the fusion) union-find inside a 32x16 tile in smem, every
 //                   pixel labelled with its tile-local root (a global index);
 //   k_ccl_border -- unions across tile borders in global memory;
 //   k_ccl_final  -- path compression + warp-aggregated component areas.
@@ -317,39 +290,99 @@ __device__ __forceinline__ void uf_union(Ptr lab, int* raw, int a, int b) {
   }
 }
 
-// Tile rows are warps (kTileW == 32): a pixel starts as the index of the first
-// pixel of its horizontal run (ballot bit tricks), then vertically adjacent
-// runs are merged with union-find (path halving) in shared memory.
-__global__ void __launch_bounds__(kTileW * kTileH) k_ccl_local(int w, int h, long long plane,
-                                                             const uint8_t* __restrict__ mask,
-                                                             int* __restrict__ lab) {
-  static_assert(kTileW == 32, "tile rows are warps");
+// Shared-memory copy of the patch records covering one tile.
+struct TileRecords {
+  const uint8_t* st;
+  const double* pr;
+  const double* uu;
+  const double* sg;
+  int ky0, kx0, ncol;
+  __device__ __forceinline__ int at(int ky, int kx) const { return (ky - ky0) * ncol + (kx - kx0); }
+  __device__ __forceinline__ uint8_t stage(int ky, int kx) const { return st[at(ky, kx)]; }
+  __device__ __forceinline__ double prob(int ky, int kx) const { return pr[at(ky, kx)]; }
+  __device__ __forceinline__ double u(int ky, int kx) const { return uu[at(ky, kx)]; }
+  __device__ __forceinline__ double sigma(int ky, int kx) const { return sg[at(ky, kx)]; }
+};
+
+constexpr int kTileRec = 160;  // max covering patches per 32x16 tile (stride >= 2, s <= 32)
+
+// fuse_level at the finest level (src/coarse_to_fine.cpp:101-150) with the
+// probability threshold of filter_validity (src/depth_variance.cpp:81-86),
+// then the tile-local pass of the component labelling -- one CTA per 32x16
+// tile. The records of the covering patches are staged in shared memory and
+// each pixel gathers them in ascending patch index (fuse_level's order).
+template <bool kVar>
+__global__ void __launch_bounds__(kTileW * kTileH) k_fuse_ccl_local(
+    Level L, FinestBufs fb, const double* __restrict__ mask, double threshold) {
   __shared__ int sl[kTileW * kTileH];
+  __shared__ double s_pr[kTileRec], s_u[kTileRec], s_sg[kTileRec];
+  __shared__ uint8_t s_st[kTileRec];
+  const Grid& g = L.g;
+  const int w = L.w, h = L.h;
   const int tiles_x = (w + kTileW - 1) / kTileW;
   const int tx0 = (blockIdx.x % tiles_x) * kTileW, ty0 = (blockIdx.x / tiles_x) * kTileH;
+  const long long pair = blockIdx.y;
   const int t = threadIdx.x, lx = t % kTileW, ly = t / kTileW;
   const int x = tx0 + lx, y = ty0 + ly;
-  const long long base = blockIdx.y * plane;
-  const bool m = x < w && y < h && mask[base + (long long)y * w + x];
-  const unsigned bits = __ballot_sync(0xffffffffu, m);
+  int kx0, kx1, ky0, ky1;
+  covering_range(tx0, min(tx0 + kTileW, w) - 1, g.nx, g.size, g.stride, g.lastx0, &kx0, &kx1);
+  covering_range(ty0, min(ty0 + kTileH, h) - 1, g.ny, g.size, g.stride, g.lasty0, &ky0, &ky1);
+  const int ncol = kx1 - kx0 + 1, nrec = ncol * (ky1 - ky0 + 1);
+  const long long rbase = pair * (long long)g.nx * g.ny;
+  const bool staged = nrec <= kTileRec;
+  if (staged) {
+    for (int q = t; q < nrec; q += blockDim.x) {
+      const long long r = rbase + (long long)(ky0 + q / ncol) * g.nx + kx0 + q % ncol;
+      s_st[q] = L.stage[r];
+      s_pr[q] = L.prob[r];
+      s_u[q] = L.u[r];
+      if (kVar) s_sg[q] = L.sigma[r];
+    }
+  }
+  __syncthreads();
+  bool keep = false;
+  if (x < w && y < h) {
+    Fused f;
+    if (staged) {
+      const TileRecords rec{s_st, s_pr, s_u, s_sg, ky0, kx0, ncol};
+      f = gather_with<true, kVar>(g, rec, x, y, mask);
+    } else {
+      f = gather<true, kVar>(L, pair, x, y, mask);
+    }
+    const long long o = pair * L.plane + (long long)y * w + x;
+    const bool valid = !(f.sw <= 0.0);
+    double d = 0.0, p = 0.0, v = 0.0;
+    if (valid) {
+      d = __ddiv_rn(f.swu, f.sw);
+      p = __ddiv_rn(f.swp, f.sw);
+      if (kVar) v = __ddiv_rn(f.sw2s, __dmul_rn(f.sw, f.sw));
+    }
+    fb.disp[o] = d;
+    fb.prob[o] = p;
+    if (kVar) fb.var[o] = v;
+    fb.mvalid[o] = valid ? 1 : 0;
+    keep = valid && !(p < threshold);
+    fb.mask[o] = keep ? 1 : 0;
+  }
+  // ---- tile-local components: run labels (ballot bit tricks) + union-find
+  const unsigned bits = __ballot_sync(0xffffffffu, keep);
   const unsigned starts = bits & ~(bits << 1);
-  const unsigned upto = starts & (0xffffffffu >> (31 - lx));  // run starts at lanes <= lx
-  sl[t] = m ? ly * kTileW + (31 - __clz(upto)) : -1;
+  const unsigned upto = starts & (0xffffffffu >> (31 - lx));
+  sl[t] = keep ? ly * kTileW + (31 - __clz(upto)) : -1;
   __syncthreads();
   volatile int* vl = sl;
-  // one union per vertically overlapping pixel pair; runs make chains short
-  if (m && ly > 0 && sl[t - kTileW] >= 0) {
+  if (keep && ly > 0 && sl[t - kTileW] >= 0) {
     int a = sl[t], b = sl[t - kTileW];
     for (;;) {
       while (vl[a] != a) {
-        const int g = vl[vl[a]];
-        vl[a] = g;
-        a = g;
+        const int gg = vl[vl[a]];
+        vl[a] = gg;
+        a = gg;
       }
       while (vl[b] != b) {
-        const int g = vl[vl[b]];
-        vl[b] = g;
-        b = g;
+        const int gg = vl[vl[b]];
+        vl[b] = gg;
+        b = gg;
       }
       if (a == b) break;
       if (a < b) {
@@ -363,9 +396,9 @@ __global__ void __launch_bounds__(kTileW * kTileH) k_ccl_local(int w, int h, lon
     }
   }
   __syncthreads();
-  if (m) {
+  if (keep) {
     const int r = uf_find(vl, t);
-    lab[base + (long long)y * w + x] = (ty0 + r / kTileW) * w + tx0 + r % kTileW;
+    fb.label[pair * L.plane + (long long)y * w + x] = (ty0 + r / kTileW) * w + tx0 + r % kTileW;
   }
 }
 
@@ -534,21 +567,21 @@ void launch_level_tables(const Level& L, int n_pairs, cudaStream_t s) {
   k_level_tables<<<grid, 256, 0, s>>>(L);
 }
 
-void launch_fuse_finest(const Level& L, const FinestBufs& fb, const double* mask,
-                        int want_var, double threshold, int n_pairs, cudaStream_t s) {
-  dim3 grid(blocks_for((long long)L.w * L.h, 256), n_pairs);
-  k_fuse_finest<<<grid, 256, 0, s>>>(L, fb, mask, want_var, threshold);
-}
-
-void launch_ccl(int w, int h, long long plane, int full_w, int full_h, int e,
-                const uint8_t* mask, int* lab, int* area, int n_pairs, cudaStream_t s) {
-  const int tiles = ((w + kTileW - 1) / kTileW) * ((h + kTileH - 1) / kTileH);
-  k_ccl_local<<<dim3(tiles, n_pairs), kTileW * kTileH, 0, s>>>(w, h, plane, mask, lab);
+void launch_fuse_ccl(const Level& L, const FinestBufs& fb, const double* mask, int want_var,
+                     double threshold, int full_w, int full_h, int e, int* area, int n_pairs,
+                     cudaStream_t s) {
+  const int w = L.w, h = L.h;
+  const long long plane = L.plane;
   const int tx = (w + kTileW - 1) / kTileW, ty = (h + kTileH - 1) / kTileH;
+  if (want_var)
+    k_fuse_ccl_local<true><<<dim3(tx * ty, n_pairs), kTileW * kTileH, 0, s>>>(L, fb, mask, threshold);
+  else
+    k_fuse_ccl_local<false><<<dim3(tx * ty, n_pairs), kTileW * kTileH, 0, s>>>(L, fb, mask, threshold);
   const long long nb = (long long)(tx - 1) * h + (long long)(ty - 1) * w;
-  if (nb > 0) k_ccl_border<<<dim3(blocks_for(nb, 256), n_pairs), 256, 0, s>>>(w, h, plane, mask, lab);
-  dim3 grid(blocks_for((long long)w * h, 256), n_pairs);
-  k_ccl_final<<<grid, 256, 0, s>>>(w, h, plane, full_w, full_h, e, mask, lab, area);
+  if (nb > 0)
+    k_ccl_border<<<dim3(blocks_for(nb, 256), n_pairs), 256, 0, s>>>(w, h, plane, fb.mask, fb.label);
+  k_ccl_final<<<dim3(blocks_for((long long)w * h, 256), n_pairs), 256, 0, s>>>(
+      w, h, plane, full_w, full_h, e, fb.mask, fb.label, area);
 }
 
 void launch_output(const OutputArgs& a, int f64, int n_pairs, cudaStream_t s) {

@@ -35,6 +35,8 @@ struct BandPlan {
   int fpitch;      // smem slots per left/gradient row (floats)
   int bpitch;      // bytes per validity row
   int use_smem;    // 0: read the level tables from global memory
+  int r64;         // right rows staged as fp64 (else fp32, converted per tap)
+  int rpad;        // zero slots either side of a staged right row (= patch size)
   size_t smem_bytes;
   int npb;         // max patches per band = rb * nx
 };
@@ -50,7 +52,7 @@ struct BandLayout {
 };
 
 __host__ __device__ inline BandLayout band_layout(int rows, int rpitch, int fpitch, int bpitch,
-                                                  int npb, int nwin, bool valid) {
+                                                  int npb, int nwin, bool valid, bool r64) {
   BandLayout l;
   size_t o = 0;
   auto take = [&](size_t bytes, size_t align) {
@@ -59,7 +61,7 @@ __host__ __device__ inline BandLayout band_layout(int rows, int rpitch, int fpit
     o += bytes;
     return r;
   };
-  l.oR = take(size_t(rows) * rpitch * 8, 16);
+  l.oR = take(size_t(rows) * rpitch * (r64 ? 8 : 4), 16);
   l.oL = take(size_t(rows) * fpitch * 4, 16);
   l.oG = take(size_t(rows) * fpitch * 4, 16);
   l.oLQ = take(valid ? size_t(rows) * bpitch : 0, 16);
@@ -150,10 +152,10 @@ void launch_downsample(const float* sl, const uint8_t* slv, const float* sr,
 void launch_level_tables(const Level& L, int n_pairs, cudaStream_t s);
 cudaError_t launch_patches(const Level& L, const Level& P, const PatchParams& pp,
                            const BandPlan& bp, cudaStream_t s);
-void launch_fuse_finest(const Level& L, const FinestBufs& fb, const double* mask,
-                        int want_var, double threshold, int n_pairs, cudaStream_t s);
-void launch_ccl(int w, int h, long long plane, int full_w, int full_h, int e,
-                const uint8_t* mask, int* lab, int* area, int n_pairs, cudaStream_t s);
+// fuse_level (finest) + threshold + 4-connected components with area sums
+void launch_fuse_ccl(const Level& L, const FinestBufs& fb, const double* mask, int want_var,
+                     double threshold, int full_w, int full_h, int e, int* area, int n_pairs,
+                     cudaStream_t s);
 cudaError_t launch_debug_eval(const Level& L, int size, int all_valid, int nq, const int* qx,
                               const int* qy, const double* qu, double* msq, double* jr, int* n,
                               cudaStream_t s);

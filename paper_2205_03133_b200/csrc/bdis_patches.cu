@@ -49,11 +49,11 @@ struct Ev {
   int n;
 };
 
-template <bool kSmem>
+template <bool kSmem, bool kR64 = false>
 struct Rows {
-  // right view rows: fp64 in shared memory (converted once at staging, padded
-  // x + x/16 for 8-byte slots), fp32 rows of (w+1) in global memory
-  using RT = typename std::conditional<kSmem, double, float>::type;
+  // right view rows: in shared memory fp64 (kR64: converted once at staging,
+  // slots x + x/16) or fp32 (slots x + x/32); fp32 rows of (w+1) in global
+  using RT = typename std::conditional<kSmem && kR64, double, float>::type;
   const RT* R;
   const float* Lf;   // left view
   const float* Gf;   // gradient of the left view
@@ -61,14 +61,16 @@ struct Rows {
   const uint8_t* rq;
   int rp, fp, bp;    // row pitches (slots)
   __device__ __forceinline__ static int s4(int x) { return kSmem ? x + (x >> 5) : x; }
-  __device__ __forceinline__ static int s8(int x) { return kSmem ? x + (x >> 4) : x; }
+  __device__ __forceinline__ static int s8(int x) {
+    return !kSmem ? x : (kR64 ? x + (x >> 4) : x + (x >> 5));
+  }
 };
 
 // eval_patch_residual (src/lk_solver.cpp:38-81) of a lattice patch whose
 // footprint starts at column x0 and row r0 of `rw`, at disparity u.
-template <int S, bool kSmem, bool kValid>
-__device__ __forceinline__ Ev eval_patch(const Rows<kSmem>& rw, int w, int s_rt, int x0, int r0,
-                                         double mean, double u) {
+template <int S, bool kSmem, bool kValid, bool kR64>
+__device__ __forceinline__ Ev eval_patch(const Rows<kSmem, kR64>& rw, int w, int s_rt, int x0,
+                                         int r0, int rpad, double mean, double u) {
   constexpr int SA = S > 0 ? S : kMaxPatch;
   const int s = S > 0 ? S : s_rt;
   const double wm1 = (double)(w - 1);
@@ -97,7 +99,7 @@ __device__ __forceinline__ Ev eval_patch(const Rows<kSmem>& rw, int w, int s_rt,
   // contiguous (x0_i = base + i -- always, unless x sits within rounding of an
   // integer) sample i reads taps base+i, base+i+1 and reuses the left tap of
   // column i+1. Out-of-image columns (invalid samples, inc/image.hpp:55,68)
-  // read the zero padding kRowPad slots either side of the row and are masked
+  // read the zero padding (`rpad` = s slots either side of the row) and are masked
   // out of the sums. Lanes therefore never split between code paths.
   int base = 0;
   bool ctg = kSmem && !kValid && S > 0 && inb != 0;
@@ -124,7 +126,7 @@ __device__ __forceinline__ Ev eval_patch(const Rows<kSmem>& rw, int w, int s_rt,
     }
     const int n = SA * __popc(inb);
     ev.n = n;
-    const int xb = base + kRowPad;  // smem column of tap `base`
+    const int xb = base + rpad;  // smem column of tap `base`
     double sum = 0.0;
     const auto* rr = rw.R + r0 * rw.rp;
 #pragma unroll 1
@@ -164,7 +166,7 @@ __device__ __forceinline__ Ev eval_patch(const Rows<kSmem>& rw, int w, int s_rt,
   }
   // Validity masks, a runtime patch size, non-contiguous taps or global rows:
   // per-sample predicates.
-  const int xo = kSmem ? kRowPad : 0;
+  const int xo = kSmem ? rpad : 0;
   int n = 0;
   double sum = 0.0;
 #pragma unroll 1
@@ -222,7 +224,7 @@ __device__ __forceinline__ Ev eval_patch(const Rows<kSmem>& rw, int w, int s_rt,
 }  // namespace
 
 
-template <int S, bool kSmem, bool kValid>
+template <int S, bool kSmem, bool kValid, bool kR64>
 __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams pp, BandPlan bp) {
   extern __shared__ __align__(16) unsigned char smem[];
   const Grid& g = L.g;
@@ -241,8 +243,10 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
 
   // ---- shared-memory carve-up (mirrors band_layout on the host)
   const BandLayout lay = band_layout(bp.use_smem ? bp.smem_rows : 0, bp.rpitch, bp.fpitch,
-                                     bp.bpitch, bp.npb, nwin, kValid);
-  double* sR = (double*)(smem + lay.oR);
+                                     bp.bpitch, bp.npb, nwin, kValid, kR64);
+  using RT = typename Rows<kSmem, kR64>::RT;
+  RT* sR = (RT*)(smem + lay.oR);
+  const int rpad = kSmem ? bp.rpad : 0;
   float* sL = (float*)(smem + lay.oL);
   float* sG = (float*)(smem + lay.oG);
   uint8_t* sLQ = smem + lay.oLQ;
@@ -259,18 +263,18 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
   uint8_t* st_wok = smem + lay.oWok;
 
   const long long pbase = pair * L.plane;
-  Rows<kSmem> rw;
+  Rows<kSmem, kR64> rw;
   int rofs;  // row index of image row y in rw is y - rofs
   if constexpr (kSmem) {
     // ---- stage the band (coalesced global reads, padded shared writes)
     const float* gR = L.rpad + pair * (long long)(w + 1) * h + (long long)ylo * (w + 1);
-    // right rows with kRowPad zero slots either side (x in [-kRowPad, w + kRowPad])
-    const int rw2 = w + 1 + 2 * kRowPad;
+    // right rows with rpad zero slots either side (x in [-rpad, w + rpad])
+    const int rw2 = w + 1 + 2 * rpad;
 #pragma unroll 4
     for (int q = tid; q < nrows * rw2; q += nt) {
-      const int r = q / rw2, x = q - r * rw2 - kRowPad;
-      sR[r * bp.rpitch + Rows<true>::s8(x + kRowPad)] =
-          (x >= 0 && x <= w) ? (double)__ldg(gR + (long long)r * (w + 1) + x) : 0.0;
+      const int r = q / rw2, x = q - r * rw2 - rpad;
+      sR[r * bp.rpitch + Rows<true, kR64>::s8(x + rpad)] =
+          (x >= 0 && x <= w) ? (RT)__ldg(gR + (long long)r * (w + 1) + x) : (RT)0;
     }
     const float* gl0 = L.left + pbase + (long long)ylo * w;
     const float* gg0 = L.grad + pbase + (long long)ylo * w;
@@ -398,7 +402,7 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
     start(p);
     while (p >= 0) {
       const double uu = k < 0 ? u : __dadd_rn(u, pp.woff[k]);
-      const Ev ev = eval_patch<S, kSmem, kValid>(rw, w, s, x0, r0, mean, uu);
+      const Ev ev = eval_patch<S, kSmem, kValid, kR64>(rw, w, s, x0, r0, rpad, mean, uu);
       bool next = false;
       if (k >= 0) {
         // sample_window: valid iff every template pixel was sampled (:31-36)
@@ -537,19 +541,22 @@ BandPlan plan_bands(const Level& L, const PatchParams& pp, int max_smem_per_cta)
   const Grid& g = L.g;
   BandPlan bp{};
   const bool valid = !pp.all_valid;
-  bp.rpitch = pad8_host(L.w + 2 * kRowPad) + 1;   // slots for x in [-kRowPad, w + kRowPad]
-  bp.fpitch = (L.w - 1 + ((L.w - 1) >> 5)) + 1;  // slots for x in [0, w-1]
-  bp.bpitch = valid ? L.w : 0;
-  auto bytes_for = [&](int rb) {
-    const int rows = (rb - 1) * g.stride + g.size;
-    return band_layout(rows, bp.rpitch, bp.fpitch, bp.bpitch, rb * g.nx, pp.nwin, valid).total;
-  };
-  // ~1.5 patches per lane of a 128-thread CTA, while `ctas` CTAs fit an SM
-  // (PSTEREO_TUNE_THREADS / _PPL10 / _CTAS override, for tuning runs only)
   auto env = [](const char* k, int d) {
     const char* v = getenv(k);
     return v ? atoi(v) : d;
   };
+  bp.r64 = env("PSTEREO_TUNE_R64", 0);
+  bp.rpad = g.size;
+  bp.rpitch = (bp.r64 ? pad8_host(L.w + 2 * bp.rpad) : pad4_host(L.w + 2 * bp.rpad)) + 1;
+  bp.fpitch = (L.w - 1 + ((L.w - 1) >> 5)) + 1;  // slots for x in [0, w-1]
+  bp.bpitch = valid ? L.w : 0;
+  auto bytes_for = [&](int rb) {
+    const int rows = (rb - 1) * g.stride + g.size;
+    return band_layout(rows, bp.rpitch, bp.fpitch, bp.bpitch, rb * g.nx, pp.nwin, valid,
+                       bp.r64).total;
+  };
+  // ~1.5 patches per lane of a 128-thread CTA, while `ctas` CTAs fit an SM
+  // (PSTEREO_TUNE_THREADS / _PPL10 / _CTAS override, for tuning runs only)
   const int threads = env("PSTEREO_TUNE_THREADS", 128);
   const int ppl10 = env("PSTEREO_TUNE_PPL10", 15);
   const int ctas = env("PSTEREO_TUNE_CTAS", 2);
@@ -563,7 +570,7 @@ BandPlan plan_bands(const Level& L, const PatchParams& pp, int max_smem_per_cta)
   bp.smem_rows = (rb - 1) * g.stride + g.size;
   bp.smem_bytes = bp.use_smem ? bytes_for(rb)
                               : band_layout(0, bp.rpitch, bp.fpitch, bp.bpitch, bp.npb, pp.nwin,
-                                            valid).total;
+                                            valid, bp.r64).total;
   bp.threads = std::min(threads, std::max(32, ((bp.npb + 31) / 32) * 32));
   return bp;
 }
@@ -571,7 +578,7 @@ BandPlan plan_bands(const Level& L, const PatchParams& pp, int max_smem_per_cta)
 template <int S, bool kSmem, bool kValid>
 static cudaError_t launch_t(const Level& L, const Level& P, const PatchParams& pp,
                             const BandPlan& bp, cudaStream_t s) {
-  auto kern = k_patches<S, kSmem, kValid>;
+  auto kern = (kSmem && bp.r64) ? k_patches<S, kSmem, kValid, true> : k_patches<S, kSmem, kValid, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)bp.smem_bytes);
   if (e != cudaSuccess) return e;
@@ -631,7 +638,7 @@ __global__ void k_debug_eval(Level L, int size, int nq, const int* __restrict__ 
       ++cnt;
     }
   const double mean = cnt ? __ddiv_rn(sum, (double)cnt) : 0.0;
-  const Ev ev = eval_patch<0, false, kValid>(rw, L.w, size, x0, y0, mean, qu[q]);
+  const Ev ev = eval_patch<0, false, kValid, false>(rw, L.w, size, x0, y0, 0, mean, qu[q]);
   msq[q] = ev.msq;
   jr[q] = ev.jr;
   n[q] = ev.n;
