@@ -23,6 +23,8 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include <math_constants.h>
 
 #include "bdis_device.cuh"
@@ -487,6 +489,32 @@ __global__ void k_output(OutputArgs a) {
   const int x0 = fx << a.e, x1 = min((fx + 1) << a.e, a.W);
   const int y0 = fy << a.e, y1 = min((fy + 1) << a.e, a.H);
   const long long pbase = pair * (long long)a.W * a.H;
+  using T2 = typename std::conditional<sizeof(T) == 8, double2, float2>::type;
+  if (a.e == 1 && x1 - x0 == 2 && (a.W & 1) == 0) {
+    // 2x2 blocks on an even-width image: vector stores, two rows
+    const T2 dd{(T)d, (T)d}, pp2{(T)p, (T)p}, de{(T)depth, (T)depth};
+    const T2 vv2{(T)v, (T)v}, sg2{(T)sg, (T)sg};
+    const uchar2 kv{(unsigned char)keep, (unsigned char)keep};
+    const uchar2 mv2{(unsigned char)mv, (unsigned char)mv};
+    const uchar2 dv2{(unsigned char)dv, (unsigned char)dv};
+    const uchar2 sv2{(unsigned char)sv, (unsigned char)sv};
+    for (int y = y0; y < y1; ++y) {
+      const long long o = pbase + (long long)y * a.W + x0;
+      if (a.out_disp) *(T2*)((T*)a.out_disp + o) = dd;
+      if (a.out_dvalid) *(uchar2*)(a.out_dvalid + o) = kv;
+      if (a.out_prob) *(T2*)((T*)a.out_prob + o) = pp2;
+      if (a.out_mdisp) *(T2*)((T*)a.out_mdisp + o) = dd;
+      if (a.out_mvalid) *(uchar2*)(a.out_mvalid + o) = mv2;
+      if (a.out_depth) *(T2*)((T*)a.out_depth + o) = de;
+      if (a.out_depth_valid) *(uchar2*)(a.out_depth_valid + o) = dv2;
+      if (a.has_var) {
+        if (a.out_var) *(T2*)((T*)a.out_var + o) = vv2;
+        if (a.out_sigma) *(T2*)((T*)a.out_sigma + o) = sg2;
+        if (a.out_sigma_valid) *(uchar2*)(a.out_sigma_valid + o) = sv2;
+      }
+    }
+    return;
+  }
   for (int y = y0; y < y1; ++y) {
     for (int x = x0; x < x1; ++x) {
       const long long o = pbase + (long long)y * a.W + x;
