@@ -175,8 +175,8 @@ struct pstereo_ctx {
   DevBuf<uint8_t> full_valid[2];
   std::vector<LevelBufs> levels;  // index e (0 unused unless finest_exp == 0)
   // finest fields
-  DevBuf<double> fdisp, fprob, fvar;
-  DevBuf<uint8_t> fmvalid, fmask;
+  DevBuf<double> fdisp, fprob, fdepth, fvar, fsigma;  // sized as doubles, typed per call
+  DevBuf<uint8_t> fflags;
   DevBuf<int> flabel, farea;
   DevBuf<int> stats;
   // staging for host outputs
@@ -386,9 +386,10 @@ void pstereo_gpu_destroy(pstereo_ctx* ctx) {
   }
   ctx->fdisp.release();
   ctx->fprob.release();
+  ctx->fdepth.release();
   ctx->fvar.release();
-  ctx->fmvalid.release();
-  ctx->fmask.release();
+  ctx->fsigma.release();
+  ctx->fflags.release();
   ctx->flabel.release();
   ctx->farea.release();
   ctx->stats.release();
@@ -676,18 +677,34 @@ int run_device(pstereo_ctx* ctx, const std::vector<LevelGeom>& geo, int n, int W
   // ---- finest fusion, confidence filter, output (src/pipeline.cpp:15-27)
   const Level& F = lv.back();
   const size_t fnp = size_t(F.plane) * n;
-  CK(ctx->fdisp.ensure(fnp));
-  CK(ctx->fprob.ensure(fnp));
-  if (prm.estimate_variance) CK(ctx->fvar.ensure(fnp));
-  CK(ctx->fmvalid.ensure(fnp));
-  CK(ctx->fmask.ensure(fnp));
+  // which finest planes the requested outputs need
+  const bool need_disp = dev_ptr[0] || dev_ptr[7];
+  const bool need_prob = dev_ptr[2] != nullptr;
+  const bool need_depth = dev_ptr[3] != nullptr;
+  const bool need_sigma = dev_ptr[5] != nullptr;
+  const bool need_var = dev_ptr[9] != nullptr;
+  if (need_disp) CK(ctx->fdisp.ensure(fnp));
+  if (need_prob) CK(ctx->fprob.ensure(fnp));
+  if (need_depth) CK(ctx->fdepth.ensure(fnp));
+  if (need_var) CK(ctx->fvar.ensure(fnp));
+  if (need_sigma) CK(ctx->fsigma.ensure(fnp));
+  CK(ctx->fflags.ensure(fnp));
   CK(ctx->flabel.ensure(fnp));
   CK(ctx->farea.ensure(fnp));
-  FinestBufs fb{ctx->fdisp.p, ctx->fprob.p, prm.estimate_variance ? ctx->fvar.p : nullptr,
-                ctx->fmvalid.p, ctx->fmask.p, ctx->flabel.p};
+  FinestBufs fb;
+  fb.disp = need_disp ? (void*)ctx->fdisp.p : nullptr;
+  fb.prob = need_prob ? (void*)ctx->fprob.p : nullptr;
+  fb.depth = need_depth ? (void*)ctx->fdepth.p : nullptr;
+  fb.var = need_var ? (void*)ctx->fvar.p : nullptr;
+  fb.sigma = need_sigma ? (void*)ctx->fsigma.p : nullptr;
+  fb.flags = ctx->fflags.p;
+  fb.label = ctx->flabel.p;
+  fb.scale_d = fe == 0 ? 1.0 : std::pow(2.0, fe);
+  fb.scale_v = fe == 0 ? 1.0 : std::pow(4.0, fe);
+  fb.fb = focal * baseline;
+  fb.threshold = prm.pixel_threshold;
   CK(cudaMemsetAsync(ctx->farea.p, 0, fnp * sizeof(int), s));
-  launch_fuse_ccl(F, fb, ctx->mask.p, prm.estimate_variance, prm.pixel_threshold, W, H, fe,
-                  ctx->farea.p, n, s);
+  launch_fuse_ccl(F, fb, ctx->mask.p, prm.estimate_variance, f64, W, H, fe, ctx->farea.p, n, s);
   ctx->launches += 3;
 
   OutputArgs oa;
@@ -698,21 +715,12 @@ int run_device(pstereo_ctx* ctx, const std::vector<LevelGeom>& geo, int n, int W
   oa.fw = F.w;
   oa.fh = F.h;
   oa.fplane = F.plane;
-  oa.disp = ctx->fdisp.p;
-  oa.prob = ctx->fprob.p;
-  oa.var = prm.estimate_variance ? ctx->fvar.p : nullptr;
-  oa.mvalid = ctx->fmvalid.p;
-  oa.fmask = ctx->fmask.p;
-  oa.label = ctx->flabel.p;
+  oa.fb = fb;
   oa.area = ctx->farea.p;
   {
     const long long mp = llround(std::ceil(prm.gamma * double(S) * double(S) - 1e-9));
     oa.min_px = std::max(mp, 1ll);  // src/depth_variance.cpp:87-90
   }
-  oa.scale_d = fe == 0 ? 1.0 : std::pow(2.0, fe);
-  oa.scale_v = fe == 0 ? 1.0 : std::pow(4.0, fe);
-  oa.fb = focal * baseline;
-  oa.has_var = prm.estimate_variance;
   oa.out_disp = dev_ptr[0];
   oa.out_dvalid = (uint8_t*)dev_ptr[1];
   oa.out_prob = dev_ptr[2];

@@ -120,17 +120,23 @@ __global__ void k_level_tables(Level L) {
 // view, its gradient_x (src/pyramid.cpp:30-42) and the padded right view.
 // Replaces k_gray_u8 + k_downsample + k_level_tables: the full-resolution fp32
 // planes never touch HBM.
+// to_grayscale of one source pixel through shared lookup tables built with
+// the reference's own expressions: gray = float(p * (1/255)); RGB: the three
+// products 0.299 R, 0.587 G, 0.114 B (doubles), summed left to right.
+struct GrayLut {
+  const float* g1;   // [256] gray
+  const double* c3;  // [3][256] RGB channel products
+};
+
 template <bool kU8>
-__device__ __forceinline__ float src_px(const PyrArgs& a, int view, long long pair, int x,
-                                        int y) {
+__device__ __forceinline__ float src_px(const PyrArgs& a, const GrayLut& lut, int view,
+                                        long long pair, int x, int y) {
   const long long i = pair * (long long)a.W * a.H + (long long)y * a.W + x;
   if (kU8) {
     const uint8_t* p = (view ? a.u8r : a.u8l) + i * a.C;
-    const double inv255 = 1.0 / 255.0;
-    if (a.C == 1) return __double2float_rn(__dmul_rn((double)p[0], inv255));
-    const double s = __dadd_rn(__dadd_rn(__dmul_rn(0.299, (double)p[0]), __dmul_rn(0.587, (double)p[1])),
-                               __dmul_rn(0.114, (double)p[2]));
-    return __double2float_rn(__dmul_rn(s, inv255));
+    if (a.C == 1) return lut.g1[p[0]];
+    const double s = __dadd_rn(__dadd_rn(lut.c3[p[0]], lut.c3[256 + p[1]]), lut.c3[512 + p[2]]);
+    return __double2float_rn(__dmul_rn(s, 1.0 / 255.0));
   }
   return (view ? a.f0r : a.f0l)[i];
 }
@@ -148,6 +154,19 @@ __global__ void __launch_bounds__(256) k_pyramid(PyrArgs a) {
   const int ce = a.ce, fe = a.fe;
   // level-1 rows of this band live in buf0 (L then R), level e >= 2 alternate
   float* buf[2] = {sbuf, sbuf + 2 * a.buf_floats};
+  // grayscale lookup tables after the level buffers (8-byte aligned)
+  double* c3 = (double*)(sbuf + ((4 * a.buf_floats + 1) & ~1));
+  float* g1 = (float*)(c3 + 768);
+  if (kU8) {
+    for (int q = tid; q < 256; q += nt) {
+      g1[q] = __double2float_rn(__dmul_rn((double)q, 1.0 / 255.0));  // src/image.cpp:30
+      c3[q] = __dmul_rn(0.299, (double)q);                            // src/image.cpp:36
+      c3[256 + q] = __dmul_rn(0.587, (double)q);
+      c3[512 + q] = __dmul_rn(0.114, (double)q);
+    }
+    __syncthreads();
+  }
+  const GrayLut lut{g1, c3};
   auto store = [&](int e, int y0, int rows, const float* Lb, const float* Rb) {
     const int w = a.ws[e];
     const long long pl = pair * (long long)w * a.hs[e];
@@ -178,18 +197,18 @@ __global__ void __launch_bounds__(256) k_pyramid(PyrArgs a) {
     const long long pl = pair * (long long)W * a.H, pr = pair * (long long)(W + 1) * a.H;
     for (int q = tid; q < (r1 - r0) * W; q += nt) {
       const int y = r0 + q / W, x = q % W;
-      const float l = src_px<kU8>(a, 0, pair, x, y);
+      const float l = src_px<kU8>(a, lut, 0, pair, x, y);
       float g = 0.0f;
       if (W >= 2) {
-        if (x == 0) g = __fsub_rn(src_px<kU8>(a, 0, pair, 1, y), l);
-        else if (x == W - 1) g = __fsub_rn(l, src_px<kU8>(a, 0, pair, W - 2, y));
-        else g = __fmul_rn(0.5f, __fsub_rn(src_px<kU8>(a, 0, pair, x + 1, y),
-                                           src_px<kU8>(a, 0, pair, x - 1, y)));
+        if (x == 0) g = __fsub_rn(src_px<kU8>(a, lut, 0, pair, 1, y), l);
+        else if (x == W - 1) g = __fsub_rn(l, src_px<kU8>(a, lut, 0, pair, W - 2, y));
+        else g = __fmul_rn(0.5f, __fsub_rn(src_px<kU8>(a, lut, 0, pair, x + 1, y),
+                                           src_px<kU8>(a, lut, 0, pair, x - 1, y)));
       }
       const long long o = pl + (long long)y * W + x;
       a.L[0][o] = l;
       a.G[0][o] = g;
-      const float rv = src_px<kU8>(a, 1, pair, x, y);
+      const float rv = src_px<kU8>(a, lut, 1, pair, x, y);
       float* rp = a.Rp[0] + pr + (long long)y * (W + 1);
       rp[x] = rv;
       if (x == W - 1) rp[W] = rv;
@@ -206,10 +225,10 @@ __global__ void __launch_bounds__(256) k_pyramid(PyrArgs a) {
       const int y = y0 + q / w, x = q % w;
       const int sx0 = 2 * x, sx1 = min(2 * x + 1, a.W - 1);
       const int sy0 = 2 * y, sy1 = min(2 * y + 1, a.H - 1);
-      Lb[q] = down4(src_px<kU8>(a, 0, pair, sx0, sy0), src_px<kU8>(a, 0, pair, sx1, sy0),
-                    src_px<kU8>(a, 0, pair, sx0, sy1), src_px<kU8>(a, 0, pair, sx1, sy1));
-      Rb[q] = down4(src_px<kU8>(a, 1, pair, sx0, sy0), src_px<kU8>(a, 1, pair, sx1, sy0),
-                    src_px<kU8>(a, 1, pair, sx0, sy1), src_px<kU8>(a, 1, pair, sx1, sy1));
+      Lb[q] = down4(src_px<kU8>(a, lut, 0, pair, sx0, sy0), src_px<kU8>(a, lut, 0, pair, sx1, sy0),
+                    src_px<kU8>(a, lut, 0, pair, sx0, sy1), src_px<kU8>(a, lut, 0, pair, sx1, sy1));
+      Rb[q] = down4(src_px<kU8>(a, lut, 1, pair, sx0, sy0), src_px<kU8>(a, lut, 1, pair, sx1, sy0),
+                    src_px<kU8>(a, lut, 1, pair, sx0, sy1), src_px<kU8>(a, lut, 1, pair, sx1, sy1));
     }
     __syncthreads();
     if (1 >= fe) store(1, y0, rows, Lb, Rb);
@@ -236,7 +255,10 @@ __global__ void __launch_bounds__(256) k_pyramid(PyrArgs a) {
   }
 }
 
-size_t pyramid_smem_bytes(const PyrArgs& a) { return a.ce >= 1 ? 4 * a.buf_floats * sizeof(float) : 0; }
+size_t pyramid_smem_bytes(const PyrArgs& a) {
+  const size_t bufs = a.ce >= 1 ? size_t((4 * a.buf_floats + 1) & ~1) * sizeof(float) : 0;
+  return bufs + 768 * sizeof(double) + 256 * sizeof(float);  // + grayscale tables
+}
 
 cudaError_t launch_pyramid(const PyrArgs& a, bool u8, cudaStream_t s) {
   const size_t smem = pyramid_smem_bytes(a);
@@ -313,9 +335,9 @@ constexpr int kTileRec = 160;  // max covering patches per 32x16 tile (stride >=
 // then the tile-local pass of the component labelling -- one CTA per 32x16
 // tile. The records of the covering patches are staged in shared memory and
 // each pixel gathers them in ascending patch index (fuse_level's order).
-template <bool kVar>
+template <bool kVar, typename T>
 __global__ void __launch_bounds__(kTileW * kTileH) k_fuse_ccl_local(
-    Level L, FinestBufs fb, const double* __restrict__ mask, double threshold) {
+    Level L, FinestBufs fb, const double* __restrict__ mask) {
   __shared__ int sl[kTileW * kTileH];
   __shared__ double s_pr[kTileRec], s_u[kTileRec], s_sg[kTileRec];
   __shared__ uint8_t s_st[kTileRec];
@@ -352,19 +374,34 @@ __global__ void __launch_bounds__(kTileW * kTileH) k_fuse_ccl_local(
       f = gather<true, kVar>(L, pair, x, y, mask);
     }
     const long long o = pair * L.plane + (long long)y * w + x;
-    const bool valid = !(f.sw <= 0.0);
+    const bool valid = !(f.sw <= 0.0);  // fuse_level: sw <= 0 stays invalid (:138)
     double d = 0.0, p = 0.0, v = 0.0;
     if (valid) {
       d = __ddiv_rn(f.swu, f.sw);
       p = __ddiv_rn(f.swp, f.sw);
       if (kVar) v = __ddiv_rn(f.sw2s, __dmul_rn(f.sw, f.sw));
     }
-    fb.disp[o] = d;
-    fb.prob[o] = p;
-    if (kVar) fb.var[o] = v;
-    fb.mvalid[o] = valid ? 1 : 0;
-    keep = valid && !(p < threshold);
-    fb.mask[o] = keep ? 1 : 0;
+    // upsample_to_full values (:166-180): scale 2^fe, 1, 4^fe where valid, else 0
+    const double D = valid ? __dmul_rn(fb.scale_d, d) : 0.0;
+    const double Pv = valid ? __dmul_rn(1.0, p) : 0.0;
+    const double V = valid ? __dmul_rn(fb.scale_v, v) : 0.0;
+    const bool deep = D >= 0.1;  // kMinDisparity (inc/depth_variance.hpp:13)
+    keep = valid && !(Pv < fb.threshold);  // filter_validity threshold (:84)
+    if (fb.disp) ((T*)fb.disp)[o] = (T)D;
+    if (fb.prob) ((T*)fb.prob)[o] = (T)Pv;
+    if (fb.depth) ((T*)fb.depth)[o] = (T)(deep ? __ddiv_rn(fb.fb, D) : 0.0);
+    if (kVar) {
+      if (fb.var) ((T*)fb.var)[o] = (T)V;
+      if (fb.sigma) {
+        double sg = 0.0;
+        if (deep && valid) {
+          const double vv = (V < 0.0) ? 0.0 : V;  // std::max(var, 0.0)
+          sg = __dmul_rn(__ddiv_rn(fb.fb, __dmul_rn(D, D)), __dsqrt_rn(vv));
+        }
+        ((T*)fb.sigma)[o] = (T)sg;
+      }
+    }
+    fb.flags[o] = (valid ? kFlagMatch : 0) | (keep ? kFlagKeep : 0) | (deep ? kFlagDepth : 0);
   }
   // ---- tile-local components: run labels (ballot bit tricks) + union-find
   const unsigned bits = __ballot_sync(0xffffffffu, keep);
@@ -425,18 +462,18 @@ __global__ void k_ccl_border(int w, int h, long long plane, const uint8_t* __res
   }
   const long long base = blockIdx.y * plane;
   const int i = y * w + x;
-  if (!mask[base + i]) return;
+  if (!(mask[base + i] & kFlagKeep)) return;
   int* l = lab + base;
   volatile int* vl = l;
   const int j = left ? i - 1 : i - w;
-  if (mask[base + j]) uf_union(vl, l, i, j);
+  if (mask[base + j] & kFlagKeep) uf_union(vl, l, i, j);
 }
 
 __global__ void k_ccl_final(int w, int h, long long plane, int full_w, int full_h, int e,
                             const uint8_t* __restrict__ mask, int* lab, int* area) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const long long base = blockIdx.y * plane;
-  const bool m = i < w * h && mask[base + i];
+  const bool m = i < w * h && (mask[base + i] & kFlagKeep);
   int root = -1, weight = 0;
   if (m) {
     volatile int* vl = lab + base;
@@ -462,74 +499,61 @@ __global__ void k_ccl_final(int w, int h, long long plane, int full_w, int full_
 // sharing (src/pipeline.cpp:21-22) and disparity_to_depth (:9-41).
 template <typename T>
 __global__ void k_output(OutputArgs a) {
-  // one thread per finest-level pixel: values are computed once and written
-  // to its 2^e x 2^e full-resolution block (nearest upsampling)
+  // one thread per finest-level pixel: apply the area rule of filter_validity
+  // (src/depth_variance.cpp:87-90) and replicate the fused values over the
+  // pixel's 2^e x 2^e full-resolution block (nearest upsampling)
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.fw * a.fh) return;
   const long long pair = blockIdx.y;
   const int fx = i % a.fw, fy = i / a.fw;
   const long long f = pair * a.fplane + i;
-  const bool mv = a.mvalid[f] != 0;
+  const uint8_t fl = a.fb.flags[f];
+  const bool mv = fl & kFlagMatch;
   bool keep = false;
-  if (a.fmask[f]) keep = a.area[pair * a.fplane + a.label[f]] >= a.min_px;
-  const double d = mv ? __dmul_rn(a.scale_d, a.disp[f]) : 0.0;
-  const double p = mv ? __dmul_rn(1.0, a.prob[f]) : 0.0;
-  const bool dv = keep && (d >= 0.1);  // kMinDisparity, inc/depth_variance.hpp:13
-  const double depth = dv ? __ddiv_rn(a.fb, d) : 0.0;
-  double v = 0.0, sg = 0.0;
-  bool sv = false;
-  if (a.has_var) {
-    v = mv ? __dmul_rn(a.scale_v, a.var[f]) : 0.0;
-    sv = dv && mv;
-    if (sv) {
-      const double vv = (v < 0.0) ? 0.0 : v;  // std::max(var, 0.0)
-      sg = __dmul_rn(__ddiv_rn(a.fb, __dmul_rn(d, d)), __dsqrt_rn(vv));
-    }
-  }
+  if (fl & kFlagKeep) keep = a.area[pair * a.fplane + a.fb.label[f]] >= a.min_px;
+  const bool dv = keep && (fl & kFlagDepth);  // depth valid; sigma valid too (var valid == mv)
+  const T d = a.fb.disp ? ((const T*)a.fb.disp)[f] : (T)0;
+  const T p = a.fb.prob ? ((const T*)a.fb.prob)[f] : (T)0;
+  const T z = (dv && a.fb.depth) ? ((const T*)a.fb.depth)[f] : (T)0;
+  const T v = a.fb.var ? ((const T*)a.fb.var)[f] : (T)0;
+  const T sg = (dv && a.fb.sigma) ? ((const T*)a.fb.sigma)[f] : (T)0;
   const int x0 = fx << a.e, x1 = min((fx + 1) << a.e, a.W);
   const int y0 = fy << a.e, y1 = min((fy + 1) << a.e, a.H);
   const long long pbase = pair * (long long)a.W * a.H;
   using T2 = typename std::conditional<sizeof(T) == 8, double2, float2>::type;
   if (a.e == 1 && x1 - x0 == 2 && (a.W & 1) == 0) {
     // 2x2 blocks on an even-width image: vector stores, two rows
-    const T2 dd{(T)d, (T)d}, pp2{(T)p, (T)p}, de{(T)depth, (T)depth};
-    const T2 vv2{(T)v, (T)v}, sg2{(T)sg, (T)sg};
     const uchar2 kv{(unsigned char)keep, (unsigned char)keep};
     const uchar2 mv2{(unsigned char)mv, (unsigned char)mv};
     const uchar2 dv2{(unsigned char)dv, (unsigned char)dv};
-    const uchar2 sv2{(unsigned char)sv, (unsigned char)sv};
     for (int y = y0; y < y1; ++y) {
       const long long o = pbase + (long long)y * a.W + x0;
-      if (a.out_disp) *(T2*)((T*)a.out_disp + o) = dd;
+      if (a.out_disp) *(T2*)((T*)a.out_disp + o) = T2{d, d};
       if (a.out_dvalid) *(uchar2*)(a.out_dvalid + o) = kv;
-      if (a.out_prob) *(T2*)((T*)a.out_prob + o) = pp2;
-      if (a.out_mdisp) *(T2*)((T*)a.out_mdisp + o) = dd;
+      if (a.out_prob) *(T2*)((T*)a.out_prob + o) = T2{p, p};
+      if (a.out_mdisp) *(T2*)((T*)a.out_mdisp + o) = T2{d, d};
       if (a.out_mvalid) *(uchar2*)(a.out_mvalid + o) = mv2;
-      if (a.out_depth) *(T2*)((T*)a.out_depth + o) = de;
+      if (a.out_depth) *(T2*)((T*)a.out_depth + o) = T2{z, z};
       if (a.out_depth_valid) *(uchar2*)(a.out_depth_valid + o) = dv2;
-      if (a.has_var) {
-        if (a.out_var) *(T2*)((T*)a.out_var + o) = vv2;
-        if (a.out_sigma) *(T2*)((T*)a.out_sigma + o) = sg2;
-        if (a.out_sigma_valid) *(uchar2*)(a.out_sigma_valid + o) = sv2;
-      }
+      if (a.out_var) *(T2*)((T*)a.out_var + o) = T2{v, v};
+      if (a.out_sigma) *(T2*)((T*)a.out_sigma + o) = T2{sg, sg};
+      if (a.out_sigma_valid) *(uchar2*)(a.out_sigma_valid + o) = dv2;
     }
     return;
   }
   for (int y = y0; y < y1; ++y) {
     for (int x = x0; x < x1; ++x) {
       const long long o = pbase + (long long)y * a.W + x;
-      if (a.out_disp) ((T*)a.out_disp)[o] = (T)d;
+      if (a.out_disp) ((T*)a.out_disp)[o] = d;
       if (a.out_dvalid) a.out_dvalid[o] = keep ? 1 : 0;
-      if (a.out_prob) ((T*)a.out_prob)[o] = (T)p;
-      if (a.out_mdisp) ((T*)a.out_mdisp)[o] = (T)d;
+      if (a.out_prob) ((T*)a.out_prob)[o] = p;
+      if (a.out_mdisp) ((T*)a.out_mdisp)[o] = d;
       if (a.out_mvalid) a.out_mvalid[o] = mv ? 1 : 0;
-      if (a.out_depth) ((T*)a.out_depth)[o] = (T)depth;
+      if (a.out_depth) ((T*)a.out_depth)[o] = z;
       if (a.out_depth_valid) a.out_depth_valid[o] = dv ? 1 : 0;
-      if (a.has_var) {
-        if (a.out_var) ((T*)a.out_var)[o] = (T)v;
-        if (a.out_sigma) ((T*)a.out_sigma)[o] = (T)sg;
-        if (a.out_sigma_valid) a.out_sigma_valid[o] = sv ? 1 : 0;
-      }
+      if (a.out_var) ((T*)a.out_var)[o] = v;
+      if (a.out_sigma) ((T*)a.out_sigma)[o] = sg;
+      if (a.out_sigma_valid) a.out_sigma_valid[o] = dv ? 1 : 0;
     }
   }
 }
@@ -596,20 +620,24 @@ void launch_level_tables(const Level& L, int n_pairs, cudaStream_t s) {
 }
 
 void launch_fuse_ccl(const Level& L, const FinestBufs& fb, const double* mask, int want_var,
-                     double threshold, int full_w, int full_h, int e, int* area, int n_pairs,
+                     int f64, int full_w, int full_h, int e, int* area, int n_pairs,
                      cudaStream_t s) {
   const int w = L.w, h = L.h;
   const long long plane = L.plane;
   const int tx = (w + kTileW - 1) / kTileW, ty = (h + kTileH - 1) / kTileH;
-  if (want_var)
-    k_fuse_ccl_local<true><<<dim3(tx * ty, n_pairs), kTileW * kTileH, 0, s>>>(L, fb, mask, threshold);
-  else
-    k_fuse_ccl_local<false><<<dim3(tx * ty, n_pairs), kTileW * kTileH, 0, s>>>(L, fb, mask, threshold);
+  const dim3 grid(tx * ty, n_pairs);
+  if (want_var) {
+    if (f64) k_fuse_ccl_local<true, double><<<grid, kTileW * kTileH, 0, s>>>(L, fb, mask);
+    else k_fuse_ccl_local<true, float><<<grid, kTileW * kTileH, 0, s>>>(L, fb, mask);
+  } else {
+    if (f64) k_fuse_ccl_local<false, double><<<grid, kTileW * kTileH, 0, s>>>(L, fb, mask);
+    else k_fuse_ccl_local<false, float><<<grid, kTileW * kTileH, 0, s>>>(L, fb, mask);
+  }
   const long long nb = (long long)(tx - 1) * h + (long long)(ty - 1) * w;
   if (nb > 0)
-    k_ccl_border<<<dim3(blocks_for(nb, 256), n_pairs), 256, 0, s>>>(w, h, plane, fb.mask, fb.label);
+    k_ccl_border<<<dim3(blocks_for(nb, 256), n_pairs), 256, 0, s>>>(w, h, plane, fb.flags, fb.label);
   k_ccl_final<<<dim3(blocks_for((long long)w * h, 256), n_pairs), 256, 0, s>>>(
-      w, h, plane, full_w, full_h, e, fb.mask, fb.label, area);
+      w, h, plane, full_w, full_h, e, fb.flags, fb.label, area);
 }
 
 void launch_output(const OutputArgs& a, int f64, int n_pairs, cudaStream_t s) {

@@ -102,28 +102,28 @@ struct PyrArgs {
 size_t pyramid_smem_bytes(const PyrArgs& a);
 cudaError_t launch_pyramid(const PyrArgs& a, bool u8, cudaStream_t s);
 
+// Finest-level fields written by the fusion kernel, already upsampled values
+// in the output element type (disparity scaled by 2^fe, depth and sigma from
+// the full-resolution disparity, src/coarse_to_fine.cpp:328-337,
+// src/depth_variance.cpp:9-41); null planes are not requested.
 struct FinestBufs {
-  double* disp;
-  double* prob;
-  double* var;
-  uint8_t* mvalid;
-  uint8_t* mask;
+  void* disp;   // scale_d * d           (0 where no patch covers)
+  void* prob;   // p
+  void* depth;  // D >= 0.1 ? fb / D : 0
+  void* var;    // scale_v * v
+  void* sigma;  // fb / D^2 * sqrt(max(V, 0)) where D >= 0.1
+  uint8_t* flags;
   int* label;
+  double scale_d, scale_v, fb, threshold;
 };
+enum FinestFlag : uint8_t { kFlagMatch = 1, kFlagKeep = 2, kFlagDepth = 4 };
 
 struct OutputArgs {
   int W, H, e, fw, fh;
   long long fplane;
-  const double* disp;
-  const double* prob;
-  const double* var;
-  const uint8_t* mvalid;
-  const uint8_t* fmask;
-  const int* label;
+  FinestBufs fb;
   const int* area;
   long long min_px;
-  double scale_d, scale_v, fb;
-  int has_var;
   void* out_disp;
   uint8_t* out_dvalid;
   void* out_prob;
@@ -154,7 +154,7 @@ cudaError_t launch_patches(const Level& L, const Level& P, const PatchParams& pp
                            const BandPlan& bp, cudaStream_t s);
 // fuse_level (finest) + threshold + 4-connected components with area sums
 void launch_fuse_ccl(const Level& L, const FinestBufs& fb, const double* mask, int want_var,
-                     double threshold, int full_w, int full_h, int e, int* area, int n_pairs,
+                     int f64, int full_w, int full_h, int e, int* area, int n_pairs,
                      cudaStream_t s);
 cudaError_t launch_debug_eval(const Level& L, int size, int all_valid, int nq, const int* qx,
                               const int* qy, const double* qu, double* msq, double* jr, int* n,
