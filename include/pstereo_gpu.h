@@ -118,6 +118,13 @@ typedef struct pstereo_outputs {
   pstereo_patch_estimate* finest;
   int* finest_count;
   int finest_cap;
+  /* When fill_invalid != 0, the disparity / depth / depth_sigma planes hold
+   * invalid_value wherever their validity is 0 (the reference persists maps
+   * that way: write_pfm stores -1 at invalid pixels, src/io.cpp:297-310), so a
+   * caller can skip the u8 validity planes (4 instead of 5 bytes per pixel
+   * for disparity alone). */
+  int fill_invalid;
+  double invalid_value;
 } pstereo_outputs;
 
 typedef struct pstereo_ctx pstereo_ctx;

@@ -80,7 +80,8 @@ class _Outputs(C.Structure):
         ("depth_valid", C.c_void_p), ("depth_sigma", C.c_void_p), ("sigma_valid", C.c_void_p),
         ("match_disparity", C.c_void_p), ("match_valid", C.c_void_p), ("var_disp", C.c_void_p),
         ("stats", C.POINTER(LevelStats)), ("finest", C.POINTER(PatchEstimate)),
-        ("finest_count", i32p), ("finest_cap", C.c_int),
+        ("finest_count", i32p), ("finest_cap", C.c_int), ("fill_invalid", C.c_int),
+        ("invalid_value", C.c_double),
     ]
 
 
@@ -347,7 +348,7 @@ class Matcher:
     # ---- host-memory batched API (numpy in, numpy out)
     def run_batch(self, left, right, focal=1.0, baseline=1.0, dtype=F32, left_valid=None,
                   right_valid=None, want=("disparity", "disparity_valid"), stats=False,
-                  finest_cap=0):
+                  finest_cap=0, invalid_value=None):
         """Batched run_pipeline. left/right: uint8 [n,h,w] / [n,h,w,c], or float32
         [n,h,w] GrayImage planes (+ optional u8 validity)."""
         left = np.ascontiguousarray(left)
@@ -368,6 +369,8 @@ class Matcher:
         o = _Outputs()
         o.dtype = dtype
         o.on_device = 0
+        if invalid_value is not None:
+            o.fill_invalid, o.invalid_value = 1, float(invalid_value)
         planes = {"disparity": vt, "disparity_valid": np.uint8, "probability": vt, "depth": vt,
                   "depth_valid": np.uint8, "depth_sigma": vt, "sigma_valid": np.uint8,
                   "match_disparity": vt, "match_valid": np.uint8, "var_disp": vt}
@@ -416,10 +419,12 @@ class Matcher:
 
     # ---- device-pointer batched API (the zero-copy path used by bench.py)
     def run_device_u8(self, n, width, height, channels, left_ptr, right_ptr, outputs: dict,
-                      dtype=F32, focal=1.0, baseline=1.0, stream=None):
+                      dtype=F32, focal=1.0, baseline=1.0, stream=None, invalid_value=None):
         o = _Outputs()
         o.dtype = dtype
         o.on_device = 1
+        if invalid_value is not None:
+            o.fill_invalid, o.invalid_value = 1, float(invalid_value)
         for k, ptr in outputs.items():
             setattr(o, k, ptr)
         rc = lib().pstereo_gpu_match_u8(self._h, n, width, height, channels, left_ptr, right_ptr,
@@ -428,11 +433,13 @@ class Matcher:
             _raise(rc, self.last_error())
 
     def run_host_u8(self, n, width, height, channels, left_ptr, right_ptr, outputs: dict,
-                    dtype=F32, focal=1.0, baseline=1.0, stream=None):
+                    dtype=F32, focal=1.0, baseline=1.0, stream=None, invalid_value=None):
         """Host (ideally pinned) buffers in and out; H2D/D2H inside the call."""
         o = _Outputs()
         o.dtype = dtype
         o.on_device = 0
+        if invalid_value is not None:
+            o.fill_invalid, o.invalid_value = 1, float(invalid_value)
         for k, ptr in outputs.items():
             setattr(o, k, ptr)
         rc = lib().pstereo_gpu_match_u8(self._h, n, width, height, channels, left_ptr, right_ptr,

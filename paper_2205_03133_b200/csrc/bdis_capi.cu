@@ -473,8 +473,9 @@ struct HostCopies {
 
 int run_device(pstereo_ctx* ctx, const std::vector<LevelGeom>& geo, int n, int W, int H,
                int channels, const uint8_t* const src_u8_in[2], long long f32_offset,
-               bool have_f32_valid, double focal, double baseline, int f64,
-               void* const dev_ptr[10], const HostCopies& hc, cudaStream_t s) {
+               bool have_f32_valid, double focal, double baseline, int f64, int fill_invalid,
+               double invalid_value, void* const dev_ptr[10], const HostCopies& hc,
+               cudaStream_t s) {
   const pstereo_params& prm = ctx->params;
   const uint8_t* left_u8 = src_u8_in[0];
   const bool prof = ctx->profiling;
@@ -731,6 +732,8 @@ int run_device(pstereo_ctx* ctx, const std::vector<LevelGeom>& geo, int n, int W
   oa.out_mdisp = dev_ptr[7];
   oa.out_mvalid = (uint8_t*)dev_ptr[8];
   oa.out_var = dev_ptr[9];
+  oa.fill_invalid = fill_invalid;
+  oa.invalid_value = invalid_value;
   launch_output(oa, f64, n, s);
   ++ctx->launches;
 
@@ -893,7 +896,7 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
     }
     const int launches0 = ctx->launches;
     rc = run_device(ctx, geo, nc, W, H, channels, cu8, left_u8 ? 0 : c0, have_f32_valid, focal,
-                    baseline, f64, cout, hc, s);
+                    baseline, f64, out->fill_invalid, out->invalid_value, cout, hc, s);
     if (rc) return rc;
     (void)launches0;
     if (host_out) {

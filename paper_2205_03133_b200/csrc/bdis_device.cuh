@@ -89,16 +89,27 @@ struct GlobalRecords {
   }
 };
 
+// Covering patches of one pixel coordinate along an axis: regular patches
+// [lo, hi] (starts k*stride) plus the clamped last patch when `last`.
+struct Cover {
+  int lo, hi;
+  bool last;
+};
+
+__device__ __forceinline__ Cover cover_of(int x, int n, int s, int st, int last0) {
+  Cover c;
+  c.lo = (x - s + 1 <= 0) ? 0 : (x - s + 1 + st - 1) / st;
+  c.hi = min(n - 2, x / st);
+  c.last = x >= last0;
+  return c;
+}
+
 template <bool kProb, bool kVar, typename Rec>
-__device__ __forceinline__ Fused gather_with(const Grid& g, const Rec& rec, int x, int y,
-                                             const double* __restrict__ mask) {
+__device__ __forceinline__ Fused gather_cover(const Grid& g, const Rec& rec, int x, int y,
+                                              Cover cx, Cover cy,
+                                              const double* __restrict__ mask) {
   const int s = g.size, st = g.stride;
   Fused f{0.0, 0.0, 0.0, 0.0};
-  const int ky_lo = (y - s + 1 <= 0) ? 0 : (y - s + 1 + st - 1) / st;
-  const int ky_hi = min(g.ny - 2, y / st);
-  const int kx_lo = (x - s + 1 <= 0) ? 0 : (x - s + 1 + st - 1) / st;
-  const int kx_hi = min(g.nx - 2, x / st);
-  const bool last_x = x >= g.lastx0;
   auto add = [&](int ky, int kx, double m) {
     if (rec.stage(ky, kx) != kAccepted) return;
     const double pr = rec.prob(ky, kx);
@@ -113,12 +124,21 @@ __device__ __forceinline__ Fused gather_with(const Grid& g, const Rec& rec, int 
   };
   auto row = [&](int ky, int y0) {
     const double* mrow = mask + (y - y0) * s;
-    for (int kx = kx_lo; kx <= kx_hi; ++kx) add(ky, kx, mrow[x - kx * st]);
-    if (last_x) add(ky, g.nx - 1, mrow[x - g.lastx0]);
+    for (int kx = cx.lo; kx <= cx.hi; ++kx) add(ky, kx, mrow[x - kx * st]);
+    if (cx.last) add(ky, g.nx - 1, mrow[x - g.lastx0]);
   };
-  for (int ky = ky_lo; ky <= ky_hi; ++ky) row(ky, ky * st);
-  if (y >= g.lasty0) row(g.ny - 1, g.lasty0);
+  // ascending patch index: rows ky ascending, columns kx ascending
+  for (int ky = cy.lo; ky <= cy.hi; ++ky) row(ky, ky * st);
+  if (cy.last) row(g.ny - 1, g.lasty0);
   return f;
+}
+
+template <bool kProb, bool kVar, typename Rec>
+__device__ __forceinline__ Fused gather_with(const Grid& g, const Rec& rec, int x, int y,
+                                             const double* __restrict__ mask) {
+  return gather_cover<kProb, kVar>(g, rec, x, y,
+                                   cover_of(x, g.nx, g.size, g.stride, g.lastx0),
+                                   cover_of(y, g.ny, g.size, g.stride, g.lasty0), mask);
 }
 
 // Patches of a level covering pixel columns [xa, xb] form one contiguous index

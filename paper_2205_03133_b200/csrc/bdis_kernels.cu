@@ -354,6 +354,12 @@ __global__ void __launch_bounds__(kTileW * kTileH) k_fuse_ccl_local(
   const int ncol = kx1 - kx0 + 1, nrec = ncol * (ky1 - ky0 + 1);
   const long long rbase = pair * (long long)g.nx * g.ny;
   const bool staged = nrec <= kTileRec;
+  // covering ranges per tile column / row (no integer divisions per pixel)
+  __shared__ Cover s_cx[kTileW], s_cy[kTileH];
+  __shared__ double s_mask[kMaxPatch * kMaxPatch];
+  if (t < kTileW) s_cx[t] = cover_of(tx0 + t, g.nx, g.size, g.stride, g.lastx0);
+  else if (t < kTileW + kTileH) s_cy[t - kTileW] = cover_of(ty0 + t - kTileW, g.ny, g.size, g.stride, g.lasty0);
+  for (int q = t; q < g.size * g.size; q += blockDim.x) s_mask[q] = mask[q];
   if (staged) {
     for (int q = t; q < nrec; q += blockDim.x) {
       const long long r = rbase + (long long)(ky0 + q / ncol) * g.nx + kx0 + q % ncol;
@@ -369,7 +375,7 @@ __global__ void __launch_bounds__(kTileW * kTileH) k_fuse_ccl_local(
     Fused f;
     if (staged) {
       const TileRecords rec{s_st, s_pr, s_u, s_sg, ky0, kx0, ncol};
-      f = gather_with<true, kVar>(g, rec, x, y, mask);
+      f = gather_cover<true, kVar>(g, rec, x, y, s_cx[lx], s_cy[ly], s_mask);
     } else {
       f = gather<true, kVar>(L, pair, x, y, mask);
     }
@@ -512,11 +518,17 @@ __global__ void k_output(OutputArgs a) {
   bool keep = false;
   if (fl & kFlagKeep) keep = a.area[pair * a.fplane + a.fb.label[f]] >= a.min_px;
   const bool dv = keep && (fl & kFlagDepth);  // depth valid; sigma valid too (var valid == mv)
-  const T d = a.fb.disp ? ((const T*)a.fb.disp)[f] : (T)0;
+  T d = a.fb.disp ? ((const T*)a.fb.disp)[f] : (T)0;
   const T p = a.fb.prob ? ((const T*)a.fb.prob)[f] : (T)0;
-  const T z = (dv && a.fb.depth) ? ((const T*)a.fb.depth)[f] : (T)0;
+  T z = (dv && a.fb.depth) ? ((const T*)a.fb.depth)[f] : (T)0;
   const T v = a.fb.var ? ((const T*)a.fb.var)[f] : (T)0;
-  const T sg = (dv && a.fb.sigma) ? ((const T*)a.fb.sigma)[f] : (T)0;
+  T sg = (dv && a.fb.sigma) ? ((const T*)a.fb.sigma)[f] : (T)0;
+  const T md = d;  // MatchResult::disparity keeps its value
+  if (a.fill_invalid) {
+    const T iv = (T)a.invalid_value;
+    if (!keep) d = iv;
+    if (!dv) z = iv, sg = iv;
+  }
   const int x0 = fx << a.e, x1 = min((fx + 1) << a.e, a.W);
   const int y0 = fy << a.e, y1 = min((fy + 1) << a.e, a.H);
   const long long pbase = pair * (long long)a.W * a.H;
@@ -531,7 +543,7 @@ __global__ void k_output(OutputArgs a) {
       if (a.out_disp) *(T2*)((T*)a.out_disp + o) = T2{d, d};
       if (a.out_dvalid) *(uchar2*)(a.out_dvalid + o) = kv;
       if (a.out_prob) *(T2*)((T*)a.out_prob + o) = T2{p, p};
-      if (a.out_mdisp) *(T2*)((T*)a.out_mdisp + o) = T2{d, d};
+      if (a.out_mdisp) *(T2*)((T*)a.out_mdisp + o) = T2{md, md};
       if (a.out_mvalid) *(uchar2*)(a.out_mvalid + o) = mv2;
       if (a.out_depth) *(T2*)((T*)a.out_depth + o) = T2{z, z};
       if (a.out_depth_valid) *(uchar2*)(a.out_depth_valid + o) = dv2;
@@ -547,7 +559,7 @@ __global__ void k_output(OutputArgs a) {
       if (a.out_disp) ((T*)a.out_disp)[o] = d;
       if (a.out_dvalid) a.out_dvalid[o] = keep ? 1 : 0;
       if (a.out_prob) ((T*)a.out_prob)[o] = p;
-      if (a.out_mdisp) ((T*)a.out_mdisp)[o] = d;
+      if (a.out_mdisp) ((T*)a.out_mdisp)[o] = md;
       if (a.out_mvalid) a.out_mvalid[o] = mv ? 1 : 0;
       if (a.out_depth) ((T*)a.out_depth)[o] = z;
       if (a.out_depth_valid) a.out_depth_valid[o] = dv ? 1 : 0;

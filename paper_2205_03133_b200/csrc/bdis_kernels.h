@@ -134,6 +134,8 @@ struct OutputArgs {
   void* out_mdisp;
   uint8_t* out_mvalid;
   void* out_var;
+  int fill_invalid;
+  double invalid_value;
 };
 
 struct StatsArgs {

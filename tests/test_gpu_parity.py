@@ -155,3 +155,23 @@ def test_chunked_host_pipeline(gpu, monkeypatch):
         parts = m.run_batch(left, right, dtype=P.F64, want=want, stats=True)
     for k in want + ["stats"]:
         assert np.array_equal(whole[k], parts[k]), k
+
+
+def test_invalid_value_fill(gpu):
+    """fill_invalid writes the PFM-style sentinel (src/io.cpp:297-310) into
+    invalid disparity/depth pixels and leaves valid ones untouched."""
+    P = gpu
+    left, right = P.synth_batch(1, 2, seed0=1, width=160, height=120)
+    cfg = P.PipelineConfig.baseline(1)
+    want = ["disparity", "disparity_valid", "depth", "depth_valid", "depth_sigma",
+            "sigma_valid", "match_disparity"]
+    with P.Matcher(cfg, 160, 120, 2) as m:
+        a = m.run_batch(left, right, focal=500.0, baseline=5.0, want=want)
+        b = m.run_batch(left, right, focal=500.0, baseline=5.0, want=want, invalid_value=-1.0)
+    for plane, ok in (("disparity", "disparity_valid"), ("depth", "depth_valid"),
+                      ("depth_sigma", "sigma_valid")):
+        v = a[ok].astype(bool)
+        assert np.array_equal(b[plane][v], a[plane][v])
+        assert (b[plane][~v] == -1.0).all()
+    assert np.array_equal(a["match_disparity"], b["match_disparity"])
+    assert (~a["disparity_valid"].astype(bool)).any()
