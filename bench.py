@@ -12,7 +12,8 @@ reduction of the timings.
 
   value   device-resident inputs/outputs, CUDA events on the launch stream
   e2e     the same through the public C ABI with pinned HOST buffers: H2D of
-          both views and D2H of disparity+validity inside every timed step
+          both views and D2H of the disparity map (NaN = invalid, i.e. the
+          validity mask folded in) inside every timed step
   roofline  dominant kernel (k_patches, all levels) from live CUDA events
   cpu_baseline  the reference (oracle/_ref, the unmodified reference sources)
           on this host's cores, bounded sample (rank 0, N=1 only)
