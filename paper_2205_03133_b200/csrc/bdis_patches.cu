@@ -258,7 +258,8 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
   double* st_wres = (double*)(smem + lay.oWres);
   int* st_cnt = (int*)(smem + lay.oCnt);
   int* pool = (int*)(smem + lay.oPool);
-  int* counters = (int*)(smem + lay.oCounters);  // [0]: pool size, [1]: next to take
+  int* counters = (int*)(smem + lay.oCounters);  // [0] pool size, [1..4] see phase 2
+  int* wq = (int*)(smem + lay.oWq);               // queued window samples p*nwin + k
   uint8_t* st_stage = smem + lay.oStage;
   uint8_t* st_wok = smem + lay.oWok;
 
@@ -314,7 +315,8 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
     rw.bp = w;
     rofs = 0;
   }
-  if (tid < 2) counters[tid] = 0;
+  if (tid < 8) counters[tid] = 0;
+  for (int q = tid; q < bp.npb * nwin; q += nt) wq[q] = -1;
   __syncthreads();
 
   // ---- phase 1: extract_patch + precompute_patch_system + u0 (:250-262)
@@ -377,30 +379,60 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
   }
   __syncthreads();
 
-  // ---- phase 2: persistent lanes, one residual evaluation per loop trip
+  // ---- phase 2: persistent lanes, one residual evaluation per loop trip.
+  // Work items: a new patch from the pool (its LK iterations stay on the lane
+  // that took it) or one window sample of a converged patch. When a lane's LK
+  // converges it queues window samples 1..nwin-1 for any lane and evaluates
+  // sample 0 itself, so near the end of the pool idle lanes absorb the
+  // windows of the last patches instead of waiting for them.
   {
     const int n_pool = counters[0];
-    auto take = [&]() {
-      const int q = atomicAdd(&counters[1], 1);
-      return q < n_pool ? pool[q] : -1;
-    };
-    int p = take();
-    int k = -1, it = 0, x0 = 0, r0 = 0;
+    volatile int* vc = counters;  // [1] pool next, [2] queue head, [3] queue tail, [4] LK running
+    volatile int* vwq = wq;
+    int p = -1, k = -1, it = 0, x0 = 0, r0 = 0;
     double u = 0.0, prev = CUDART_INF, lastd = 0.0, mean = 0.0;
-    auto start = [&](int np) {
+    auto load = [&](int np) {
       p = np;
-      if (p < 0) return;
       x0 = col_start(p % g.nx);
       r0 = row_start(ky0 + p / g.nx) - rofs;
-      u = st_u[p];
       mean = st_mean[p];
-      k = -1;
-      it = 0;
-      prev = CUDART_INF;
-      lastd = 0.0;
+      u = st_u[p];
     };
-    start(p);
-    while (p >= 0) {
+    auto next_item = [&]() -> bool {
+      for (;;) {
+        int t = vc[3];
+        while (t < vc[2]) {  // a queued window sample
+          const int old = atomicCAS(&counters[3], t, t + 1);
+          if (old == t) {
+            int item;
+            while ((item = vwq[t]) < 0) __nanosleep(32);  // reserved, being written
+            load(item / nwin);
+            k = item % nwin;
+            return true;
+          }
+          t = old;
+        }
+        if (vc[1] < n_pool) {  // a new patch
+          const int q = atomicAdd(&counters[1], 1);
+          if (q < n_pool) {
+            atomicAdd(&counters[4], 1);
+            load(pool[q]);
+            k = -1;
+            it = 0;
+            prev = CUDART_INF;
+            lastd = 0.0;
+            return true;
+          }
+        }
+        if (vc[4] == 0) {  // no LK running: once the queue is drained, done
+          __threadfence_block();
+          if (vc[3] >= vc[2]) return false;
+        }
+        __nanosleep(64);
+      }
+    };
+    bool have = next_item();
+    while (have) {
       const double uu = k < 0 ? u : __dadd_rn(u, pp.woff[k]);
       const Ev ev = eval_patch<S, kSmem, kValid, kR64>(rw, w, s, x0, r0, rpad, mean, uu);
       bool next = false;
@@ -408,7 +440,7 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
         // sample_window: valid iff every template pixel was sampled (:31-36)
         st_wres[p * nwin + k] = ev.msq;
         st_wok[p * nwin + k] = ev.n == st_cnt[p];
-        next = ++k == nwin;
+        next = true;
       } else {
         // one iteration of solve_patch_disparity (src/lk_solver.cpp:96-127)
         ++it;
@@ -440,13 +472,20 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
           if (conv) {
             st_stage[p] = kConverged;
             st_u[p] = u;
-            k = 0;  // window samples next
+            __threadfence_block();  // u visible before any lane can pop this patch's samples
+            if (nwin > 1) {
+              const int q0 = atomicAdd(&counters[2], nwin - 1);
+              for (int kk = 1; kk < nwin; ++kk) vwq[q0 + kk - 1] = p * nwin + kk;
+            }
+            k = 0;  // this lane evaluates window sample 0
           } else {
             next = true;
           }
+          __threadfence_block();
+          atomicSub(&counters[4], 1);
         }
       }
-      if (next) start(take());
+      if (next) have = next_item();
     }
   }
   __syncthreads();
