@@ -387,7 +387,7 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
   // windows of the last patches instead of waiting for them.
   {
     const int n_pool = counters[0];
-    volatile int* vc = counters;  // [1] pool next, [2] queue head, [3] queue tail, [4] LK running
+    volatile int* vc = counters;  // [1] pool next, [2] queue head, [3] queue tail
     volatile int* vwq = wq;
     int p = -1, k = -1, it = 0, x0 = 0, r0 = 0;
     double u = 0.0, prev = CUDART_INF, lastd = 0.0, mean = 0.0;
@@ -399,7 +399,7 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
       u = st_u[p];
     };
     auto next_item = [&]() -> bool {
-      for (;;) {
+      {
         int t = vc[3];
         while (t < vc[2]) {  // a queued window sample
           const int old = atomicCAS(&counters[3], t, t + 1);
@@ -415,7 +415,6 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
         if (vc[1] < n_pool) {  // a new patch
           const int q = atomicAdd(&counters[1], 1);
           if (q < n_pool) {
-            atomicAdd(&counters[4], 1);
             load(pool[q]);
             k = -1;
             it = 0;
@@ -424,11 +423,10 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
             return true;
           }
         }
-        if (vc[4] == 0) {  // no LK running: once the queue is drained, done
-          __threadfence_block();
-          if (vc[3] >= vc[2]) return false;
-        }
-        __nanosleep(64);
+        // Nothing to take right now: this lane retires (no spinning next to
+        // working lanes of its warp). Samples queued later are still drained:
+        // the lane that queues them keeps taking items until the queue is empty.
+        return false;
       }
     };
     bool have = next_item();
@@ -481,8 +479,6 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
           } else {
             next = true;
           }
-          __threadfence_block();
-          atomicSub(&counters[4], 1);
         }
       }
       if (next) have = next_item();
