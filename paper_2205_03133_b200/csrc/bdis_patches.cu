@@ -258,8 +258,7 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
   double* st_wres = (double*)(smem + lay.oWres);
   int* st_cnt = (int*)(smem + lay.oCnt);
   int* pool = (int*)(smem + lay.oPool);
-  int* counters = (int*)(smem + lay.oCounters);  // [0] pool size, [1..4] see phase 2
-  int* wq = (int*)(smem + lay.oWq);               // queued window samples p*nwin + k
+  int* counters = (int*)(smem + lay.oCounters);  // [0]: pool size, [1]: next to take
   uint8_t* st_stage = smem + lay.oStage;
   uint8_t* st_wok = smem + lay.oWok;
 
@@ -315,8 +314,7 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
     rw.bp = w;
     rofs = 0;
   }
-  if (tid < 8) counters[tid] = 0;
-  for (int q = tid; q < bp.npb * nwin; q += nt) wq[q] = -1;
+  if (tid < 2) counters[tid] = 0;
   __syncthreads();
 
   // ---- phase 1: extract_patch + precompute_patch_system + u0 (:250-262)
@@ -379,58 +377,30 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
   }
   __syncthreads();
 
-  // ---- phase 2: persistent lanes, one residual evaluation per loop trip.
-  // Work items: a new patch from the pool (its LK iterations stay on the lane
-  // that took it) or one window sample of a converged patch. When a lane's LK
-  // converges it queues window samples 1..nwin-1 for any lane and evaluates
-  // sample 0 itself, so near the end of the pool idle lanes absorb the
-  // windows of the last patches instead of waiting for them.
+  // ---- phase 2: persistent lanes, one residual evaluation per loop trip
   {
     const int n_pool = counters[0];
-    volatile int* vc = counters;  // [1] pool next, [2] queue head, [3] queue tail
-    volatile int* vwq = wq;
-    int p = -1, k = -1, it = 0, x0 = 0, r0 = 0;
+    auto take = [&]() {
+      const int q = atomicAdd(&counters[1], 1);
+      return q < n_pool ? pool[q] : -1;
+    };
+    int p = take();
+    int k = -1, it = 0, x0 = 0, r0 = 0;
     double u = 0.0, prev = CUDART_INF, lastd = 0.0, mean = 0.0;
-    auto load = [&](int np) {
+    auto start = [&](int np) {
       p = np;
+      if (p < 0) return;
       x0 = col_start(p % g.nx);
       r0 = row_start(ky0 + p / g.nx) - rofs;
-      mean = st_mean[p];
       u = st_u[p];
+      mean = st_mean[p];
+      k = -1;
+      it = 0;
+      prev = CUDART_INF;
+      lastd = 0.0;
     };
-    auto next_item = [&]() -> bool {
-      {
-        int t = vc[3];
-        while (t < vc[2]) {  // a queued window sample
-          const int old = atomicCAS(&counters[3], t, t + 1);
-          if (old == t) {
-            int item;
-            while ((item = vwq[t]) < 0) __nanosleep(32);  // reserved, being written
-            load(item / nwin);
-            k = item % nwin;
-            return true;
-          }
-          t = old;
-        }
-        if (vc[1] < n_pool) {  // a new patch
-          const int q = atomicAdd(&counters[1], 1);
-          if (q < n_pool) {
-            load(pool[q]);
-            k = -1;
-            it = 0;
-            prev = CUDART_INF;
-            lastd = 0.0;
-            return true;
-          }
-        }
-        // Nothing to take right now: this lane retires (no spinning next to
-        // working lanes of its warp). Samples queued later are still drained:
-        // the lane that queues them keeps taking items until the queue is empty.
-        return false;
-      }
-    };
-    bool have = next_item();
-    while (have) {
+    start(p);
+    while (p >= 0) {
       const double uu = k < 0 ? u : __dadd_rn(u, pp.woff[k]);
       const Ev ev = eval_patch<S, kSmem, kValid, kR64>(rw, w, s, x0, r0, rpad, mean, uu);
       bool next = false;
@@ -438,7 +408,7 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
         // sample_window: valid iff every template pixel was sampled (:31-36)
         st_wres[p * nwin + k] = ev.msq;
         st_wok[p * nwin + k] = ev.n == st_cnt[p];
-        next = true;
+        next = ++k == nwin;
       } else {
         // one iteration of solve_patch_disparity (src/lk_solver.cpp:96-127)
         ++it;
@@ -470,18 +440,13 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
           if (conv) {
             st_stage[p] = kConverged;
             st_u[p] = u;
-            __threadfence_block();  // u visible before any lane can pop this patch's samples
-            if (nwin > 1) {
-              const int q0 = atomicAdd(&counters[2], nwin - 1);
-              for (int kk = 1; kk < nwin; ++kk) vwq[q0 + kk - 1] = p * nwin + kk;
-            }
-            k = 0;  // this lane evaluates window sample 0
+            k = 0;  // window samples next
           } else {
             next = true;
           }
         }
       }
-      if (next) have = next_item();
+      if (next) start(take());
     }
   }
   __syncthreads();
