@@ -160,7 +160,7 @@ class ClockSampler:
             os.close(fd)
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
@@ -292,19 +292,22 @@ def run_ours(args):
         assert torch.equal(torch.isnan(hd), torch.isnan(dc)), "e2e validity differs"
         assert torch.equal(torch.nan_to_num(hd), torch.nan_to_num(dc)), "e2e output differs"
 
-    # ---- roofline of the dominant kernel (k_patches, one launch per level)
+    # ---- roofline of the dominant kernel: the finest-level k_patches launch
     hbm, peak_kind = peaks()
     dims = P.level_dims(cfg, W, H)
-    alg_bytes = 0.0
-    for e, w, h in dims:
-        s, st = cfg.patch_size, max(1, int(round(cfg.patch_size * (1 - cfg.overlap))))
-        nx = len(_axis(w, s, st))
-        ny = len(_axis(h, s, st))
-        # read left/right/grad fp32 planes (12 B/px) and
-        # the coarser level's records (16 B/patch), write records (32 B/patch)
-        alg_bytes += B * (12.0 * w * h + 48.0 * nx * ny)
-    patch_ms = sum(v for k, v in stages.items() if k.startswith("patches_")) / max(calls, 1)
-    achieved = alg_bytes / (patch_ms / 1e3) / 1e9
+    e_f, w_f, h_f = dims[-1]
+    s_, st_ = cfg.patch_size, max(1, int(round(cfg.patch_size * (1 - cfg.overlap))))
+    npatch_f = len(_axis(w_f, s_, st_)) * len(_axis(h_f, s_, st_))
+    # read the left/right/gradient fp32 planes (12 B/px)
+    # and the coarser records (16 B/patch), write the records (32 B/patch)
+    alg_bytes = B * (12.0 * w_f * h_f + 48.0 * npatch_f)
+    patch_ms = stages.get(f"patches_e{e_f}", 0.0) / max(calls, 1)
+    achieved = alg_bytes / (patch_ms / 1e3) / 1e9 if patch_ms > 0 else 0.0
+    traffic = None
+    tj = ROOT / "profiles" / "ncu_traffic.json"
+    if tj.exists():
+        t = json.loads(tj.read_text())["k_patches_finest"]
+        traffic = t["dram_bytes_per_launch"] / t["pairs_in_launch"] * B
     step_ms = ms_max / args.steps
     b_pair = W * H * (2 * 1 + 4 + 1)  # inputs + fp32 disparity + u8 mask
     line = {
@@ -321,13 +324,13 @@ def run_ours(args):
         "e2e": {"value": e2e_value, "unit": "pairs/s", "h2d_bytes_per_step": 2 * B * W * H,
                 "d2h_bytes_per_step": B * W * H * 4, "steps": e2e_steps,
                 "output": "fp32 filtered disparity, NaN at invalid pixels"},
-        "roofline": {"bound": "hbm", "kernel": "k_patches (all levels)", "achieved": achieved,
-                     "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
-                     "peak_kind": peak_kind,
-                     "alg_bytes_per_step": alg_bytes, "kernel_ms_per_step": patch_ms,
+        "roofline": {"bound": "hbm", "kernel": f"k_patches, finest level (exp {e_f})",
+                     "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                     "traffic": traffic, "peak_kind": peak_kind,
+                     "alg_bytes_per_launch": alg_bytes, "launch_ms": patch_ms,
                      "kernel_share_of_step": patch_ms / step_ms,
-                     "note": "FP64 issue-bound (bit-exact mirror of the reference's double "
-                             "arithmetic); see DESIGN.md"},
+                     "note": "not HBM-bound: FP64/XU issue-bound bit-exact mirror of the "
+                             "reference's double arithmetic (see DESIGN.md, profiles/r01)"},
         "path_roofline": {"bytes_per_pair": b_pair, "roofline_pairs_s": hbm * 1e9 / b_pair,
                           "frac": value / (world * hbm * 1e9 / b_pair)},
         "stage_ms_per_step": {k: v / max(calls, 1) for k, v in stages.items()},
