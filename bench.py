@@ -14,7 +14,8 @@ reduction of the timings.
   e2e     the same through the public C ABI with pinned HOST buffers: H2D of
           both views and D2H of the disparity map (NaN = invalid, i.e. the
           validity mask folded in) inside every timed step
-  roofline  dominant kernel (k_patches, all levels) from live CUDA events
+  roofline  dominant kernel (the finest-level k_patches launch) from live CUDA
+          events; traffic from the committed ncu capture (profiles/)
   cpu_baseline  the reference (oracle/_ref, the unmodified reference sources)
           on this host's cores, bounded sample (rank 0, N=1 only)
 
