@@ -177,7 +177,7 @@ struct pstereo_ctx {
   // finest fields
   DevBuf<double> fdisp, fprob, fdepth, fvar, fsigma;  // sized as doubles, typed per call
   DevBuf<uint8_t> fflags;
-  DevBuf<int> flabel, farea;
+  DevBuf<int> flabel, farea, froots, fnroots;
   DevBuf<int> stats;
   // staging for host outputs
   DevBuf<uint8_t> out_stage[10];
@@ -392,6 +392,8 @@ void pstereo_gpu_destroy(pstereo_ctx* ctx) {
   ctx->fflags.release();
   ctx->flabel.release();
   ctx->farea.release();
+  ctx->froots.release();
+  ctx->fnroots.release();
   ctx->stats.release();
   for (auto& b : ctx->out_stage) b.release();
   for (auto e : ctx->chunk_events) cudaEventDestroy(e);
@@ -692,6 +694,9 @@ int run_device(pstereo_ctx* ctx, const std::vector<LevelGeom>& geo, int n, int W
   CK(ctx->fflags.ensure(fnp));
   CK(ctx->flabel.ensure(fnp));
   CK(ctx->farea.ensure(fnp));
+  const size_t ntiles = size_t(ccl_tiles(F.w, F.h)) * n;
+  CK(ctx->froots.ensure(ntiles * ccl_tile_px()));
+  CK(ctx->fnroots.ensure(ntiles));
   FinestBufs fb;
   fb.disp = need_disp ? (void*)ctx->fdisp.p : nullptr;
   fb.prob = need_prob ? (void*)ctx->fprob.p : nullptr;
@@ -699,13 +704,19 @@ int run_device(pstereo_ctx* ctx, const std::vector<LevelGeom>& geo, int n, int W
   fb.var = need_var ? (void*)ctx->fvar.p : nullptr;
   fb.sigma = need_sigma ? (void*)ctx->fsigma.p : nullptr;
   fb.flags = ctx->fflags.p;
-  fb.label = ctx->flabel.p;
   fb.scale_d = fe == 0 ? 1.0 : std::pow(2.0, fe);
   fb.scale_v = fe == 0 ? 1.0 : std::pow(4.0, fe);
   fb.fb = focal * baseline;
   fb.threshold = prm.pixel_threshold;
-  CK(cudaMemsetAsync(ctx->farea.p, 0, fnp * sizeof(int), s));
-  launch_fuse_ccl(F, fb, ctx->mask.p, prm.estimate_variance, f64, W, H, fe, ctx->farea.p, n, s);
+  CclBufs cb;
+  cb.label = ctx->flabel.p;
+  cb.larea = ctx->farea.p;
+  cb.roots = ctx->froots.p;
+  cb.nroots = ctx->fnroots.p;
+  cb.full_w = W;
+  cb.full_h = H;
+  cb.e = fe;
+  launch_fuse_ccl(F, fb, ctx->mask.p, prm.estimate_variance, f64, cb, n, s);
   ctx->launches += 3;
 
   OutputArgs oa;
@@ -717,6 +728,7 @@ int run_device(pstereo_ctx* ctx, const std::vector<LevelGeom>& geo, int n, int W
   oa.fh = F.h;
   oa.fplane = F.plane;
   oa.fb = fb;
+  oa.label = ctx->flabel.p;
   oa.area = ctx->farea.p;
   {
     const long long mp = llround(std::ceil(prm.gamma * double(S) * double(S) - 1e-9));

@@ -279,13 +279,18 @@ cudaError_t launch_pyramid(const PyrArgs& a, bool u8, cudaStream_t s) {
 // 4-connected components of the thresholded finest mask (the full-resolution
 // mask is its block replication, so components and areas carry over with
 // per-pixel area weights, src/depth_variance.cpp:43-92). Three passes:
-//   k_fuse_ccl_local -- (after the fusion) union-find inside a 32x16 tile in smem, every
-//                   pixel labelled with its tile-local root (a global index);
+//   k_fuse_ccl_local -- (after the fusion) components inside a 32x32 tile:
+//                   horizontal runs from ballots, one smem union per
+//                   overlapping run segment, run areas summed at the tile-local
+//                   roots; every kept pixel labelled with its tile-local root
+//                   (a global index), the roots listed per tile;
 //   k_ccl_border -- unions across tile borders in global memory;
-//   k_ccl_final  -- path compression + warp-aggregated component areas.
+//   k_ccl_merge  -- per tile-local root: area added to its global root, link
+//                   compressed to point at it (no per-pixel pass, no memset).
 // Links always point to the smaller index (atomicMin), so the partition --
 // and therefore the kept mask -- does not depend on scheduling.
-constexpr int kTileW = 32, kTileH = 16;
+constexpr int kTileW = 32, kTileH = 32, kTilePx = kTileW * kTileH;
+constexpr int kFuseThreads = 256, kFuseWarps = kFuseThreads / 32, kFuseRows = kTileH / kFuseWarps;
 
 template <typename Ptr>
 __device__ __forceinline__ int uf_find(Ptr lab, int p) {
@@ -314,137 +319,217 @@ __device__ __forceinline__ void uf_union(Ptr lab, int* raw, int a, int b) {
   }
 }
 
-// Shared-memory copy of the patch records covering one tile.
+// tile-local index of the first pixel of the run holding `lane` in `bits`
+__device__ __forceinline__ int run_start(unsigned bits, int row, int lane) {
+  const unsigned starts = bits & ~(bits << 1);
+  const unsigned upto = starts & (0xffffffffu >> (31 - lane));
+  return row * kTileW + (31 - __clz(upto));
+}
+
+// Shared-memory copy of the patch records covering one tile; records that are
+// not accepted carry zero weight (prob = u = sigma = 0), which leaves the
+// fusion sums bit-identical to skipping them (sums start at +0.0 and never
+// become -0.0 under round-to-nearest, so adding +0.0 is the identity).
 struct TileRecords {
-  const uint8_t* st;
   const double* pr;
   const double* uu;
   const double* sg;
   int ky0, kx0, ncol;
-  __device__ __forceinline__ int at(int ky, int kx) const { return (ky - ky0) * ncol + (kx - kx0); }
-  __device__ __forceinline__ uint8_t stage(int ky, int kx) const { return st[at(ky, kx)]; }
-  __device__ __forceinline__ double prob(int ky, int kx) const { return pr[at(ky, kx)]; }
-  __device__ __forceinline__ double u(int ky, int kx) const { return uu[at(ky, kx)]; }
-  __device__ __forceinline__ double sigma(int ky, int kx) const { return sg[at(ky, kx)]; }
 };
 
-constexpr int kTileRec = 160;  // max covering patches per 32x16 tile (stride >= 2, s <= 32)
+constexpr int kTileRec = 320;  // records staged per tile; more -> global gather
+
+template <bool kVar>
+__device__ __forceinline__ Fused gather_tile(const Grid& g, const TileRecords& rec, int x, int y,
+                                             Cover cx, Cover cy,
+                                             const double* __restrict__ mask) {
+  const int s = g.size, st = g.stride;
+  Fused f{0.0, 0.0, 0.0, 0.0};
+  auto add = [&](int q, double m) {
+    const double pr = rec.pr[q];
+    const double w = __dmul_rn(pr, m);
+    f.sw = __dadd_rn(f.sw, w);
+    f.swu = __dadd_rn(f.swu, __dmul_rn(w, rec.uu[q]));
+    f.swp = __dadd_rn(f.swp, __dmul_rn(w, pr));
+    if (kVar) {
+      const double sk = rec.sg[q];
+      f.sw2s = __dadd_rn(f.sw2s, __dmul_rn(__dmul_rn(__dmul_rn(w, w), sk), sk));
+    }
+  };
+  auto row = [&](int ky, int y0) {
+    const double* mrow = mask + (y - y0) * s + x;
+    const int qrow = (ky - rec.ky0) * rec.ncol - rec.kx0;
+    for (int kx = cx.lo; kx <= cx.hi; ++kx) add(qrow + kx, mrow[-kx * st]);
+    if (cx.last) add(qrow + g.nx - 1, mrow[-g.lastx0]);
+  };
+  // ascending patch index: rows ky ascending, columns kx ascending (:122-135)
+  for (int ky = cy.lo; ky <= cy.hi; ++ky) row(ky, ky * st);
+  if (cy.last) row(g.ny - 1, g.lasty0);
+  return f;
+}
 
 // fuse_level at the finest level (src/coarse_to_fine.cpp:101-150) with the
 // probability threshold of filter_validity (src/depth_variance.cpp:81-86),
-// then the tile-local pass of the component labelling -- one CTA per 32x16
-// tile. The records of the covering patches are staged in shared memory and
-// each pixel gathers them in ascending patch index (fuse_level's order).
+// then the tile-local pass of the component labelling -- one CTA per 32x32
+// tile, each warp four rows, each thread one column (its column cover is
+// computed once). The records of the covering patches are staged in shared
+// memory and each pixel gathers them in ascending patch index.
 template <bool kVar, typename T>
-__global__ void __launch_bounds__(kTileW * kTileH) k_fuse_ccl_local(
-    Level L, FinestBufs fb, const double* __restrict__ mask) {
-  __shared__ int sl[kTileW * kTileH];
-  __shared__ double s_pr[kTileRec], s_u[kTileRec], s_sg[kTileRec];
-  __shared__ uint8_t s_st[kTileRec];
+__global__ void __launch_bounds__(kFuseThreads) k_fuse_ccl_local(
+    Level L, FinestBufs fb, const double* __restrict__ mask, CclBufs cb) {
+  __shared__ int sl[kTilePx];
+  __shared__ int s_area[kTilePx];
+  __shared__ unsigned s_bits[kTileH];
+  __shared__ double s_pr[kTileRec], s_u[kTileRec], s_sg[kVar ? kTileRec : 1];
+  __shared__ Cover s_cy[kTileH];
+  __shared__ double s_mask[kMaxPatch * kMaxPatch];
+  __shared__ int s_nroot;
   const Grid& g = L.g;
   const int w = L.w, h = L.h;
   const int tiles_x = (w + kTileW - 1) / kTileW;
-  const int tx0 = (blockIdx.x % tiles_x) * kTileW, ty0 = (blockIdx.x / tiles_x) * kTileH;
+  const int tile = blockIdx.x;
+  const int tx0 = (tile % tiles_x) * kTileW, ty0 = (tile / tiles_x) * kTileH;
   const long long pair = blockIdx.y;
-  const int t = threadIdx.x, lx = t % kTileW, ly = t / kTileW;
-  const int x = tx0 + lx, y = ty0 + ly;
-  int kx0, kx1, ky0, ky1;
-  covering_range(tx0, min(tx0 + kTileW, w) - 1, g.nx, g.size, g.stride, g.lastx0, &kx0, &kx1);
-  covering_range(ty0, min(ty0 + kTileH, h) - 1, g.ny, g.size, g.stride, g.lasty0, &ky0, &ky1);
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int x = tx0 + lane;
+  const int wl = min(kTileW, w - tx0) - 1, hl = min(kTileH, h - ty0) - 1;
+  const Cover cx = cover_of(x, g.nx, g.size, g.stride, g.lastx0);
+  // covering_range of the tile's columns from the first / last lane's covers
+  const int lo0 = __shfl_sync(0xffffffffu, cx.lo, 0);
+  const int hi1 = __shfl_sync(0xffffffffu, cx.hi, wl);
+  const bool last1 = __shfl_sync(0xffffffffu, (int)cx.last, wl) != 0;
+  const int kx0 = min(g.nx - 1, lo0);
+  const int kx1 = max(kx0, last1 ? g.nx - 1 : hi1);
+  if (t < kTileH) s_cy[t] = cover_of(ty0 + t, g.ny, g.size, g.stride, g.lasty0);
+  for (int q = t; q < g.size * g.size; q += kFuseThreads) s_mask[q] = mask[q];
+  if (t == 0) s_nroot = 0;
+  __syncthreads();
+  const int ky0 = min(g.ny - 1, s_cy[0].lo);
+  const int ky1 = max(ky0, s_cy[hl].last ? g.ny - 1 : s_cy[hl].hi);
   const int ncol = kx1 - kx0 + 1, nrec = ncol * (ky1 - ky0 + 1);
-  const long long rbase = pair * (long long)g.nx * g.ny;
   const bool staged = nrec <= kTileRec;
-  // covering ranges per tile column / row (no integer divisions per pixel)
-  __shared__ Cover s_cx[kTileW], s_cy[kTileH];
-  __shared__ double s_mask[kMaxPatch * kMaxPatch];
-  if (t < kTileW) s_cx[t] = cover_of(tx0 + t, g.nx, g.size, g.stride, g.lastx0);
-  else if (t < kTileW + kTileH) s_cy[t - kTileW] = cover_of(ty0 + t - kTileW, g.ny, g.size, g.stride, g.lasty0);
-  for (int q = t; q < g.size * g.size; q += blockDim.x) s_mask[q] = mask[q];
   if (staged) {
-    for (int q = t; q < nrec; q += blockDim.x) {
+    const long long rbase = pair * (long long)g.nx * g.ny;
+    for (int q = t; q < nrec; q += kFuseThreads) {
       const long long r = rbase + (long long)(ky0 + q / ncol) * g.nx + kx0 + q % ncol;
-      s_st[q] = L.stage[r];
-      s_pr[q] = L.prob[r];
-      s_u[q] = L.u[r];
-      if (kVar) s_sg[q] = L.sigma[r];
+      const bool acc = L.stage[r] == kAccepted;  // fuse_level skips the rest (:127)
+      s_pr[q] = acc ? L.prob[r] : 0.0;
+      s_u[q] = acc ? L.u[r] : 0.0;
+      if (kVar) s_sg[q] = acc ? L.sigma[r] : 0.0;
     }
   }
   __syncthreads();
-  bool keep = false;
-  if (x < w && y < h) {
-    Fused f;
-    if (staged) {
-      const TileRecords rec{s_st, s_pr, s_u, s_sg, ky0, kx0, ncol};
-      f = gather_cover<true, kVar>(g, rec, x, y, s_cx[lx], s_cy[ly], s_mask);
-    } else {
-      f = gather<true, kVar>(L, pair, x, y, mask);
-    }
-    const long long o = pair * L.plane + (long long)y * w + x;
-    const bool valid = !(f.sw <= 0.0);  // fuse_level: sw <= 0 stays invalid (:138)
-    double d = 0.0, p = 0.0, v = 0.0;
-    if (valid) {
-      d = __ddiv_rn(f.swu, f.sw);
-      p = __ddiv_rn(f.swp, f.sw);
-      if (kVar) v = __ddiv_rn(f.sw2s, __dmul_rn(f.sw, f.sw));
-    }
-    // upsample_to_full values (:166-180): scale 2^fe, 1, 4^fe where valid, else 0
-    const double D = valid ? __dmul_rn(fb.scale_d, d) : 0.0;
-    const double Pv = valid ? __dmul_rn(1.0, p) : 0.0;
-    const double V = valid ? __dmul_rn(fb.scale_v, v) : 0.0;
-    const bool deep = D >= 0.1;  // kMinDisparity (inc/depth_variance.hpp:13)
-    keep = valid && !(Pv < fb.threshold);  // filter_validity threshold (:84)
-    if (fb.disp) ((T*)fb.disp)[o] = (T)D;
-    if (fb.prob) ((T*)fb.prob)[o] = (T)Pv;
-    if (fb.depth) ((T*)fb.depth)[o] = (T)(deep ? __ddiv_rn(fb.fb, D) : 0.0);
-    if (kVar) {
-      if (fb.var) ((T*)fb.var)[o] = (T)V;
-      if (fb.sigma) {
-        double sg = 0.0;
-        if (deep && valid) {
-          const double vv = (V < 0.0) ? 0.0 : V;  // std::max(var, 0.0)
-          sg = __dmul_rn(__ddiv_rn(fb.fb, __dmul_rn(D, D)), __dsqrt_rn(vv));
+  const TileRecords rec{s_pr, s_u, s_sg, ky0, kx0, ncol};
+  const long long pbase = pair * L.plane;
+#pragma unroll 1
+  for (int i = 0; i < kFuseRows; ++i) {
+    const int ly = warp + i * kFuseWarps, y = ty0 + ly;
+    bool keep = false;
+    if (x < w && y < h) {
+      const Fused f = staged ? gather_tile<kVar>(g, rec, x, y, cx, s_cy[ly], s_mask)
+                             : gather<true, kVar>(L, pair, x, y, mask);
+      const long long o = pbase + (long long)y * w + x;
+      const bool valid = !(f.sw <= 0.0);  // fuse_level: sw <= 0 stays invalid (:138)
+      double d = 0.0, p = 0.0, v = 0.0;
+      if (valid) {
+        d = __ddiv_rn(f.swu, f.sw);
+        p = __ddiv_rn(f.swp, f.sw);
+        if (kVar) v = __ddiv_rn(f.sw2s, __dmul_rn(f.sw, f.sw));
+      }
+      // upsample_to_full values (:166-180): scale 2^fe, 1, 4^fe where valid, else 0
+      const double D = valid ? __dmul_rn(fb.scale_d, d) : 0.0;
+      const double Pv = valid ? __dmul_rn(1.0, p) : 0.0;
+      const double V = valid ? __dmul_rn(fb.scale_v, v) : 0.0;
+      const bool deep = D >= 0.1;  // kMinDisparity (inc/depth_variance.hpp:13)
+      keep = valid && !(Pv < fb.threshold);  // filter_validity threshold (:84)
+      if (fb.disp) ((T*)fb.disp)[o] = (T)D;
+      if (fb.prob) ((T*)fb.prob)[o] = (T)Pv;
+      if (fb.depth) ((T*)fb.depth)[o] = (T)(deep ? __ddiv_rn(fb.fb, D) : 0.0);
+      if (kVar) {
+        if (fb.var) ((T*)fb.var)[o] = (T)V;
+        if (fb.sigma) {
+          double sg = 0.0;
+          if (deep && valid) {
+            const double vv = (V < 0.0) ? 0.0 : V;  // std::max(var, 0.0)
+            sg = __dmul_rn(__ddiv_rn(fb.fb, __dmul_rn(D, D)), __dsqrt_rn(vv));
+          }
+          ((T*)fb.sigma)[o] = (T)sg;
         }
-        ((T*)fb.sigma)[o] = (T)sg;
       }
+      fb.flags[o] = (valid ? kFlagMatch : 0) | (keep ? kFlagKeep : 0) | (deep ? kFlagDepth : 0);
     }
-    fb.flags[o] = (valid ? kFlagMatch : 0) | (keep ? kFlagKeep : 0) | (deep ? kFlagDepth : 0);
+    const unsigned bits = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) s_bits[ly] = bits;
+    const int idx = ly * kTileW + lane;
+    if (keep && !(lane > 0 && ((bits >> (lane - 1)) & 1u))) {  // run start
+      sl[idx] = idx;
+      s_area[idx] = 0;
+    }
   }
-  // ---- tile-local components: run labels (ballot bit tricks) + union-find
-  const unsigned bits = __ballot_sync(0xffffffffu, keep);
-  const unsigned starts = bits & ~(bits << 1);
-  const unsigned upto = starts & (0xffffffffu >> (31 - lx));
-  sl[t] = keep ? ly * kTileW + (31 - __clz(upto)) : -1;
   __syncthreads();
+  // one union per column segment where a run overlaps the run above it
   volatile int* vl = sl;
-  if (keep && ly > 0 && sl[t - kTileW] >= 0) {
-    int a = sl[t], b = sl[t - kTileW];
+  for (int i = 0; i < kFuseRows; ++i) {
+    const int ly = warp + i * kFuseWarps;
+    if (ly == 0) continue;
+    const unsigned b = s_bits[ly], a = s_bits[ly - 1];
+    const unsigned both = a & b;
+    if (!(((both & ~(both << 1)) >> lane) & 1u)) continue;
+    int ra = run_start(b, ly, lane), rb = run_start(a, ly - 1, lane);
     for (;;) {
-      while (vl[a] != a) {
-        const int gg = vl[vl[a]];
-        vl[a] = gg;
-        a = gg;
+      while (vl[ra] != ra) {
+        const int gg = vl[vl[ra]];
+        vl[ra] = gg;
+        ra = gg;
       }
-      while (vl[b] != b) {
-        const int gg = vl[vl[b]];
-        vl[b] = gg;
-        b = gg;
+      while (vl[rb] != rb) {
+        const int gg = vl[vl[rb]];
+        vl[rb] = gg;
+        rb = gg;
       }
-      if (a == b) break;
-      if (a < b) {
-        const int tmp = a;
-        a = b;
-        b = tmp;
+      if (ra == rb) break;
+      if (ra < rb) {
+        const int tmp = ra;
+        ra = rb;
+        rb = tmp;
       }
-      const int old = atomicMin(&sl[a], b);
-      if (old == a) break;
-      a = old;
+      const int old = atomicMin(&sl[ra], rb);
+      if (old == ra) break;
+      ra = old;
     }
   }
   __syncthreads();
-  if (keep) {
-    const int r = uf_find(vl, t);
-    fb.label[pair * L.plane + (long long)y * w + x] = (ty0 + r / kTileW) * w + tx0 + r % kTileW;
+  // labels and run areas (weights: full-resolution pixels per finest pixel)
+  const int full = 1 << cb.e;
+  for (int i = 0; i < kFuseRows; ++i) {
+    const int ly = warp + i * kFuseWarps, y = ty0 + ly;
+    const unsigned bits = s_bits[ly];
+    if (!((bits >> lane) & 1u)) continue;
+    const int idx = ly * kTileW + lane;
+    const int s0 = run_start(bits, ly, lane);
+    const int root = uf_find(sl, s0);
+    cb.label[pbase + (long long)y * w + x] = (ty0 + root / kTileW) * w + tx0 + root % kTileW;
+    if (s0 == idx) {
+      const unsigned rest = ~(bits >> lane);
+      const int len = rest ? __ffs(rest) - 1 : 32;
+      int sx = len << cb.e;
+      if (x + len - 1 == w - 1) sx -= full - min(full, cb.full_w - ((w - 1) << cb.e));
+      atomicAdd(&s_area[root], sx * min(full, cb.full_h - (y << cb.e)));
+    }
   }
+  __syncthreads();
+  const long long tid = pair * gridDim.x + tile;
+  for (int i = 0; i < kFuseRows; ++i) {
+    const int ly = warp + i * kFuseWarps;
+    const int idx = ly * kTileW + lane;
+    const unsigned bits = s_bits[ly];
+    if (!((bits >> lane) & 1u) || sl[idx] != idx) continue;
+    const int gi = (ty0 + ly) * w + x;
+    cb.larea[pbase + gi] = s_area[idx];
+    cb.roots[tid * kTilePx + atomicAdd(&s_nroot, 1)] = gi;
+  }
+  __syncthreads();
+  if (t == 0) cb.nroots[tid] = s_nroot;
 }
 
 __global__ void k_ccl_border(int w, int h, long long plane, const uint8_t* __restrict__ mask,
@@ -475,28 +560,24 @@ __global__ void k_ccl_border(int w, int h, long long plane, const uint8_t* __res
   if (mask[base + j] & kFlagKeep) uf_union(vl, l, i, j);
 }
 
-__global__ void k_ccl_final(int w, int h, long long plane, int full_w, int full_h, int e,
-                            const uint8_t* __restrict__ mask, int* lab, int* area) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const long long base = blockIdx.y * plane;
-  const bool m = i < w * h && (mask[base + i] & kFlagKeep);
-  int root = -1, weight = 0;
-  if (m) {
-    volatile int* vl = lab + base;
-    root = uf_find(vl, i);
-    lab[base + i] = root;
-    const int x = i % w, y = i / w;
-    weight = min(1 << e, full_w - (x << e)) * min(1 << e, full_h - (y << e));
-  }
-  // one atomic per distinct root in the warp
-  unsigned pending = __ballot_sync(0xffffffffu, m);
-  while (pending) {
-    const int leader = __ffs(pending) - 1;
-    const int r = __shfl_sync(0xffffffffu, root, leader);
-    const bool mine = m && root == r;
-    const int sum = __reduce_add_sync(0xffffffffu, mine ? weight : 0);
-    if ((int)(threadIdx.x & 31) == leader) atomicAdd(&area[base + r], sum);
-    pending &= ~__ballot_sync(0xffffffffu, mine);
+// one warp per tile: every tile-local root adds its area to its global root
+// (roots never receive from themselves, so the read of a non-root's area does
+// not race) and is linked straight to it for k_output's two-load lookup
+__global__ void k_ccl_merge(int n_tiles, int n_pairs, long long plane, CclBufs cb) {
+  const long long wid = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (wid >= (long long)n_tiles * n_pairs) return;
+  const long long pair = wid / n_tiles;
+  const int n = cb.nroots[wid];
+  const int* rl = cb.roots + wid * kTilePx;
+  int* lab = cb.label + pair * plane;
+  volatile int* vl = lab;
+  for (int k = threadIdx.x & 31; k < n; k += 32) {
+    const int r = rl[k];
+    const int R = uf_find(vl, r);
+    if (R != r) {
+      atomicAdd(&cb.larea[pair * plane + R], cb.larea[pair * plane + r]);
+      vl[r] = R;
+    }
   }
 }
 
@@ -516,7 +597,10 @@ __global__ void k_output(OutputArgs a) {
   const uint8_t fl = a.fb.flags[f];
   const bool mv = fl & kFlagMatch;
   bool keep = false;
-  if (fl & kFlagKeep) keep = a.area[pair * a.fplane + a.fb.label[f]] >= a.min_px;
+  if (fl & kFlagKeep) {  // local root -> global root (k_ccl_merge) -> component area
+    const int* lab = a.label + pair * a.fplane;
+    keep = a.area[pair * a.fplane + lab[lab[i]]] >= a.min_px;
+  }
   const bool dv = keep && (fl & kFlagDepth);  // depth valid; sigma valid too (var valid == mv)
   T d = a.fb.disp ? ((const T*)a.fb.disp)[f] : (T)0;
   const T p = a.fb.prob ? ((const T*)a.fb.prob)[f] : (T)0;
@@ -632,25 +716,27 @@ void launch_level_tables(const Level& L, int n_pairs, cudaStream_t s) {
 }
 
 void launch_fuse_ccl(const Level& L, const FinestBufs& fb, const double* mask, int want_var,
-                     int f64, int full_w, int full_h, int e, int* area, int n_pairs,
-                     cudaStream_t s) {
+                     int f64, const CclBufs& cb, int n_pairs, cudaStream_t s) {
   const int w = L.w, h = L.h;
   const long long plane = L.plane;
-  const int tx = (w + kTileW - 1) / kTileW, ty = (h + kTileH - 1) / kTileH;
-  const dim3 grid(tx * ty, n_pairs);
+  const int nt = ccl_tiles(w, h);
+  const dim3 grid(nt, n_pairs);
   if (want_var) {
-    if (f64) k_fuse_ccl_local<true, double><<<grid, kTileW * kTileH, 0, s>>>(L, fb, mask);
-    else k_fuse_ccl_local<true, float><<<grid, kTileW * kTileH, 0, s>>>(L, fb, mask);
+    if (f64) k_fuse_ccl_local<true, double><<<grid, kFuseThreads, 0, s>>>(L, fb, mask, cb);
+    else k_fuse_ccl_local<true, float><<<grid, kFuseThreads, 0, s>>>(L, fb, mask, cb);
   } else {
-    if (f64) k_fuse_ccl_local<false, double><<<grid, kTileW * kTileH, 0, s>>>(L, fb, mask);
-    else k_fuse_ccl_local<false, float><<<grid, kTileW * kTileH, 0, s>>>(L, fb, mask);
+    if (f64) k_fuse_ccl_local<false, double><<<grid, kFuseThreads, 0, s>>>(L, fb, mask, cb);
+    else k_fuse_ccl_local<false, float><<<grid, kFuseThreads, 0, s>>>(L, fb, mask, cb);
   }
+  const int tx = (w + kTileW - 1) / kTileW, ty = (h + kTileH - 1) / kTileH;
   const long long nb = (long long)(tx - 1) * h + (long long)(ty - 1) * w;
   if (nb > 0)
-    k_ccl_border<<<dim3(blocks_for(nb, 256), n_pairs), 256, 0, s>>>(w, h, plane, fb.flags, fb.label);
-  k_ccl_final<<<dim3(blocks_for((long long)w * h, 256), n_pairs), 256, 0, s>>>(
-      w, h, plane, full_w, full_h, e, fb.flags, fb.label, area);
+    k_ccl_border<<<dim3(blocks_for(nb, 256), n_pairs), 256, 0, s>>>(w, h, plane, fb.flags, cb.label);
+  k_ccl_merge<<<blocks_for((long long)nt * n_pairs * 32, 256), 256, 0, s>>>(nt, n_pairs, plane, cb);
 }
+
+int ccl_tiles(int w, int h) { return ((w + kTileW - 1) / kTileW) * ((h + kTileH - 1) / kTileH); }
+int ccl_tile_px() { return kTilePx; }
 
 void launch_output(const OutputArgs& a, int f64, int n_pairs, cudaStream_t s) {
   dim3 grid(blocks_for((long long)a.fw * a.fh, 256), n_pairs);

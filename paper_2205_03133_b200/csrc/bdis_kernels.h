@@ -113,16 +113,28 @@ struct FinestBufs {
   void* var;    // scale_v * v
   void* sigma;  // fb / D^2 * sqrt(max(V, 0)) where D >= 0.1
   uint8_t* flags;
-  int* label;
   double scale_d, scale_v, fb, threshold;
 };
 enum FinestFlag : uint8_t { kFlagMatch = 1, kFlagKeep = 2, kFlagDepth = 4 };
+
+// component labelling state at the finest level (per pair: one plane of
+// labels and areas, ccl_tiles() root lists of ccl_tile_px() entries)
+struct CclBufs {
+  int* label;   // kept pixel -> tile-local root; tile-local root -> global root
+  int* larea;   // at tile-local roots: tile-local area; at global roots: total
+  int* roots;   // [pair][tile][ccl_tile_px()] tile-local roots (global indices)
+  int* nroots;  // [pair][tile]
+  int full_w, full_h, e;
+};
+int ccl_tiles(int w, int h);
+int ccl_tile_px();
 
 struct OutputArgs {
   int W, H, e, fw, fh;
   long long fplane;
   FinestBufs fb;
-  const int* area;
+  const int* label;
+  const int* area;  // component area at global roots (CclBufs::larea)
   long long min_px;
   void* out_disp;
   uint8_t* out_dvalid;
@@ -156,8 +168,7 @@ cudaError_t launch_patches(const Level& L, const Level& P, const PatchParams& pp
                            const BandPlan& bp, cudaStream_t s);
 // fuse_level (finest) + threshold + 4-connected components with area sums
 void launch_fuse_ccl(const Level& L, const FinestBufs& fb, const double* mask, int want_var,
-                     int f64, int full_w, int full_h, int e, int* area, int n_pairs,
-                     cudaStream_t s);
+                     int f64, const CclBufs& cb, int n_pairs, cudaStream_t s);
 cudaError_t launch_debug_eval(const Level& L, int size, int all_valid, int nq, const int* qx,
                               const int* qy, const double* qu, double* msq, double* jr, int* n,
                               cudaStream_t s);

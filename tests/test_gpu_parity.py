@@ -67,6 +67,17 @@ def test_odd_dimensions(gpu, port, w, h):
     _check(P, port, cfg, l[None], r[None])
 
 
+@pytest.mark.parametrize("w,h", [(97, 75), (131, 67)])
+def test_odd_dimensions_upsampled(gpu, port, w, h):
+    """Odd full-resolution sizes with finest_exp 1: the last finest column/row
+    covers one full-resolution pixel, which the component areas must weigh."""
+    P = gpu
+    l, r = P.synth_pair(0, seed=6, width=w, height=h, blur_sigma=8.0, d_range=6.0, d_min=1.0)
+    cfg = P.PipelineConfig(coarsest_exp=2, finest_exp=1, patch_size=6, overlap=0.5,
+                           estimate_variance=True, gamma=0.05)
+    _check(P, port, cfg, l[None], r[None])
+
+
 def test_rgb_and_rgba_validity(gpu, port):
     P = gpu
     l, r = P.synth_pair(0, seed=11, width=160, height=120, channels=3)
