@@ -523,7 +523,8 @@ __global__ void __launch_bounds__(kFuseThreads) k_fuse_ccl_local(
     const int ly = warp + i * kFuseWarps;
     const int idx = ly * kTileW + lane;
     const unsigned bits = s_bits[ly];
-    if (!((bits >> lane) & 1u) || sl[idx] != idx) continue;
+    // roots are run starts whose link is themselves (sl holds nothing elsewhere)
+    if (!(((bits & ~(bits << 1)) >> lane) & 1u) || sl[idx] != idx) continue;
     const int gi = (ty0 + ly) * w + x;
     cb.larea[pbase + gi] = s_area[idx];
     cb.roots[tid * kTilePx + atomicAdd(&s_nroot, 1)] = gi;

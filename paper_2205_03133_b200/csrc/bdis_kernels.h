@@ -46,7 +46,7 @@ struct BandPlan {
 struct BandLayout {
   size_t oR, oL, oG, oLQ, oRQ;
   size_t oMean, oHess, oTmsq, oU, oWres;
-  size_t oCnt, oPool, oCounters;
+  size_t oCnt, oPool, oWlist, oCounters;
   size_t oStage, oWok;
   size_t total;
 };
@@ -73,6 +73,7 @@ __host__ __device__ inline BandLayout band_layout(int rows, int rpitch, int fpit
   l.oWres = take(size_t(npb) * nwin * 8, 8);
   l.oCnt = take(size_t(npb) * 4, 4);
   l.oPool = take(size_t(npb) * 4, 4);
+  l.oWlist = take(size_t(npb) * 4, 4);
   l.oCounters = take(4 * 4, 4);
   l.oStage = take(size_t(npb), 1);
   l.oWok = take(size_t(npb) * nwin, 1);

@@ -68,7 +68,7 @@ struct Rows {
 
 // eval_patch_residual (src/lk_solver.cpp:38-81) of a lattice patch whose
 // footprint starts at column x0 and row r0 of `rw`, at disparity u.
-template <int S, bool kSmem, bool kValid, bool kR64>
+template <int S, bool kSmem, bool kValid, bool kR64, bool kJr = true>
 __device__ __forceinline__ Ev eval_patch(const Rows<kSmem, kR64>& rw, int w, int s_rt, int x0,
                                          int r0, int rpad, double mean, double u) {
   constexpr int SA = S > 0 ? S : kMaxPatch;
@@ -157,7 +157,7 @@ __device__ __forceinline__ Ev eval_patch(const Rows<kSmem, kR64>& rw, int w, int
         // r * 1 == r; masked columns: r * 0 = +-0 adds nothing to ssr / jr
         const double r = __dmul_rn(__dsub_rn(__dsub_rn(v, rmean), t), mk[i]);
         ssr = __dadd_rn(ssr, __dmul_rn(r, r));
-        jr = __dadd_rn(jr, __dmul_rn((double)gr[offT[i]], r));
+        if (kJr) jr = __dadd_rn(jr, __dmul_rn((double)gr[offT[i]], r));
       }
     }
     ev.msq = __ddiv_rn(ssr, (double)n);
@@ -212,7 +212,7 @@ __device__ __forceinline__ Ev eval_patch(const Rows<kSmem, kR64>& rw, int w, int
         const double t = __dsub_rn((double)lr[rw.s4(x0 + i)], mean);
         const double r = __dsub_rn(__dsub_rn(v, rmean), t);
         ssr = __dadd_rn(ssr, __dmul_rn(r, r));
-        jr = __dadd_rn(jr, __dmul_rn((double)gr[rw.s4(x0 + i)], r));
+        if (kJr) jr = __dadd_rn(jr, __dmul_rn((double)gr[rw.s4(x0 + i)], r));
       }
     }
   }
@@ -258,7 +258,8 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
   double* st_wres = (double*)(smem + lay.oWres);
   int* st_cnt = (int*)(smem + lay.oCnt);
   int* pool = (int*)(smem + lay.oPool);
-  int* counters = (int*)(smem + lay.oCounters);  // [0]: pool size, [1]: next to take
+  int* wlist = (int*)(smem + lay.oWlist);
+  int* counters = (int*)(smem + lay.oCounters);  // pool size, next to take, converged
   uint8_t* st_stage = smem + lay.oStage;
   uint8_t* st_wok = smem + lay.oWok;
 
@@ -314,7 +315,7 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
     rw.bp = w;
     rofs = 0;
   }
-  if (tid < 2) counters[tid] = 0;
+  if (tid < 3) counters[tid] = 0;
   __syncthreads();
 
   // ---- phase 1: extract_patch + precompute_patch_system + u0 (:250-262)
@@ -377,7 +378,8 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
   }
   __syncthreads();
 
-  // ---- phase 2: persistent lanes, one residual evaluation per loop trip
+  // ---- phase 2a: persistent lanes run the LK solves (one residual evaluation
+  // per loop trip) and take the next patch from the pool when one ends
   {
     const int n_pool = counters[0];
     auto take = [&]() {
@@ -385,7 +387,7 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
       return q < n_pool ? pool[q] : -1;
     };
     int p = take();
-    int k = -1, it = 0, x0 = 0, r0 = 0;
+    int it = 0, x0 = 0, r0 = 0;
     double u = 0.0, prev = CUDART_INF, lastd = 0.0, mean = 0.0;
     auto start = [&](int np) {
       p = np;
@@ -394,59 +396,63 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
       r0 = row_start(ky0 + p / g.nx) - rofs;
       u = st_u[p];
       mean = st_mean[p];
-      k = -1;
       it = 0;
       prev = CUDART_INF;
       lastd = 0.0;
     };
     start(p);
     while (p >= 0) {
-      const double uu = k < 0 ? u : __dadd_rn(u, pp.woff[k]);
-      const Ev ev = eval_patch<S, kSmem, kValid, kR64>(rw, w, s, x0, r0, rpad, mean, uu);
-      bool next = false;
-      if (k >= 0) {
-        // sample_window: valid iff every template pixel was sampled (:31-36)
-        st_wres[p * nwin + k] = ev.msq;
-        st_wok[p * nwin + k] = ev.n == st_cnt[p];
-        next = ++k == nwin;
+      const Ev ev = eval_patch<S, kSmem, kValid, kR64>(rw, w, s, x0, r0, rpad, mean, u);
+      // one iteration of solve_patch_disparity (src/lk_solver.cpp:96-127)
+      ++it;
+      bool done = false, conv = false;
+      if (ev.n == 0) {
+        done = true;
       } else {
-        // one iteration of solve_patch_disparity (src/lk_solver.cpp:96-127)
-        ++it;
-        bool done = false, conv = false;
-        if (ev.n == 0) {
-          done = true;
-        } else {
-          const double r = ev.msq;
-          if (it >= pp.min_it) {
-            if (r < pp.stop_good) {
-              conv = done = true;
-            } else if (r > __dmul_rn(pp.stop_bad, st_tmsq[p])) {
-              done = true;
-            } else if (isfinite(prev) && __dsub_rn(prev, r) < __dmul_rn(pp.stop_improve, prev)) {
-              conv = it > 1 && fabs(lastd) < 1e-2;
-              done = true;
-            }
-          }
-          if (!done) {
-            const double delta = __ddiv_rn(ev.jr, st_hess[p]);
-            u = __dadd_rn(u, delta);
-            lastd = delta;
-            prev = r;
-            if (fabs(delta) < 1e-2) conv = done = true;  // kUpdateEpsilon
-            else if (it >= pp.max_it) done = true;
+        const double r = ev.msq;
+        if (it >= pp.min_it) {
+          if (r < pp.stop_good) {
+            conv = done = true;
+          } else if (r > __dmul_rn(pp.stop_bad, st_tmsq[p])) {
+            done = true;
+          } else if (isfinite(prev) && __dsub_rn(prev, r) < __dmul_rn(pp.stop_improve, prev)) {
+            conv = it > 1 && fabs(lastd) < 1e-2;
+            done = true;
           }
         }
-        if (done) {
-          if (conv) {
-            st_stage[p] = kConverged;
-            st_u[p] = u;
-            k = 0;  // window samples next
-          } else {
-            next = true;
-          }
+        if (!done) {
+          const double delta = __ddiv_rn(ev.jr, st_hess[p]);
+          u = __dadd_rn(u, delta);
+          lastd = delta;
+          prev = r;
+          if (fabs(delta) < 1e-2) conv = done = true;  // kUpdateEpsilon
+          else if (it >= pp.max_it) done = true;
         }
       }
-      if (next) start(take());
+      if (done) {
+        if (conv) {
+          st_stage[p] = kConverged;
+          st_u[p] = u;
+          wlist[atomicAdd(&counters[2], 1)] = p;
+        }
+        start(take());
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- phase 2b: the window samples of every converged patch (:31-36), one
+  // evaluation per job, dealt round-robin over all lanes (no tail)
+  {
+    const int jobs = counters[2] * nwin;
+    for (int j = tid; j < jobs; j += nt) {
+      const int p = wlist[j / nwin], k = j - (j / nwin) * nwin;
+      const Ev ev = eval_patch<S, kSmem, kValid, kR64, false>(
+          rw, w, s, col_start(p % g.nx), row_start(ky0 + p / g.nx) - rofs, rpad, st_mean[p],
+          __dadd_rn(st_u[p], pp.woff[k]));
+      // sample_window: valid iff every template pixel was sampled
+      st_wres[p * nwin + k] = ev.msq;
+      st_wok[p * nwin + k] = ev.n == st_cnt[p];
     }
   }
   __syncthreads();

@@ -140,6 +140,43 @@ def test_determinism(gpu):
         assert np.array_equal(a[k], b[k]), k
 
 
+def test_large_batch_determinism(gpu, port):
+    """Many CTAs per SM over several waves (stale shared memory from earlier
+    CTAs, every SM busy): device-resident runs repeat bit-for-bit, the chunked
+    host path agrees with them, and sampled pairs match the oracle."""
+    import torch
+
+    P = gpu
+    n, w, h = 96, 320, 240
+    left, right = P.synth_batch(0, n, seed0=40, width=w, height=h)
+    cfg = P.PipelineConfig.baseline(0)
+    dev = torch.device("cuda", 0)
+    dl, dr = torch.from_numpy(left).to(dev), torch.from_numpy(right).to(dev)
+    with P.Matcher(cfg, w, h, n) as m:
+        runs = []
+        for _ in range(2):
+            d = torch.empty((n, h, w), dtype=torch.float32, device=dev)
+            m.run_device_u8(n, w, h, 1, dl.data_ptr(), dr.data_ptr(), {"disparity": d.data_ptr()},
+                            invalid_value=float("nan"))
+            torch.cuda.synchronize()
+            runs.append(d.cpu().numpy())
+        hd = np.empty((n, h, w), np.float32)
+        m.run_host_u8(n, w, h, 1, left.ctypes.data, right.ctypes.data,
+                      {"disparity": hd.ctypes.data}, invalid_value=float("nan"))
+        torch.cuda.synchronize()
+    for other in (runs[1], hd):
+        assert np.array_equal(np.isnan(runs[0]), np.isnan(other))
+        assert np.array_equal(np.nan_to_num(runs[0]), np.nan_to_num(other))
+    for k in (0, n - 1):
+        lf, lv = port.to_grayscale(left[k])
+        rf, rv = port.to_grayscale(right[k])
+        pipe, _ = run_oracle(port, lf, rf, cfg, 1.0, 1.0, lv, rv)
+        ov = np.asarray(pipe["disparity_valid"]).astype(bool)
+        assert np.array_equal(~np.isnan(runs[0][k]), ov)
+        od = np.asarray(pipe["disparity"]).astype(np.float32)
+        assert np.array_equal(runs[0][k][ov], od[ov])
+
+
 def test_errors(gpu):
     P = gpu
     with pytest.raises(P.ConfigError):
