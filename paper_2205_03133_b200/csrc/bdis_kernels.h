@@ -47,12 +47,14 @@ struct BandLayout {
   size_t oR, oL, oG, oLQ, oRQ;
   size_t oMean, oHess, oTmsq, oU, oWres;
   size_t oCnt, oPool, oWlist, oCounters;
+  size_t oSlotU, oSlotPrev, oSlotLastd, oSlotP, oSlotIt;
   size_t oStage, oWok;
   size_t total;
 };
 
 __host__ __device__ inline BandLayout band_layout(int rows, int rpitch, int fpitch, int bpitch,
-                                                  int npb, int nwin, bool valid, bool r64) {
+                                                  int npb, int nwin, bool valid, bool r64,
+                                                  int nslots) {
   BandLayout l;
   size_t o = 0;
   auto take = [&](size_t bytes, size_t align) {
@@ -74,7 +76,12 @@ __host__ __device__ inline BandLayout band_layout(int rows, int rpitch, int fpit
   l.oCnt = take(size_t(npb) * 4, 4);
   l.oPool = take(size_t(npb) * 4, 4);
   l.oWlist = take(size_t(npb) * 4, 4);
-  l.oCounters = take(4 * 4, 4);
+  l.oCounters = take(24 * 4, 4);
+  l.oSlotU = take(size_t(nslots) * 8, 8);
+  l.oSlotPrev = take(size_t(nslots) * 8, 8);
+  l.oSlotLastd = take(size_t(nslots) * 8, 8);
+  l.oSlotP = take(size_t(nslots) * 4, 4);
+  l.oSlotIt = take(size_t(nslots) * 4, 4);
   l.oStage = take(size_t(npb), 1);
   l.oWok = take(size_t(npb) * nwin, 1);
   l.total = (o + 15) / 16 * 16;

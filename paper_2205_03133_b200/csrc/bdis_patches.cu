@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
 
   // ---- shared-memory carve-up (mirrors band_layout on the host)
   const BandLayout lay = band_layout(bp.use_smem ? bp.smem_rows : 0, bp.rpitch, bp.fpitch,
-                                     bp.bpitch, bp.npb, nwin, kValid, kR64);
+                                     bp.bpitch, bp.npb, nwin, kValid, kR64, bp.threads);
   using RT = typename Rows<kSmem, kR64>::RT;
   RT* sR = (RT*)(smem + lay.oR);
   const int rpad = kSmem ? bp.rpad : 0;
@@ -259,7 +259,12 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
   int* st_cnt = (int*)(smem + lay.oCnt);
   int* pool = (int*)(smem + lay.oPool);
   int* wlist = (int*)(smem + lay.oWlist);
-  int* counters = (int*)(smem + lay.oCounters);  // pool size, next to take, converged
+  int* counters = (int*)(smem + lay.oCounters);
+  double* sl_u = (double*)(smem + lay.oSlotU);
+  double* sl_prev = (double*)(smem + lay.oSlotPrev);
+  double* sl_lastd = (double*)(smem + lay.oSlotLastd);
+  int* sl_p = (int*)(smem + lay.oSlotP);
+  int* sl_it = (int*)(smem + lay.oSlotIt);
   uint8_t* st_stage = smem + lay.oStage;
   uint8_t* st_wok = smem + lay.oWok;
 
@@ -315,7 +320,7 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
     rw.bp = w;
     rofs = 0;
   }
-  if (tid < 3) counters[tid] = 0;
+  if (tid < 24) counters[tid] = 0;
   __syncthreads();
 
   // ---- phase 1: extract_patch + precompute_patch_system + u0 (:250-262)
@@ -372,90 +377,139 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
       st_u[p] = u;
       st_cnt[p] = count;
       const double xc = __dsub_rn(cx, u);  // in_bounds(cx - u0, cy), lk_solver.cpp:89
-      if (xc >= 0.0 && xc <= (double)(w - 1)) pool[atomicAdd(&counters[0], 1)] = p;
+      if (xc >= 0.0 && xc <= (double)(w - 1)) pool[atomicAdd(&counters[0], 1)] = p;  // cNPool
     }
     st_stage[p] = stage;
   }
   __syncthreads();
 
-  // ---- phase 2a: persistent lanes run the LK solves (one residual evaluation
-  // per loop trip) and take the next patch from the pool when one ends
+  // ---- phase 2: rounds of one residual evaluation per busy lane. Slots
+  // [0, n_act) hold the running LK solves (src/lk_solver.cpp:83-132), packed to
+  // the lowest lanes after every round and refilled from the pool; the next
+  // lanes take window samples (src/window_posterior.cpp:10-36) of patches that
+  // converged in earlier rounds. Idle warps go straight to the barrier, so a
+  // long solve keeps one warp busy, not a quarter of every warp.
+  enum { cNPool, cConv, cNAct, cPoolNext = 4, cWNext = 6, cWAvail = 8, cAlive = 10 };
   {
-    const int n_pool = counters[0];
-    auto take = [&]() {
-      const int q = atomicAdd(&counters[1], 1);
-      return q < n_pool ? pool[q] : -1;
-    };
-    int p = take();
-    int it = 0, x0 = 0, r0 = 0;
-    double u = 0.0, prev = CUDART_INF, lastd = 0.0, mean = 0.0;
-    auto start = [&](int np) {
-      p = np;
-      if (p < 0) return;
-      x0 = col_start(p % g.nx);
-      r0 = row_start(ky0 + p / g.nx) - rofs;
-      u = st_u[p];
-      mean = st_mean[p];
-      it = 0;
-      prev = CUDART_INF;
-      lastd = 0.0;
-    };
-    start(p);
-    while (p >= 0) {
-      const Ev ev = eval_patch<S, kSmem, kValid, kR64>(rw, w, s, x0, r0, rpad, mean, u);
-      // one iteration of solve_patch_disparity (src/lk_solver.cpp:96-127)
-      ++it;
-      bool done = false, conv = false;
-      if (ev.n == 0) {
-        done = true;
-      } else {
-        const double r = ev.msq;
-        if (it >= pp.min_it) {
-          if (r < pp.stop_good) {
-            conv = done = true;
-          } else if (r > __dmul_rn(pp.stop_bad, st_tmsq[p])) {
+    const int n_pool = counters[cNPool];
+    const int n0 = min(n_pool, nt);
+    if (tid < n0) {
+      const int p = pool[tid];
+      sl_p[tid] = p;
+      sl_it[tid] = 0;
+      sl_u[tid] = st_u[p];
+      sl_prev[tid] = CUDART_INF;
+      sl_lastd[tid] = 0.0;
+    }
+    if (tid == 0) {
+      counters[cNAct] = n0;
+      counters[cPoolNext] = n0;
+      counters[cWNext] = 0;
+      counters[cWAvail] = 0;
+    }
+    __syncthreads();
+    const int warp = tid >> 5, lane = tid & 31;
+#pragma unroll 1
+    for (int par = 0;; par ^= 1) {
+      const int na = counters[cNAct + par], pn = counters[cPoolNext + par];
+      const int wn = counters[cWNext + par], wa = counters[cWAvail + par] * nwin;
+      const int wjobs = min(nt - na, wa - wn);
+      if (na == 0 && wjobs == 0) break;
+      bool alive = false;
+      int p = 0, it = 0, k = -1;
+      double u = 0.0, prev = 0.0, lastd = 0.0, ue = 0.0;
+      const bool lk = tid < na, busy = tid < na + wjobs;
+      if (lk) {
+        p = sl_p[tid];
+        it = sl_it[tid];
+        u = sl_u[tid];
+        prev = sl_prev[tid];
+        lastd = sl_lastd[tid];
+        ue = u;
+      } else if (busy) {
+        const int j = wn + tid - na;
+        p = wlist[j / nwin];
+        k = j - (j / nwin) * nwin;
+        ue = __dadd_rn(st_u[p], pp.woff[k]);
+      }
+      if (busy) {
+        // one code path for both kinds of job: a warp costs one evaluation
+        const Ev ev = eval_patch<S, kSmem, kValid, kR64>(
+            rw, w, s, col_start(p % g.nx), row_start(ky0 + p / g.nx) - rofs, rpad, st_mean[p], ue);
+        if (!lk) {
+          // sample_window: valid iff every template pixel was sampled (:31-36)
+          st_wres[p * nwin + k] = ev.msq;
+          st_wok[p * nwin + k] = ev.n == st_cnt[p];
+        } else {
+          // one iteration of solve_patch_disparity (src/lk_solver.cpp:96-127)
+          ++it;
+          bool done = false, conv = false;
+          if (ev.n == 0) {
             done = true;
-          } else if (isfinite(prev) && __dsub_rn(prev, r) < __dmul_rn(pp.stop_improve, prev)) {
-            conv = it > 1 && fabs(lastd) < 1e-2;
-            done = true;
+          } else {
+            const double r = ev.msq;
+            if (it >= pp.min_it) {
+              if (r < pp.stop_good) {
+                conv = done = true;
+              } else if (r > __dmul_rn(pp.stop_bad, st_tmsq[p])) {
+                done = true;
+              } else if (isfinite(prev) && __dsub_rn(prev, r) < __dmul_rn(pp.stop_improve, prev)) {
+                conv = it > 1 && fabs(lastd) < 1e-2;
+                done = true;
+              }
+            }
+            if (!done) {
+              const double delta = __ddiv_rn(ev.jr, st_hess[p]);
+              u = __dadd_rn(u, delta);
+              lastd = delta;
+              prev = r;
+              if (fabs(delta) < 1e-2) conv = done = true;  // kUpdateEpsilon
+              else if (it >= pp.max_it) done = true;
+            }
           }
-        }
-        if (!done) {
-          const double delta = __ddiv_rn(ev.jr, st_hess[p]);
-          u = __dadd_rn(u, delta);
-          lastd = delta;
-          prev = r;
-          if (fabs(delta) < 1e-2) conv = done = true;  // kUpdateEpsilon
-          else if (it >= pp.max_it) done = true;
+          if (done && conv) {
+            st_stage[p] = kConverged;
+            st_u[p] = u;
+            wlist[atomicAdd(&counters[cConv], 1)] = p;
+          }
+          alive = !done;
         }
       }
-      if (done) {
-        if (conv) {
-          st_stage[p] = kConverged;
-          st_u[p] = u;
-          wlist[atomicAdd(&counters[2], 1)] = p;
-        }
-        start(take());
+      const unsigned bal = __ballot_sync(0xffffffffu, alive);
+      if (lane == 0) counters[cAlive + warp] = __popc(bal);
+      __syncthreads();
+      int before = 0, n_alive = 0;
+      for (int q = 0; q < (nt >> 5); ++q) {
+        const int c = counters[cAlive + q];
+        before += q < warp ? c : 0;
+        n_alive += c;
       }
+      if (alive) {
+        const int d = before + __popc(bal & ((1u << lane) - 1u));
+        sl_p[d] = p;
+        sl_it[d] = it;
+        sl_u[d] = u;
+        sl_prev[d] = prev;
+        sl_lastd[d] = lastd;
+      }
+      const int refill = min(nt - n_alive, n_pool - pn);
+      if (tid >= n_alive && tid < n_alive + refill) {
+        const int np = pool[pn + tid - n_alive];
+        sl_p[tid] = np;
+        sl_it[tid] = 0;
+        sl_u[tid] = st_u[np];
+        sl_prev[tid] = CUDART_INF;
+        sl_lastd[tid] = 0.0;
+      }
+      if (tid == 0) {
+        counters[cNAct + (par ^ 1)] = n_alive + refill;
+        counters[cPoolNext + (par ^ 1)] = pn + refill;
+        counters[cWNext + (par ^ 1)] = wn + wjobs;
+        counters[cWAvail + (par ^ 1)] = counters[cConv];
+      }
+      __syncthreads();
     }
   }
-  __syncthreads();
-
-  // ---- phase 2b: the window samples of every converged patch (:31-36), one
-  // evaluation per job, dealt round-robin over all lanes (no tail)
-  {
-    const int jobs = counters[2] * nwin;
-    for (int j = tid; j < jobs; j += nt) {
-      const int p = wlist[j / nwin], k = j - (j / nwin) * nwin;
-      const Ev ev = eval_patch<S, kSmem, kValid, kR64, false>(
-          rw, w, s, col_start(p % g.nx), row_start(ky0 + p / g.nx) - rofs, rpad, st_mean[p],
-          __dadd_rn(st_u[p], pp.woff[k]));
-      // sample_window: valid iff every template pixel was sampled
-      st_wres[p * nwin + k] = ev.msq;
-      st_wok[p * nwin + k] = ev.n == st_cnt[p];
-    }
-  }
-  __syncthreads();
 
   // ---- phase 3: posterior, propagation, variance and the records (:268-299)
   const long long rec0 = pair * (long long)g.nx * g.ny + (long long)ky0 * g.nx;
@@ -556,14 +610,14 @@ BandPlan plan_bands(const Level& L, const PatchParams& pp, int max_smem_per_cta)
   bp.rpitch = (bp.r64 ? pad8_host(L.w + 2 * bp.rpad) : pad4_host(L.w + 2 * bp.rpad)) + 1;
   bp.fpitch = (L.w - 1 + ((L.w - 1) >> 5)) + 1;  // slots for x in [0, w-1]
   bp.bpitch = valid ? L.w : 0;
+  const int threads = env("PSTEREO_TUNE_THREADS", 128);
   auto bytes_for = [&](int rb) {
     const int rows = (rb - 1) * g.stride + g.size;
     return band_layout(rows, bp.rpitch, bp.fpitch, bp.bpitch, rb * g.nx, pp.nwin, valid,
-                       bp.r64).total;
+                       bp.r64, threads).total;
   };
   // ~1.5 patches per lane of a 128-thread CTA, while `ctas` CTAs fit an SM
   // (PSTEREO_TUNE_THREADS / _PPL10 / _CTAS override, for tuning runs only)
-  const int threads = env("PSTEREO_TUNE_THREADS", 128);
   const int ppl10 = env("PSTEREO_TUNE_PPL10", 15);
   const int ctas = env("PSTEREO_TUNE_CTAS", 2);
   const size_t per_sm = size_t(max_smem_per_cta) / ctas - 1024;
@@ -576,7 +630,7 @@ BandPlan plan_bands(const Level& L, const PatchParams& pp, int max_smem_per_cta)
   bp.smem_rows = (rb - 1) * g.stride + g.size;
   bp.smem_bytes = bp.use_smem ? bytes_for(rb)
                               : band_layout(0, bp.rpitch, bp.fpitch, bp.bpitch, bp.npb, pp.nwin,
-                                            valid, bp.r64).total;
+                                            valid, bp.r64, threads).total;
   bp.threads = std::min(threads, std::max(32, ((bp.npb + 31) / 32) * 32));
   return bp;
 }
