@@ -655,6 +655,100 @@ __global__ void k_output(OutputArgs a) {
   }
 }
 
+// The same per-pixel rule for the common layout -- 2x2 blocks (finest_exp 1),
+// W = 2 fw, H = 2 fh, fw % 4 == 0, 16-byte aligned planes: one thread per
+// four finest pixels, vector loads of the finest fields and 16-byte streaming
+// stores of the two 8-pixel output rows.
+template <typename T>
+__device__ __forceinline__ void put_row8(void* base, long long o, T v0, T v1, T v2, T v3) {
+  T* p = (T*)base + o;
+  if constexpr (sizeof(T) == 4) {
+    __stcs((float4*)p, make_float4(v0, v0, v1, v1));
+    __stcs((float4*)p + 1, make_float4(v2, v2, v3, v3));
+  } else {
+    __stcs((double2*)p, make_double2(v0, v0));
+    __stcs((double2*)p + 1, make_double2(v1, v1));
+    __stcs((double2*)p + 2, make_double2(v2, v2));
+    __stcs((double2*)p + 3, make_double2(v3, v3));
+  }
+}
+
+__device__ __forceinline__ void put_row8_u8(uint8_t* base, long long o, unsigned m4) {
+  // m4: one bit per finest pixel -> 8 bytes of 0/1
+  const unsigned lo = (m4 & 1u) * 0x0101u | ((m4 >> 1) & 1u) * 0x01010000u;
+  const unsigned hi = ((m4 >> 2) & 1u) * 0x0101u | ((m4 >> 3) & 1u) * 0x01010000u;
+  __stcs((uint2*)(base + o), make_uint2(lo, hi));
+}
+
+template <typename T>
+__device__ __forceinline__ void load4(const void* base, long long f, T* v) {
+  if constexpr (sizeof(T) == 4) {
+    const float4 q = *(const float4*)((const float*)base + f);
+    v[0] = q.x, v[1] = q.y, v[2] = q.z, v[3] = q.w;
+  } else {
+    const double2 q0 = *(const double2*)((const double*)base + f);
+    const double2 q1 = *((const double2*)((const double*)base + f) + 1);
+    v[0] = q0.x, v[1] = q0.y, v[2] = q1.x, v[3] = q1.y;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_output_x4(OutputArgs a) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  const int qw = a.fw >> 2;
+  if (q >= qw * a.fh) return;
+  const long long pair = blockIdx.y;
+  const int fy = q / qw, fx = (q - fy * qw) << 2;
+  const long long f = pair * a.fplane + (long long)fy * a.fw + fx;
+  const uchar4 fl = *(const uchar4*)(a.fb.flags + f);
+  const uint8_t fls[4] = {fl.x, fl.y, fl.z, fl.w};
+  unsigned keep = 0, mv = 0, dv = 0;
+  const int* lab = a.label + pair * a.fplane;
+  const int* area = a.area + pair * a.fplane;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    mv |= (unsigned)((fls[k] & kFlagMatch) != 0) << k;
+    if (fls[k] & kFlagKeep) {  // local root -> global root -> component area
+      const bool kp = area[lab[lab[fy * a.fw + fx + k]]] >= a.min_px;
+      keep |= (unsigned)kp << k;
+      dv |= (unsigned)(kp && (fls[k] & kFlagDepth)) << k;
+    }
+  }
+  T d[4] = {0, 0, 0, 0}, p[4] = {0, 0, 0, 0}, z[4] = {0, 0, 0, 0}, v[4] = {0, 0, 0, 0},
+    sg[4] = {0, 0, 0, 0}, md[4];
+  if (a.fb.disp) load4<T>(a.fb.disp, f, d);
+  if (a.fb.prob) load4<T>(a.fb.prob, f, p);
+  if (a.fb.depth) load4<T>(a.fb.depth, f, z);
+  if (a.fb.var) load4<T>(a.fb.var, f, v);
+  if (a.fb.sigma) load4<T>(a.fb.sigma, f, sg);
+  const T iv = (T)a.invalid_value;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    md[k] = d[k];  // MatchResult::disparity keeps its value
+    const bool kk = (keep >> k) & 1u, dd = (dv >> k) & 1u;
+    if (!dd) z[k] = 0, sg[k] = 0;
+    if (a.fill_invalid) {
+      if (!kk) d[k] = iv;
+      if (!dd) z[k] = iv, sg[k] = iv;
+    }
+  }
+  const long long pbase = pair * (long long)a.W * a.H;
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const long long o = pbase + (long long)(2 * fy + r) * a.W + 2 * fx;
+    if (a.out_disp) put_row8<T>(a.out_disp, o, d[0], d[1], d[2], d[3]);
+    if (a.out_dvalid) put_row8_u8(a.out_dvalid, o, keep);
+    if (a.out_prob) put_row8<T>(a.out_prob, o, p[0], p[1], p[2], p[3]);
+    if (a.out_mdisp) put_row8<T>(a.out_mdisp, o, md[0], md[1], md[2], md[3]);
+    if (a.out_mvalid) put_row8_u8(a.out_mvalid, o, mv);
+    if (a.out_depth) put_row8<T>(a.out_depth, o, z[0], z[1], z[2], z[3]);
+    if (a.out_depth_valid) put_row8_u8(a.out_depth_valid, o, dv);
+    if (a.out_var) put_row8<T>(a.out_var, o, v[0], v[1], v[2], v[3]);
+    if (a.out_sigma) put_row8<T>(a.out_sigma, o, sg[0], sg[1], sg[2], sg[3]);
+    if (a.out_sigma_valid) put_row8_u8(a.out_sigma_valid, o, dv);
+  }
+}
+
 // MatchStats per pair and level (src/coarse_to_fine.cpp:302-314).
 __global__ void k_stats(StatsArgs a) {
   const int pair = blockIdx.x, lvl = blockIdx.y;
@@ -739,7 +833,26 @@ void launch_fuse_ccl(const Level& L, const FinestBufs& fb, const double* mask, i
 int ccl_tiles(int w, int h) { return ((w + kTileW - 1) / kTileW) * ((h + kTileH - 1) / kTileH); }
 int ccl_tile_px() { return kTilePx; }
 
+static bool aligned(const void* p, size_t n) { return ((uintptr_t)p % n) == 0; }
+
 void launch_output(const OutputArgs& a, int f64, int n_pairs, cudaStream_t s) {
+  const size_t vt = 16;  // float4 / double2
+  bool x4 = a.e == 1 && a.W == 2 * a.fw && a.H == 2 * a.fh && a.fw % 4 == 0 &&
+            a.fplane % 4 == 0;
+  for (const void* p : {(const void*)a.out_disp, (const void*)a.out_prob, (const void*)a.out_mdisp,
+                        (const void*)a.out_depth, (const void*)a.out_var, (const void*)a.out_sigma,
+                        (const void*)a.fb.disp, (const void*)a.fb.prob, (const void*)a.fb.depth,
+                        (const void*)a.fb.var, (const void*)a.fb.sigma})
+    x4 = x4 && aligned(p, vt);
+  for (const void* p : {(const void*)a.out_dvalid, (const void*)a.out_mvalid,
+                        (const void*)a.out_depth_valid, (const void*)a.out_sigma_valid})
+    x4 = x4 && aligned(p, 8);
+  if (x4) {
+    dim3 grid(blocks_for((long long)(a.fw / 4) * a.fh, 256), n_pairs);
+    if (f64) k_output_x4<double><<<grid, 256, 0, s>>>(a);
+    else k_output_x4<float><<<grid, 256, 0, s>>>(a);
+    return;
+  }
   dim3 grid(blocks_for((long long)a.fw * a.fh, 256), n_pairs);
   if (f64) k_output<double><<<grid, 256, 0, s>>>(a);
   else k_output<float><<<grid, 256, 0, s>>>(a);

@@ -610,15 +610,16 @@ BandPlan plan_bands(const Level& L, const PatchParams& pp, int max_smem_per_cta)
   bp.rpitch = (bp.r64 ? pad8_host(L.w + 2 * bp.rpad) : pad4_host(L.w + 2 * bp.rpad)) + 1;
   bp.fpitch = (L.w - 1 + ((L.w - 1) >> 5)) + 1;  // slots for x in [0, w-1]
   bp.bpitch = valid ? L.w : 0;
-  const int threads = env("PSTEREO_TUNE_THREADS", 128);
+  const int threads = env("PSTEREO_TUNE_THREADS", 192);
   auto bytes_for = [&](int rb) {
     const int rows = (rb - 1) * g.stride + g.size;
     return band_layout(rows, bp.rpitch, bp.fpitch, bp.bpitch, rb * g.nx, pp.nwin, valid,
                        bp.r64, threads).total;
   };
-  // ~1.5 patches per lane of a 128-thread CTA, while `ctas` CTAs fit an SM
-  // (PSTEREO_TUNE_THREADS / _PPL10 / _CTAS override, for tuning runs only)
-  const int ppl10 = env("PSTEREO_TUNE_PPL10", 15);
+  // up to ~2 patches per slot of a 192-thread CTA, while two CTAs fit an SM
+  // (measured best of a T x ppl x CTAs sweep at the bench workload;
+  // PSTEREO_TUNE_THREADS / _PPL10 / _CTAS override, for tuning runs only)
+  const int ppl10 = env("PSTEREO_TUNE_PPL10", 20);
   const int ctas = env("PSTEREO_TUNE_CTAS", 2);
   const size_t per_sm = size_t(max_smem_per_cta) / ctas - 1024;
   int rb = std::max(1, std::min(g.ny, (ppl10 * threads / 10 + g.nx / 2) / g.nx));
