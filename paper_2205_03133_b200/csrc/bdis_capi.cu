@@ -141,6 +141,53 @@ struct LevelBufs {
   DevBuf<uint8_t> lvalid, rvalid, lq, rq, stage;
   DevBuf<float> rpad;
   DevBuf<double> u, prob, post, sigma;
+  void release() {
+    left.release();
+    right.release();
+    grad.release();
+    lvalid.release();
+    rvalid.release();
+    lq.release();
+    rq.release();
+    stage.release();
+    rpad.release();
+    u.release();
+    prob.release();
+    post.release();
+    sigma.release();
+  }
+};
+
+// Per-stream working set of one device-resident run (pyramid levels, patch
+// records, finest fields, component labels). The host-buffer pipeline keeps
+// two, so consecutive chunks run on two streams and overlap each other's
+// launch latency and tails.
+struct Scratch {
+  std::vector<LevelBufs> levels;  // index e (0 unused unless finest_exp == 0)
+  DevBuf<float> gray[2];          // full-resolution gray (masked u8 inputs)
+  DevBuf<uint8_t> gray_valid[2];
+  DevBuf<double> fdisp, fprob, fdepth, fvar, fsigma;  // sized as doubles, typed per call
+  DevBuf<uint8_t> fflags;
+  DevBuf<int> flabel, farea, froots, fnroots;
+  DevBuf<int> stats;
+  void release() {
+    for (auto& L : levels) L.release();
+    for (int v = 0; v < 2; ++v) {
+      gray[v].release();
+      gray_valid[v].release();
+    }
+    fdisp.release();
+    fprob.release();
+    fdepth.release();
+    fvar.release();
+    fsigma.release();
+    fflags.release();
+    flabel.release();
+    farea.release();
+    froots.release();
+    fnroots.release();
+    stats.release();
+  }
 };
 
 }  // namespace
@@ -173,17 +220,12 @@ struct pstereo_ctx {
   DevBuf<uint8_t> in_u8[2];
   DevBuf<float> full[2];
   DevBuf<uint8_t> full_valid[2];
-  std::vector<LevelBufs> levels;  // index e (0 unused unless finest_exp == 0)
-  // finest fields
-  DevBuf<double> fdisp, fprob, fdepth, fvar, fsigma;  // sized as doubles, typed per call
-  DevBuf<uint8_t> fflags;
-  DevBuf<int> flabel, farea, froots, fnroots;
-  DevBuf<int> stats;
+  Scratch scr[2];  // [0]: the call's stream, [1]: the pipeline's second compute stream
   // staging for host outputs
   DevBuf<uint8_t> out_stage[10];
   // host-buffer pipeline (chunked H2D / compute / D2H)
   int chunk_pairs = 0;
-  cudaStream_t s_in = nullptr, s_out = nullptr;
+  cudaStream_t s_in = nullptr, s_out = nullptr, s_comp = nullptr;
   std::vector<cudaEvent_t> chunk_events;
 };
 
@@ -355,7 +397,7 @@ int pstereo_gpu_create(int device, const pstereo_params* p, int max_width, int m
     pstereo_gpu_destroy(ctx);
     return PSTEREO_EINTERNAL;
   }
-  ctx->levels.resize(size_t(p->coarsest_exp) + 1);
+  for (auto& sc : ctx->scr) sc.levels.resize(size_t(p->coarsest_exp) + 1);
   if (const char* v = getenv("PSTEREO_CHUNK_PAIRS")) ctx->chunk_pairs = atoi(v);
   *out = ctx;
   return PSTEREO_OK;
@@ -369,36 +411,12 @@ void pstereo_gpu_destroy(pstereo_ctx* ctx) {
   for (auto& b : ctx->in_u8) b.release();
   for (auto& b : ctx->full) b.release();
   for (auto& b : ctx->full_valid) b.release();
-  for (auto& L : ctx->levels) {
-    L.left.release();
-    L.right.release();
-    L.grad.release();
-    L.lvalid.release();
-    L.rvalid.release();
-    L.lq.release();
-    L.rq.release();
-    L.stage.release();
-    L.rpad.release();
-    L.u.release();
-    L.prob.release();
-    L.post.release();
-    L.sigma.release();
-  }
-  ctx->fdisp.release();
-  ctx->fprob.release();
-  ctx->fdepth.release();
-  ctx->fvar.release();
-  ctx->fsigma.release();
-  ctx->fflags.release();
-  ctx->flabel.release();
-  ctx->farea.release();
-  ctx->froots.release();
-  ctx->fnroots.release();
-  ctx->stats.release();
+  for (auto& sc : ctx->scr) sc.release();
   for (auto& b : ctx->out_stage) b.release();
   for (auto e : ctx->chunk_events) cudaEventDestroy(e);
   if (ctx->s_in) cudaStreamDestroy(ctx->s_in);
   if (ctx->s_out) cudaStreamDestroy(ctx->s_out);
+  if (ctx->s_comp) cudaStreamDestroy(ctx->s_comp);
   for (auto* pool : {&ctx->ev_pending, &ctx->ev_free})
     for (auto& set : *pool)
       for (auto ev : set.ev) cudaEventDestroy(ev);
@@ -473,8 +491,8 @@ struct HostCopies {
   double* fsg = nullptr;
 };
 
-int run_device(pstereo_ctx* ctx, const std::vector<LevelGeom>& geo, int n, int W, int H,
-               int channels, const uint8_t* const src_u8_in[2], long long f32_offset,
+int run_device(pstereo_ctx* ctx, Scratch& sc, const std::vector<LevelGeom>& geo, int n, int W,
+               int H, int channels, const uint8_t* const src_u8_in[2], long long f32_offset,
                bool have_f32_valid, double focal, double baseline, int f64, int fill_invalid,
                double invalid_value, void* const dev_ptr[10], const HostCopies& hc,
                cudaStream_t s) {
@@ -545,8 +563,8 @@ int run_device(pstereo_ctx* ctx, const std::vector<LevelGeom>& geo, int n, int W
     for (int v = 0; v < 2; ++v) CK(cudaMemsetAsync((void*)fval[v], 1, size_t(npx), s));
   if (left_u8 && !fused) {
     for (int v = 0; v < 2; ++v) {
-      CK(ctx->full[v].ensure(size_t(npx)));
-      CK(ctx->full_valid[v].ensure(size_t(npx)));
+      CK(sc.gray[v].ensure(size_t(npx)));
+      CK(sc.gray_valid[v].ensure(size_t(npx)));
     }
   }
   CK(mark());
@@ -555,7 +573,7 @@ int run_device(pstereo_ctx* ctx, const std::vector<LevelGeom>& geo, int n, int W
   std::vector<Level> lv(geo.size());
   for (size_t li = 0; li < geo.size(); ++li) {
     const LevelGeom& G = geo[li];
-    LevelBufs& B = ctx->levels[G.e];
+    LevelBufs& B = sc.levels[G.e];
     Level& L = lv[li];
     std::memset(&L, 0, sizeof L);
     L.e = G.e;
@@ -566,10 +584,10 @@ int run_device(pstereo_ctx* ctx, const std::vector<LevelGeom>& geo, int n, int W
     CK(B.grad.ensure(np));
     CK(B.rpad.ensure(size_t(G.w + 1) * G.h * n));
     if (G.e == 0 && !fused) {
-      L.left = left_u8 ? ctx->full[0].p : fsrc[0];
-      L.right = left_u8 ? ctx->full[1].p : fsrc[1];
-      L.lvalid = left_u8 ? ctx->full_valid[0].p : fval[0];
-      L.rvalid = left_u8 ? ctx->full_valid[1].p : fval[1];
+      L.left = left_u8 ? sc.gray[0].p : fsrc[0];
+      L.right = left_u8 ? sc.gray[1].p : fsrc[1];
+      L.lvalid = left_u8 ? sc.gray_valid[0].p : fval[0];
+      L.rvalid = left_u8 ? sc.gray_valid[1].p : fval[1];
     } else {
       CK(B.left.ensure(np));
       L.left = B.left.p;
@@ -610,23 +628,23 @@ int run_device(pstereo_ctx* ctx, const std::vector<LevelGeom>& geo, int n, int W
     // general path (masked inputs): grayscale, cascade, then the tables
     if (left_u8) {
       for (int v = 0; v < 2; ++v) {
-        launch_gray_u8(src_u8[v], channels, npx, ctx->full[v].p, ctx->full_valid[v].p, s);
+        launch_gray_u8(src_u8[v], channels, npx, sc.gray[v].p, sc.gray_valid[v].p, s);
         ++ctx->launches;
       }
     }
     for (int e = 1; e <= ce; ++e) {
-      LevelBufs& B = ctx->levels[e];
+      LevelBufs& B = sc.levels[e];
       const size_t np = size_t(ws[e]) * hs[e] * n;
       CK(B.left.ensure(np));
       CK(B.right.ensure(np));
       CK(B.lvalid.ensure(np));
       CK(B.rvalid.ensure(np));
-      const float* sl = e == 1 ? (left_u8 ? ctx->full[0].p : fsrc[0]) : ctx->levels[e - 1].left.p;
-      const float* sr = e == 1 ? (left_u8 ? ctx->full[1].p : fsrc[1]) : ctx->levels[e - 1].right.p;
+      const float* sl = e == 1 ? (left_u8 ? sc.gray[0].p : fsrc[0]) : sc.levels[e - 1].left.p;
+      const float* sr = e == 1 ? (left_u8 ? sc.gray[1].p : fsrc[1]) : sc.levels[e - 1].right.p;
       const uint8_t* slv =
-          e == 1 ? (left_u8 ? ctx->full_valid[0].p : fval[0]) : ctx->levels[e - 1].lvalid.p;
+          e == 1 ? (left_u8 ? sc.gray_valid[0].p : fval[0]) : sc.levels[e - 1].lvalid.p;
       const uint8_t* srv =
-          e == 1 ? (left_u8 ? ctx->full_valid[1].p : fval[1]) : ctx->levels[e - 1].rvalid.p;
+          e == 1 ? (left_u8 ? sc.gray_valid[1].p : fval[1]) : sc.levels[e - 1].rvalid.p;
       launch_downsample(sl, slv, sr, srv, ws[e - 1], hs[e - 1], B.left.p, B.lvalid.p, B.right.p,
                         B.rvalid.p, ws[e], hs[e], n, s);
       ++ctx->launches;
@@ -634,7 +652,7 @@ int run_device(pstereo_ctx* ctx, const std::vector<LevelGeom>& geo, int n, int W
     for (size_t li = 0; li < geo.size(); ++li) {
       Level& L = lv[li];
       if (L.e != 0) {
-        LevelBufs& B = ctx->levels[L.e];
+        LevelBufs& B = sc.levels[L.e];
         L.left = B.left.p;
         L.right = B.right.p;
         L.lvalid = B.lvalid.p;
@@ -686,33 +704,33 @@ int run_device(pstereo_ctx* ctx, const std::vector<LevelGeom>& geo, int n, int W
   const bool need_depth = dev_ptr[3] != nullptr;
   const bool need_sigma = dev_ptr[5] != nullptr;
   const bool need_var = dev_ptr[9] != nullptr;
-  if (need_disp) CK(ctx->fdisp.ensure(fnp));
-  if (need_prob) CK(ctx->fprob.ensure(fnp));
-  if (need_depth) CK(ctx->fdepth.ensure(fnp));
-  if (need_var) CK(ctx->fvar.ensure(fnp));
-  if (need_sigma) CK(ctx->fsigma.ensure(fnp));
-  CK(ctx->fflags.ensure(fnp));
-  CK(ctx->flabel.ensure(fnp));
-  CK(ctx->farea.ensure(fnp));
+  if (need_disp) CK(sc.fdisp.ensure(fnp));
+  if (need_prob) CK(sc.fprob.ensure(fnp));
+  if (need_depth) CK(sc.fdepth.ensure(fnp));
+  if (need_var) CK(sc.fvar.ensure(fnp));
+  if (need_sigma) CK(sc.fsigma.ensure(fnp));
+  CK(sc.fflags.ensure(fnp));
+  CK(sc.flabel.ensure(fnp));
+  CK(sc.farea.ensure(fnp));
   const size_t ntiles = size_t(ccl_tiles(F.w, F.h)) * n;
-  CK(ctx->froots.ensure(ntiles * ccl_tile_px()));
-  CK(ctx->fnroots.ensure(ntiles));
+  CK(sc.froots.ensure(ntiles * ccl_tile_px()));
+  CK(sc.fnroots.ensure(ntiles));
   FinestBufs fb;
-  fb.disp = need_disp ? (void*)ctx->fdisp.p : nullptr;
-  fb.prob = need_prob ? (void*)ctx->fprob.p : nullptr;
-  fb.depth = need_depth ? (void*)ctx->fdepth.p : nullptr;
-  fb.var = need_var ? (void*)ctx->fvar.p : nullptr;
-  fb.sigma = need_sigma ? (void*)ctx->fsigma.p : nullptr;
-  fb.flags = ctx->fflags.p;
+  fb.disp = need_disp ? (void*)sc.fdisp.p : nullptr;
+  fb.prob = need_prob ? (void*)sc.fprob.p : nullptr;
+  fb.depth = need_depth ? (void*)sc.fdepth.p : nullptr;
+  fb.var = need_var ? (void*)sc.fvar.p : nullptr;
+  fb.sigma = need_sigma ? (void*)sc.fsigma.p : nullptr;
+  fb.flags = sc.fflags.p;
   fb.scale_d = fe == 0 ? 1.0 : std::pow(2.0, fe);
   fb.scale_v = fe == 0 ? 1.0 : std::pow(4.0, fe);
   fb.fb = focal * baseline;
   fb.threshold = prm.pixel_threshold;
   CclBufs cb;
-  cb.label = ctx->flabel.p;
-  cb.larea = ctx->farea.p;
-  cb.roots = ctx->froots.p;
-  cb.nroots = ctx->fnroots.p;
+  cb.label = sc.flabel.p;
+  cb.larea = sc.farea.p;
+  cb.roots = sc.froots.p;
+  cb.nroots = sc.fnroots.p;
   cb.full_w = W;
   cb.full_h = H;
   cb.e = fe;
@@ -728,8 +746,8 @@ int run_device(pstereo_ctx* ctx, const std::vector<LevelGeom>& geo, int n, int W
   oa.fh = F.h;
   oa.fplane = F.plane;
   oa.fb = fb;
-  oa.label = ctx->flabel.p;
-  oa.area = ctx->farea.p;
+  oa.label = sc.flabel.p;
+  oa.area = sc.farea.p;
   {
     const long long mp = llround(std::ceil(prm.gamma * double(S) * double(S) - 1e-9));
     oa.min_px = std::max(mp, 1ll);  // src/depth_variance.cpp:87-90
@@ -758,8 +776,8 @@ int run_device(pstereo_ctx* ctx, const std::vector<LevelGeom>& geo, int n, int W
       sa.stage[li] = lv[li].stage;
       sa.np[li] = lv[li].g.nx * lv[li].g.ny;
     }
-    CK(ctx->stats.ensure(size_t(n) * lv.size() * 3));
-    sa.out = ctx->stats.p;
+    CK(sc.stats.ensure(size_t(n) * lv.size() * 3));
+    sa.out = sc.stats.p;
     launch_stats(sa, n, s);
     ++ctx->launches;
   }
@@ -767,7 +785,7 @@ int run_device(pstereo_ctx* ctx, const std::vector<LevelGeom>& geo, int n, int W
   CK(mark());
 
   if (want_stats)
-    CK(cudaMemcpyAsync(hc.stats, ctx->stats.p, size_t(n) * lv.size() * 3 * sizeof(int),
+    CK(cudaMemcpyAsync(hc.stats, sc.stats.p, size_t(n) * lv.size() * 3 * sizeof(int),
                        cudaMemcpyDeviceToHost, s));
   if (hc.fst) {
     const size_t nrec = size_t(F.g.nx) * F.g.ny * n;
@@ -854,18 +872,43 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
   if (pipelined && !ctx->s_in) {
     CK(cudaStreamCreateWithFlags(&ctx->s_in, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&ctx->s_out, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&ctx->s_comp, cudaStreamNonBlocking));
   }
-  const int n_chunks = (n + chunk - 1) / chunk;
-  while ((int)ctx->chunk_events.size() < 2 * n_chunks) {
+  // chunk boundaries: a short ramp (4, 8, 16 pairs) so the first device->host
+  // copy starts early, then `chunk` pairs each; the copy engines, not the
+  // kernels, bound a pipelined call, so its length is fill + total copy time
+  std::vector<int> starts;
+  for (int c0 = 0, ramp = pipelined ? 4 : chunk; c0 < n;) {
+    starts.push_back(c0);
+    const int step = std::min(ramp, chunk);
+    c0 += step;
+    ramp = step * 2;
+  }
+  starts.push_back(n);
+  const int n_chunks = int(starts.size()) - 1;
+  while ((int)ctx->chunk_events.size() < 2 * n_chunks + 3) {
     cudaEvent_t e;
     CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     ctx->chunk_events.push_back(e);
   }
+  cudaEvent_t* ev = ctx->chunk_events.data();
+  cudaEvent_t ev_start = ev[2 * n_chunks], ev_comp = ev[2 * n_chunks + 1],
+              ev_out = ev[2 * n_chunks + 2];
+  if (pipelined) {
+    // the helper streams start behind the work already queued on the caller's stream
+    CK(cudaEventRecord(ev_start, s));
+    for (cudaStream_t t : {ctx->s_in, ctx->s_comp, ctx->s_out}) CK(cudaStreamWaitEvent(t, ev_start, 0));
+  }
+  bool used_comp = false;
   for (int c = 0; c < n_chunks; ++c) {
-    const int c0 = c * chunk, nc = std::min(chunk, n - c0);
+    const int c0 = starts[size_t(c)], nc = starts[size_t(c) + 1] - c0;
     const size_t px0 = size_t(n_full) * c0, pxc = size_t(n_full) * nc;
+    // consecutive chunks alternate between two compute streams / working sets
+    const int slot = pipelined ? (c & 1) : 0;
+    cudaStream_t cs = slot ? ctx->s_comp : s;
+    used_comp = used_comp || slot;
     if (pipelined) {
-      cudaStream_t sc = host_in ? ctx->s_in : s;
+      cudaStream_t sc = host_in ? ctx->s_in : cs;
       if (left_u8) {
         if (host_in)
           for (int v = 0; v < 2; ++v)
@@ -880,9 +923,9 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
           else if (have_f32_valid) CK(cudaMemsetAsync(ctx->full_valid[v].p + px0, 1, pxc, sc));
         }
       }
-      if (sc != s) {
-        CK(cudaEventRecord(ctx->chunk_events[2 * c], sc));
-        CK(cudaStreamWaitEvent(s, ctx->chunk_events[2 * c], 0));
+      if (sc != cs) {
+        CK(cudaEventRecord(ev[2 * c], sc));
+        CK(cudaStreamWaitEvent(cs, ev[2 * c], 0));
       }
     } else if (!left_u8) {
       for (int v = 0; v < 2; ++v) {
@@ -906,19 +949,27 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
       hc.fpo = fpo.data() + np_f * c0;
       hc.fsg = fsg.data() + np_f * c0;
     }
-    const int launches0 = ctx->launches;
-    rc = run_device(ctx, geo, nc, W, H, channels, cu8, left_u8 ? 0 : c0, have_f32_valid, focal,
-                    baseline, f64, out->fill_invalid, out->invalid_value, cout, hc, s);
+    rc = run_device(ctx, ctx->scr[slot], geo, nc, W, H, channels, cu8, left_u8 ? 0 : c0,
+                    have_f32_valid, focal, baseline, f64, out->fill_invalid, out->invalid_value,
+                    cout, hc, cs);
     if (rc) return rc;
-    (void)launches0;
     if (host_out) {
-      CK(cudaEventRecord(ctx->chunk_events[2 * c + 1], s));
-      CK(cudaStreamWaitEvent(ctx->s_out, ctx->chunk_events[2 * c + 1], 0));
+      CK(cudaEventRecord(ev[2 * c + 1], cs));
+      CK(cudaStreamWaitEvent(ctx->s_out, ev[2 * c + 1], 0));
       for (int q = 0; q < 10; ++q)
         if (user_ptr[q])
           CK(cudaMemcpyAsync((uint8_t*)user_ptr[q] + px0 * sizes[q], cout[q], pxc * sizes[q],
                              cudaMemcpyDeviceToHost, ctx->s_out));
     }
+  }
+  // everything the call queued completes before later work on the caller's stream
+  if (used_comp) {
+    CK(cudaEventRecord(ev_comp, ctx->s_comp));
+    CK(cudaStreamWaitEvent(s, ev_comp, 0));
+  }
+  if (host_out) {
+    CK(cudaEventRecord(ev_out, ctx->s_out));
+    CK(cudaStreamWaitEvent(s, ev_out, 0));
   }
   const bool need_sync = host_out || !hstats.empty() || want_finest;
   if (host_out) CK(cudaStreamSynchronize(ctx->s_out));

@@ -43,6 +43,11 @@ struct BandPlan {
 
 // Shared-memory layout of one k_patches CTA (byte offsets), shared by the
 // host planner and the kernel.
+// k_patches shared rows: padded (x + x/32 slots against stride-4 bank
+// conflicts) or plain (immediate tap offsets, 16-byte template loads)
+constexpr bool kPadRows = true;  // left / gradient rows
+constexpr bool kPadRight = true;  // right rows (taps at data-dependent x - u)
+
 struct BandLayout {
   size_t oR, oL, oG, oLQ, oRQ;
   size_t oMean, oHess, oTmsq, oU, oWres;

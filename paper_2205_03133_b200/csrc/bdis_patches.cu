@@ -51,8 +51,10 @@ struct Ev {
 
 template <bool kSmem, bool kR64 = false>
 struct Rows {
-  // right view rows: in shared memory fp64 (kR64: converted once at staging,
-  // slots x + x/16) or fp32 (slots x + x/32); fp32 rows of (w+1) in global
+  // right view rows: in shared memory fp64 (kR64: converted once at staging)
+  // or fp32; fp32 rows of (w+1) in global. Unpadded (kPadRows == false): tap
+  // i of a row sits at a per-row base + i, so its address is an immediate
+  // offset, and the template rows load as 16-byte vectors.
   using RT = typename std::conditional<kSmem && kR64, double, float>::type;
   const RT* R;
   const float* Lf;   // left view
@@ -60,9 +62,9 @@ struct Rows {
   const uint8_t* lq; // 4-tap validity (kValid only)
   const uint8_t* rq;
   int rp, fp, bp;    // row pitches (slots)
-  __device__ __forceinline__ static int s4(int x) { return kSmem ? x + (x >> 5) : x; }
+  __device__ __forceinline__ static int s4(int x) { return (kSmem && kPadRows) ? x + (x >> 5) : x; }
   __device__ __forceinline__ static int s8(int x) {
-    return !kSmem ? x : (kR64 ? x + (x >> 4) : x + (x >> 5));
+    return !(kSmem && kPadRight) ? x : (kR64 ? x + (x >> 4) : x + (x >> 5));
   }
 };
 
@@ -143,8 +145,8 @@ __device__ __forceinline__ Ev eval_patch(const Rows<kSmem, kR64>& rw, int w, int
     const double rmean = __ddiv_rn(sum, (double)n);
     double ssr = 0.0, jr = 0.0;
     rr = rw.R + r0 * rw.rp;
-    const float* lr = rw.Lf + r0 * rw.fp;
-    const float* gr = rw.Gf + r0 * rw.fp;
+    const float* lr = rw.Lf + r0 * rw.fp + (kPadRows ? 0 : x0);
+    const float* gr = rw.Gf + r0 * rw.fp + (kPadRows ? 0 : x0);
 #pragma unroll 1
     for (int j = 0; j < SA; ++j, rr += rw.rp, lr += rw.fp, gr += rw.fp) {
       double a = (double)rr[rw.s8(xb)];
@@ -153,11 +155,11 @@ __device__ __forceinline__ Ev eval_patch(const Rows<kSmem, kR64>& rw, int w, int
         const double b = (double)rr[rw.s8(xb + i + 1)];
         const double v = __dadd_rn(__dmul_rn(mo[i], a), __dmul_rn(mf[i], b));
         a = b;
-        const double t = __dsub_rn((double)lr[offT[i]], mean);
+        const double t = __dsub_rn((double)lr[kPadRows ? offT[i] : i], mean);
         // r * 1 == r; masked columns: r * 0 = +-0 adds nothing to ssr / jr
         const double r = __dmul_rn(__dsub_rn(__dsub_rn(v, rmean), t), mk[i]);
         ssr = __dadd_rn(ssr, __dmul_rn(r, r));
-        if (kJr) jr = __dadd_rn(jr, __dmul_rn((double)gr[offT[i]], r));
+        if (kJr) jr = __dadd_rn(jr, __dmul_rn((double)gr[kPadRows ? offT[i] : i], r));
       }
     }
     ev.msq = __ddiv_rn(ssr, (double)n);
@@ -607,8 +609,10 @@ BandPlan plan_bands(const Level& L, const PatchParams& pp, int max_smem_per_cta)
   };
   bp.r64 = env("PSTEREO_TUNE_R64", 0);
   bp.rpad = g.size;
-  bp.rpitch = (bp.r64 ? pad8_host(L.w + 2 * bp.rpad) : pad4_host(L.w + 2 * bp.rpad)) + 1;
-  bp.fpitch = (L.w - 1 + ((L.w - 1) >> 5)) + 1;  // slots for x in [0, w-1]
+  bp.rpitch = kPadRight ? (bp.r64 ? pad8_host(L.w + 2 * bp.rpad) : pad4_host(L.w + 2 * bp.rpad)) + 1
+                        : L.w + 1 + 2 * bp.rpad;  // x in [-rpad, w + rpad]
+  bp.fpitch = kPadRows ? (L.w - 1 + ((L.w - 1) >> 5)) + 1  // slots for x in [0, w-1]
+                       : (L.w + 3) / 4 * 4;                // 16-byte aligned rows
   bp.bpitch = valid ? L.w : 0;
   const int threads = env("PSTEREO_TUNE_THREADS", 192);
   auto bytes_for = [&](int rb) {
