@@ -171,6 +171,36 @@ __global__ void __launch_bounds__(256) k_pyramid(PyrArgs a) {
     const int w = a.ws[e];
     const long long pl = pair * (long long)w * a.hs[e];
     const long long pr = pair * (long long)(w + 1) * a.hs[e];
+    if ((w & 3) == 0 && w >= 8 && (a.buf_floats & 3) == 0) {
+      // four pixels per thread: 16-byte stores of L and G (rows of 4k floats)
+      const int qw = w >> 2;
+      for (int q = tid; q < rows * qw; q += nt) {
+        const int r = q / qw, x = (q - r * qw) << 2;
+        const float* lr = Lb + r * w;
+        const float4 l4 = *(const float4*)(lr + x);
+        const float lm = x > 0 ? lr[x - 1] : 0.0f, lp = x + 4 < w ? lr[x + 4] : 0.0f;
+        const float l[6] = {lm, l4.x, l4.y, l4.z, l4.w, lp};
+        float g[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int xx = x + k;
+          if (xx == 0) g[k] = __fsub_rn(l[k + 2], l[k + 1]);
+          else if (xx == w - 1) g[k] = __fsub_rn(l[k + 1], l[k]);
+          else g[k] = __fmul_rn(0.5f, __fsub_rn(l[k + 2], l[k]));
+        }
+        const long long o = pl + (long long)(y0 + r) * w + x;
+        *(float4*)(a.L[e] + o) = l4;
+        *(float4*)(a.G[e] + o) = make_float4(g[0], g[1], g[2], g[3]);
+        const float4 r4 = *(const float4*)(Rb + r * w + x);
+        float* rp = a.Rp[e] + pr + (long long)(y0 + r) * (w + 1) + x;
+        rp[0] = r4.x;
+        rp[1] = r4.y;
+        rp[2] = r4.z;
+        rp[3] = r4.w;
+        if (x + 4 == w) rp[4] = r4.w;
+      }
+      return;
+    }
     for (int q = tid; q < rows * w; q += nt) {
       const int r = q / w, x = q % w;
       const float* lr = Lb + r * w;
@@ -221,6 +251,29 @@ __global__ void __launch_bounds__(256) k_pyramid(PyrArgs a) {
     const int y0 = band << (ce - 1), rows = min(1 << (ce - 1), h - y0);
     float* Lb = buf[0];
     float* Rb = buf[0] + a.buf_floats;
+    if (kU8 && a.vec8) {
+      // gray rasters, W % 8 == 0, even H: 8 source bytes of two rows per view
+      // give 4 level-1 pixels (down4 of the grayscale values, as below)
+      const int qw = w >> 2;
+      for (int q = tid; q < rows * qw; q += nt) {
+        const int r = q / qw, xq = q - r * qw;
+        const long long base = pair * (long long)a.W * a.H + (long long)(2 * (y0 + r)) * a.W + 8 * xq;
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const uint8_t* src = (v ? a.u8r : a.u8l) + base;
+          const uint2 t = __ldg((const uint2*)src);
+          const uint2 b = __ldg((const uint2*)(src + a.W));
+          const unsigned tw[2] = {t.x, t.y}, bw[2] = {b.x, b.y};
+          float o[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const unsigned ts = tw[k >> 1] >> (16 * (k & 1)), bs = bw[k >> 1] >> (16 * (k & 1));
+            o[k] = down4(g1[ts & 255u], g1[(ts >> 8) & 255u], g1[bs & 255u], g1[(bs >> 8) & 255u]);
+          }
+          *(float4*)((v ? Rb : Lb) + r * w + 4 * xq) = make_float4(o[0], o[1], o[2], o[3]);
+        }
+      }
+    } else
     for (int q = tid; q < rows * w; q += nt) {
       const int y = y0 + q / w, x = q % w;
       const int sx0 = 2 * x, sx1 = min(2 * x + 1, a.W - 1);
