@@ -392,28 +392,58 @@ struct TileRecords {
 
 constexpr int kTileRec = 320;  // records staged per tile; more -> global gather
 
-template <bool kVar>
-__device__ __forceinline__ Fused gather_tile(const Grid& g, const TileRecords& rec, int x, int y,
-                                             Cover cx, Cover cy,
+// Per-thread column list: the (at most K) patch columns covering the thread's
+// pixel column, ascending, the clamped last patch after the regular ones;
+// unused entries point at the tile's zero column (adds +0.0, the identity).
+template <int K>
+struct ColList {
+  int kxo[K];   // column within the staged records
+  int moff[K];  // x - footprint start (mask column)
+};
+
+template <int K>
+__device__ __forceinline__ bool col_list(const Grid& g, int x, Cover cx, int kx0, int zcol,
+                                         ColList<K>* cl) {
+  const int nmain = cx.hi - cx.lo + 1;
+  const int used = max(nmain, 0) + (cx.last ? 1 : 0);
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    if (k < nmain) {
+      cl->kxo[k] = cx.lo + k - kx0;
+      cl->moff[k] = x - (cx.lo + k) * g.stride;
+    } else if (cx.last && k == max(nmain, 0)) {
+      cl->kxo[k] = g.nx - 1 - kx0;
+      cl->moff[k] = x - g.lastx0;
+    } else {
+      cl->kxo[k] = zcol;
+      cl->moff[k] = 0;
+    }
+  }
+  return used <= K;
+}
+
+template <bool kVar, int K>
+__device__ __forceinline__ Fused gather_tile(const Grid& g, const TileRecords& rec, int y,
+                                             const ColList<K>& cl, Cover cy,
                                              const double* __restrict__ mask) {
   const int s = g.size, st = g.stride;
   Fused f{0.0, 0.0, 0.0, 0.0};
-  auto add = [&](int q, double m) {
-    const double pr = rec.pr[q];
-    const double w = __dmul_rn(pr, m);
-    f.sw = __dadd_rn(f.sw, w);
-    f.swu = __dadd_rn(f.swu, __dmul_rn(w, rec.uu[q]));
-    f.swp = __dadd_rn(f.swp, __dmul_rn(w, pr));
-    if (kVar) {
-      const double sk = rec.sg[q];
-      f.sw2s = __dadd_rn(f.sw2s, __dmul_rn(__dmul_rn(__dmul_rn(w, w), sk), sk));
-    }
-  };
   auto row = [&](int ky, int y0) {
-    const double* mrow = mask + (y - y0) * s + x;
-    const int qrow = (ky - rec.ky0) * rec.ncol - rec.kx0;
-    for (int kx = cx.lo; kx <= cx.hi; ++kx) add(qrow + kx, mrow[-kx * st]);
-    if (cx.last) add(qrow + g.nx - 1, mrow[-g.lastx0]);
+    const double* mrow = mask + (y - y0) * s;
+    const int qrow = (ky - rec.ky0) * rec.ncol;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int q = qrow + cl.kxo[k];
+      const double pr = rec.pr[q];
+      const double w = __dmul_rn(pr, mrow[cl.moff[k]]);
+      f.sw = __dadd_rn(f.sw, w);
+      f.swu = __dadd_rn(f.swu, __dmul_rn(w, rec.uu[q]));
+      f.swp = __dadd_rn(f.swp, __dmul_rn(w, pr));
+      if (kVar) {
+        const double sk = rec.sg[q];
+        f.sw2s = __dadd_rn(f.sw2s, __dmul_rn(__dmul_rn(__dmul_rn(w, w), sk), sk));
+      }
+    }
   };
   // ascending patch index: rows ky ascending, columns kx ascending (:122-135)
   for (int ky = cy.lo; ky <= cy.hi; ++ky) row(ky, ky * st);
@@ -427,7 +457,7 @@ __device__ __forceinline__ Fused gather_tile(const Grid& g, const TileRecords& r
 // tile, each warp four rows, each thread one column (its column cover is
 // computed once). The records of the covering patches are staged in shared
 // memory and each pixel gathers them in ascending patch index.
-template <bool kVar, typename T>
+template <bool kVar, typename T, int K>
 __global__ void __launch_bounds__(kFuseThreads) k_fuse_ccl_local(
     Level L, FinestBufs fb, const double* __restrict__ mask, CclBufs cb) {
   __shared__ int sl[kTilePx];
@@ -459,27 +489,36 @@ __global__ void __launch_bounds__(kFuseThreads) k_fuse_ccl_local(
   __syncthreads();
   const int ky0 = min(g.ny - 1, s_cy[0].lo);
   const int ky1 = max(ky0, s_cy[hl].last ? g.ny - 1 : s_cy[hl].hi);
-  const int ncol = kx1 - kx0 + 1, nrec = ncol * (ky1 - ky0 + 1);
-  const bool staged = nrec <= kTileRec;
+  // staged records: one row per patch row, the tile's columns plus a zero column
+  const int ncol = kx1 - kx0 + 1, pitch = ncol + 1, nrec = pitch * (ky1 - ky0 + 1);
+  ColList<K> cl;
+  const bool listed = col_list<K>(g, x, cx, kx0, ncol, &cl);
+  const bool all_listed = __syncthreads_and(listed || x >= w) != 0;
+  const bool staged = nrec <= kTileRec && all_listed;
   if (staged) {
     const long long rbase = pair * (long long)g.nx * g.ny;
     for (int q = t; q < nrec; q += kFuseThreads) {
-      const long long r = rbase + (long long)(ky0 + q / ncol) * g.nx + kx0 + q % ncol;
-      const bool acc = L.stage[r] == kAccepted;  // fuse_level skips the rest (:127)
+      const int rr = q / pitch, cc = q - rr * pitch;
+      bool acc = false;
+      long long r = 0;
+      if (cc < ncol) {
+        r = rbase + (long long)(ky0 + rr) * g.nx + kx0 + cc;
+        acc = L.stage[r] == kAccepted;  // fuse_level skips the rest (:127)
+      }
       s_pr[q] = acc ? L.prob[r] : 0.0;
       s_u[q] = acc ? L.u[r] : 0.0;
       if (kVar) s_sg[q] = acc ? L.sigma[r] : 0.0;
     }
   }
   __syncthreads();
-  const TileRecords rec{s_pr, s_u, s_sg, ky0, kx0, ncol};
+  const TileRecords rec{s_pr, s_u, s_sg, ky0, kx0, pitch};
   const long long pbase = pair * L.plane;
 #pragma unroll 1
   for (int i = 0; i < kFuseRows; ++i) {
     const int ly = warp + i * kFuseWarps, y = ty0 + ly;
     bool keep = false;
     if (x < w && y < h) {
-      const Fused f = staged ? gather_tile<kVar>(g, rec, x, y, cx, s_cy[ly], s_mask)
+      const Fused f = staged ? gather_tile<kVar, K>(g, rec, y, cl, s_cy[ly], s_mask)
                              : gather<true, kVar>(L, pair, x, y, mask);
       const long long o = pbase + (long long)y * w + x;
       const bool valid = !(f.sw <= 0.0);  // fuse_level: sw <= 0 stays invalid (:138)
@@ -869,12 +908,25 @@ void launch_fuse_ccl(const Level& L, const FinestBufs& fb, const double* mask, i
   const long long plane = L.plane;
   const int nt = ccl_tiles(w, h);
   const dim3 grid(nt, n_pairs);
+  // covering columns per pixel: at most ceil(size / stride) regular + the last
+  const int kcov = (L.g.size + L.g.stride - 1) / L.g.stride + 1;
+  auto go = [&](auto kv, auto kk) {
+    constexpr bool V = decltype(kv)::value;
+    constexpr int K = decltype(kk)::value;
+    if (f64) k_fuse_ccl_local<V, double, K><<<grid, kFuseThreads, 0, s>>>(L, fb, mask, cb);
+    else k_fuse_ccl_local<V, float, K><<<grid, kFuseThreads, 0, s>>>(L, fb, mask, cb);
+  };
+  using T3 = std::integral_constant<int, 3>;
+  using T4 = std::integral_constant<int, 4>;
+  using T6 = std::integral_constant<int, 6>;
   if (want_var) {
-    if (f64) k_fuse_ccl_local<true, double><<<grid, kFuseThreads, 0, s>>>(L, fb, mask, cb);
-    else k_fuse_ccl_local<true, float><<<grid, kFuseThreads, 0, s>>>(L, fb, mask, cb);
+    if (kcov <= 3) go(std::true_type{}, T3{});
+    else if (kcov <= 4) go(std::true_type{}, T4{});
+    else go(std::true_type{}, T6{});
   } else {
-    if (f64) k_fuse_ccl_local<false, double><<<grid, kFuseThreads, 0, s>>>(L, fb, mask, cb);
-    else k_fuse_ccl_local<false, float><<<grid, kFuseThreads, 0, s>>>(L, fb, mask, cb);
+    if (kcov <= 3) go(std::false_type{}, T3{});
+    else if (kcov <= 4) go(std::false_type{}, T4{});
+    else go(std::false_type{}, T6{});
   }
   const int tx = (w + kTileW - 1) / kTileW, ty = (h + kTileH - 1) / kTileH;
   const long long nb = (long long)(tx - 1) * h + (long long)(ty - 1) * w;
