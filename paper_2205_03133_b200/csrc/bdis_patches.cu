@@ -144,24 +144,33 @@ __device__ __forceinline__ Ev eval_patch(const Rows<kSmem, kR64>& rw, int w, int
     }
     const double rmean = __ddiv_rn(sum, (double)n);
     double ssr = 0.0, jr = 0.0;
-    rr = rw.R + r0 * rw.rp;
-    const float* lr = rw.Lf + r0 * rw.fp + (kPadRows ? 0 : x0);
-    const float* gr = rw.Gf + r0 * rw.fp + (kPadRows ? 0 : x0);
+    auto pass2 = [&](auto masked) {
+      constexpr bool kMask = decltype(masked)::value;
+      const auto* rr = rw.R + r0 * rw.rp;
+      const float* lr = rw.Lf + r0 * rw.fp + (kPadRows ? 0 : x0);
+      const float* gr = rw.Gf + r0 * rw.fp + (kPadRows ? 0 : x0);
 #pragma unroll 1
-    for (int j = 0; j < SA; ++j, rr += rw.rp, lr += rw.fp, gr += rw.fp) {
-      double a = (double)rr[rw.s8(xb)];
+      for (int j = 0; j < SA; ++j, rr += rw.rp, lr += rw.fp, gr += rw.fp) {
+        double a = (double)rr[rw.s8(xb)];
 #pragma unroll
-      for (int i = 0; i < SA; ++i) {
-        const double b = (double)rr[rw.s8(xb + i + 1)];
-        const double v = __dadd_rn(__dmul_rn(mo[i], a), __dmul_rn(mf[i], b));
-        a = b;
-        const double t = __dsub_rn((double)lr[kPadRows ? offT[i] : i], mean);
-        // r * 1 == r; masked columns: r * 0 = +-0 adds nothing to ssr / jr
-        const double r = __dmul_rn(__dsub_rn(__dsub_rn(v, rmean), t), mk[i]);
-        ssr = __dadd_rn(ssr, __dmul_rn(r, r));
-        if (kJr) jr = __dadd_rn(jr, __dmul_rn((double)gr[kPadRows ? offT[i] : i], r));
+        for (int i = 0; i < SA; ++i) {
+          const double b = (double)rr[rw.s8(xb + i + 1)];
+          const double v = __dadd_rn(__dmul_rn(mo[i], a), __dmul_rn(mf[i], b));
+          a = b;
+          const double t = __dsub_rn((double)lr[kPadRows ? offT[i] : i], mean);
+          double r = __dsub_rn(__dsub_rn(v, rmean), t);
+          // masked columns: r * 0 = +-0 adds nothing to ssr / jr
+          if (kMask) r = __dmul_rn(r, mk[i]);
+          ssr = __dadd_rn(ssr, __dmul_rn(r, r));
+          if (kJr) jr = __dadd_rn(jr, __dmul_rn((double)gr[kPadRows ? offT[i] : i], r));
+        }
       }
-    }
+    };
+    // every column in the image (the common case): no mask multiply; a lane
+    // only votes for the unmasked pass when its own columns are all inside
+    constexpr unsigned kAll = SA >= 32 ? 0xffffffffu : ((1u << SA) - 1u);
+    if (__all_sync(__activemask(), inb == kAll)) pass2(std::false_type{});
+    else pass2(std::true_type{});
     ev.msq = __ddiv_rn(ssr, (double)n);
     ev.jr = jr;
     return ev;
@@ -434,10 +443,15 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
         k = j - (j / nwin) * nwin;
         ue = __dadd_rn(st_u[p], pp.woff[k]);
       }
+      // warps holding no LK solve skip the jr chain (warp-uniform choice)
+      const bool warp_lk = __any_sync(0xffffffffu, lk);
       if (busy) {
-        // one code path for both kinds of job: a warp costs one evaluation
-        const Ev ev = eval_patch<S, kSmem, kValid, kR64>(
-            rw, w, s, col_start(p % g.nx), row_start(ky0 + p / g.nx) - rofs, rpad, st_mean[p], ue);
+        // one code path per warp for both kinds of job: a warp costs one evaluation
+        const int ex0 = col_start(p % g.nx), er0 = row_start(ky0 + p / g.nx) - rofs;
+        const Ev ev = warp_lk ? eval_patch<S, kSmem, kValid, kR64, true>(rw, w, s, ex0, er0, rpad,
+                                                                         st_mean[p], ue)
+                              : eval_patch<S, kSmem, kValid, kR64, false>(rw, w, s, ex0, er0, rpad,
+                                                                          st_mean[p], ue);
         if (!lk) {
           // sample_window: valid iff every template pixel was sampled (:31-36)
           st_wres[p * nwin + k] = ev.msq;
