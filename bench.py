@@ -330,8 +330,9 @@ def run_ours(args):
                      "traffic": traffic, "peak_kind": peak_kind,
                      "alg_bytes_per_launch": alg_bytes, "launch_ms": patch_ms,
                      "kernel_share_of_step": patch_ms / step_ms,
-                     "note": "not HBM-bound: FP64/XU issue-bound bit-exact mirror of the "
-                             "reference's double arithmetic (see DESIGN.md, profiles/r01)"},
+                     "note": "not HBM-bound: a latency/issue-bound FP64 mirror of the "
+                             "reference's double arithmetic (ncu: issue 47%, FP64 34%, XU 42%; "
+                             "DESIGN.md section 4, profiles/r01)"},
         "path_roofline": {"bytes_per_pair": b_pair, "roofline_pairs_s": hbm * 1e9 / b_pair,
                           "frac": value / (world * hbm * 1e9 / b_pair)},
         "stage_ms_per_step": {k: v / max(calls, 1) for k, v in stages.items()},
