@@ -130,6 +130,39 @@ def test_shifted_analytic_pair(gpu, port):
     np.testing.assert_array_equal(res["disparity"], match["disparity"])
 
 
+def test_config3_full_size(gpu, port):
+    """BASELINE config 3: 1280x1024, exps 4..1, 12x12 patches stride 4,
+    variance on -- the largest single-pair configuration."""
+    P = gpu
+    l, r = P.synth_pair(3)
+    _check(P, port, P.PipelineConfig.baseline(3), l[None], r[None])
+
+
+@pytest.mark.parametrize("w,h,ch,size,stride", [
+    (320, 240, 3, 8, 2), (320, 240, 3, 12, 6), (320, 240, 1, 16, 4), (640, 480, 3, 12, 2),
+    pytest.param(1920, 1080, 3, 16, 6, marks=pytest.mark.slow),
+])
+def test_config4_sweep(gpu, port, w, h, ch, size, stride):
+    """BASELINE config 4: sizes x patch sizes x strides, RGB through the
+    Rec.601 conversion (src/image.cpp:36)."""
+    P = gpu
+    l, r = P.synth_pair(4, seed=size * 10 + stride, width=w, height=h, channels=ch)
+    cfg = P.PipelineConfig(coarsest_exp=3, finest_exp=1, patch_size=size,
+                           overlap=1.0 - stride / size)
+    _check(P, port, cfg, l[None], r[None])
+
+
+def test_empty_batch_and_limits(gpu):
+    """n = 0 is a no-op; frames larger than the context's maximum are refused."""
+    P = gpu
+    cfg = P.PipelineConfig.baseline(0)
+    with P.Matcher(cfg, 160, 120, 2) as m:
+        out = m.run_batch(np.zeros((0, 120, 160), np.uint8), np.zeros((0, 120, 160), np.uint8))
+        assert out["disparity"].shape == (0, 120, 160)
+        with pytest.raises(P.GpuError):
+            m.run_batch(np.zeros((1, 240, 320), np.uint8), np.zeros((1, 240, 320), np.uint8))
+
+
 def test_determinism(gpu):
     P = gpu
     left, right = P.synth_batch(0, 2, seed0=0, width=320, height=240)
