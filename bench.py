@@ -305,10 +305,25 @@ def run_ours(args):
     patch_ms = stages.get(f"patches_e{e_f}", 0.0) / max(calls, 1)
     achieved = alg_bytes / (patch_ms / 1e3) / 1e9 if patch_ms > 0 else 0.0
     traffic = None
+    fp64 = None
     tj = ROOT / "profiles" / "ncu_traffic.json"
     if tj.exists():
         t = json.loads(tj.read_text())["k_patches_finest"]
         traffic = t["dram_bytes_per_launch"] / t["pairs_in_launch"] * B
+        if "fp64_inst_per_launch" in t and patch_ms > 0:
+            # the pipes this kernel actually runs on: FP64 (DADD/DMUL/DFMA) and
+            # XU (float<->double/int conversions); counts from ncu for the same
+            # launch scaled to this batch, time from the live CUDA events; peaks
+            # are this box's measured per-SM rates (scripts/microbench.cu:
+            # DADD 62.6, F2F 15.5 thread-ops/clk/SM) x 148 SMs x max clock
+            sm_hz = 148 * 1965e6
+            f_ops = t["fp64_inst_per_launch"] / t["pairs_in_launch"] * B / (patch_ms / 1e3)
+            x_ops = t["conversion_inst_per_launch"] / t["pairs_in_launch"] * B / (patch_ms / 1e3)
+            fp64 = {"unit": "T thread-inst/s",
+                    "fp64_achieved": f_ops / 1e12, "fp64_peak": 62.6 * sm_hz / 1e12,
+                    "fp64_frac": f_ops / (62.6 * sm_hz),
+                    "xu_achieved": x_ops / 1e12, "xu_peak": 15.5 * sm_hz / 1e12,
+                    "xu_frac": x_ops / (15.5 * sm_hz)}
     step_ms = ms_max / args.steps
     b_pair = W * H * (2 * 1 + 4 + 1)  # inputs + fp32 disparity + u8 mask
     line = {
@@ -330,6 +345,7 @@ def run_ours(args):
                      "traffic": traffic, "peak_kind": peak_kind,
                      "alg_bytes_per_launch": alg_bytes, "launch_ms": patch_ms,
                      "kernel_share_of_step": patch_ms / step_ms,
+                     "pipes": fp64,
                      "note": "not HBM-bound: a latency/issue-bound FP64 mirror of the "
                              "reference's double arithmetic (ncu: issue 47%, FP64 34%, XU 42%; "
                              "DESIGN.md section 4, profiles/r01)"},
