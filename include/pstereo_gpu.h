@@ -179,6 +179,29 @@ int pstereo_gpu_match_f32(pstereo_ctx* ctx, int n_pairs, int width, int height,
                           void* stream);
 
 /* Kernel launches issued by the last match call (telemetry for bench.py). */
+/* compute_metrics (src/metrics.cpp:10-52; FrameMetrics,
+ * inc/metrics.hpp:14-25) for n_frames ScalarFields of width x height:
+ * errors |estimate - reference| over pixels valid on both sides; mean error
+ * (the reference's sequential sum, bit-identical), median error (middle order
+ * statistic, mean of the two middle ones for an even count), coverage_rate =
+ * share of compared pixels with a valid sigma and |error| <= 1.96 sigma (NaN
+ * when sigma is NULL). valid_px counts the estimate's valid pixels. Planes are
+ * [frame][height][width] doubles / bytes, on the device when
+ * inputs_on_device, else host memory; out is host memory. */
+typedef struct pstereo_frame_metrics {
+  long long valid_px;
+  long long compared;
+  int has_errors;      /* 0 when no pixel was comparable (mean/median NaN) */
+  double mean_err;
+  double median_err;
+  double coverage_rate;
+} pstereo_frame_metrics;
+int pstereo_gpu_metrics(pstereo_ctx* ctx, int n_frames, int width, int height,
+                        const double* estimate, const uint8_t* estimate_valid,
+                        const double* reference, const uint8_t* reference_valid,
+                        const double* sigma, const uint8_t* sigma_valid,
+                        int inputs_on_device, pstereo_frame_metrics* out, void* stream);
+
 int pstereo_gpu_last_launch_count(const pstereo_ctx* ctx);
 
 /* Stage timing with CUDA events recorded on the launch stream (no extra

@@ -19,6 +19,7 @@
 
 #include <chrono>
 #include <cstdint>
+#include <limits>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -310,6 +311,44 @@ inline MatchResult match_stereo(const GrayImage& left, const GrayImage& right,
   for (const auto& s : stats)
     m.stats.levels.push_back({s.exp, s.grid_patches, s.extracted, s.converged, s.accepted});
   return m;
+}
+
+// FrameMetrics / compute_metrics (inc/metrics.hpp:14-32, src/metrics.cpp:10-52)
+struct FrameMetrics {
+  std::string frame;
+  double mean_err = std::numeric_limits<double>::quiet_NaN();
+  double median_err = std::numeric_limits<double>::quiet_NaN();
+  long long valid_px = 0;
+  double runtime_ms = 0.0;
+  double coverage_rate = std::numeric_limits<double>::quiet_NaN();
+  bool has_errors = false;
+};
+
+inline FrameMetrics compute_metrics(const ScalarField& estimate, const ScalarField& reference,
+                                    const ScalarField* sigma, double runtime_ms,
+                                    const std::string& frame) {
+  const int w = estimate.width, h = estimate.height;
+  pstereo_params p;
+  pstereo_default_params(&p);
+  p.coarsest_exp = 0;
+  p.finest_exp = 0;
+  p.patch_size = 2;
+  pstereo_ctx* ctx = detail::context_for(p, w, h, 1);
+  pstereo_frame_metrics m{};
+  const int rc = pstereo_gpu_metrics(
+      ctx, 1, w, h, estimate.values.data(), estimate.valid.data(), reference.values.data(),
+      reference.valid.data(), sigma ? sigma->values.data() : nullptr,
+      sigma ? sigma->valid.data() : nullptr, 0, &m, nullptr);
+  if (rc) detail::raise(rc, pstereo_gpu_last_error(ctx));
+  FrameMetrics f;
+  f.frame = frame;
+  f.runtime_ms = runtime_ms;
+  f.valid_px = m.valid_px;
+  f.has_errors = m.has_errors != 0;
+  f.mean_err = m.mean_err;
+  f.median_err = m.median_err;
+  f.coverage_rate = m.coverage_rate;
+  return f;
 }
 
 }  // namespace gpu

@@ -1385,3 +1385,47 @@ int bo_run_pipeline(const bo_image* left, const bo_image* right,
   free(mvv);
   return rc;
 }
+
+/* ------------------------------------------------------------------------
+ * compute_metrics (src/metrics.cpp:10-52): errors |est - ref| over pixels
+ * valid on both sides, in index order; mean = sequential sum / count; median
+ * = the middle order statistic (mean of the two middle ones for an even
+ * count: nth_element twice, :40-48 -- order statistics do not depend on the
+ * selection algorithm, so a sort gives the same values); coverage = share of
+ * compared pixels with a valid sigma and |e| <= 1.96 sigma (:33).
+ * ------------------------------------------------------------------------ */
+
+void bo_compute_metrics(int w, int h, const double* est, const uint8_t* est_valid,
+                        const double* ref, const uint8_t* ref_valid, const double* sigma,
+                        const uint8_t* sigma_valid, bo_frame_metrics* out) {
+  const size_t n = (size_t)w * (size_t)h;
+  out->mean_err = NAN;
+  out->median_err = NAN;
+  out->coverage_rate = NAN;
+  out->has_errors = 0;
+  out->valid_px = 0;
+  for (size_t i = 0; i < n; ++i) out->valid_px += est_valid[i] != 0; /* fields.hpp valid_count */
+  double* errs = (double*)malloc((n ? n : 1) * sizeof(double));
+  size_t m = 0;
+  long long covered = 0;
+  for (size_t i = 0; i < n; ++i) {
+    if (!est_valid[i] || !ref_valid[i]) continue;
+    const double e = fabs(est[i] - ref[i]);
+    errs[m++] = e;
+    if (sigma && sigma_valid[i] && e <= 1.96 * sigma[i]) ++covered;
+  }
+  out->compared = (long long)m;
+  if (m == 0) {
+    free(errs);
+    return;
+  }
+  out->has_errors = 1;
+  double sum = 0.0;
+  for (size_t i = 0; i < m; ++i) sum += errs[i];
+  out->mean_err = sum / (double)m;
+  qsort(errs, m, sizeof(double), cmp_double);
+  const size_t mid = m / 2;
+  out->median_err = (m % 2 == 1) ? errs[mid] : 0.5 * (errs[mid - 1] + errs[mid]);
+  if (sigma) out->coverage_rate = (double)covered / (double)m;
+  free(errs);
+}

@@ -193,6 +193,18 @@ void bo_disparity_to_depth(int w, int h, const double* disp,
                            double* depth, uint8_t* depth_valid, double* sigma,
                            uint8_t* sigma_valid);
 
+/* ---- metrics (src/metrics.cpp:10-52) ---- */
+typedef struct bo_frame_metrics {
+  long long valid_px;   /* estimate.valid_count() */
+  long long compared;   /* pixels valid in estimate and reference */
+  int has_errors;
+  double mean_err, median_err, coverage_rate; /* NaN when unavailable */
+} bo_frame_metrics;
+/* sigma / sigma_valid may be NULL (coverage_rate stays NaN) */
+void bo_compute_metrics(int w, int h, const double* est, const uint8_t* est_valid,
+                        const double* ref, const uint8_t* ref_valid, const double* sigma,
+                        const uint8_t* sigma_valid, bo_frame_metrics* out);
+
 /* ---- whole path ---- */
 int bo_match_stereo(const bo_image* left, const bo_image* right,
                     const bo_config* cfg, bo_match_outputs* out, char* msg,

@@ -57,6 +57,12 @@ class BoOutputs(C.Structure):
                 ("stats", i32p), ("n_levels", C.c_int), ("runtime_ms", C.c_double)]
 
 
+class BoFrameMetrics(C.Structure):
+    _fields_ = [("valid_px", C.c_longlong), ("compared", C.c_longlong), ("has_errors", C.c_int),
+                ("mean_err", C.c_double), ("median_err", C.c_double),
+                ("coverage_rate", C.c_double)]
+
+
 class BoMatchOutputs(C.Structure):
     _fields_ = [("disparity", f64p), ("disparity_valid", u8p), ("probability", f64p),
                 ("probability_valid", u8p), ("var_disp", f64p), ("var_valid", u8p),
@@ -346,6 +352,21 @@ class Oracle:
         return out, ov
 
     # ---- filter / depth
+    def compute_metrics(self, est, est_valid, ref, ref_valid, sigma=None, sigma_valid=None):
+        """src/metrics.cpp:10-52 -> dict(valid_px, compared, has_errors, mean_err,
+        median_err, coverage_rate)."""
+        e = np.ascontiguousarray(est, np.float64)
+        ev = np.ascontiguousarray(est_valid, np.uint8)
+        r = np.ascontiguousarray(ref, np.float64)
+        rv = np.ascontiguousarray(ref_valid, np.uint8)
+        sg = None if sigma is None else np.ascontiguousarray(sigma, np.float64)
+        sv = None if sigma is None else np.ascontiguousarray(sigma_valid, np.uint8)
+        h, w = e.shape
+        m = BoFrameMetrics()
+        self.lib.bo_compute_metrics(C.c_int(w), C.c_int(h), _p(e, f64p), _p(ev, u8p), _p(r, f64p),
+                                    _p(rv, u8p), _p(sg, f64p), _p(sv, u8p), C.byref(m))
+        return {k: getattr(m, k) for k, _ in BoFrameMetrics._fields_}
+
     def remove_small_components(self, valid, min_px):
         v = np.ascontiguousarray(valid, np.uint8)
         h, w = v.shape

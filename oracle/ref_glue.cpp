@@ -26,6 +26,7 @@
 #include "pstereo/lk_solver.hpp"
 #include "pstereo/patch.hpp"
 #include "pstereo/pipeline.hpp"
+#include "pstereo/metrics.hpp"
 #include "pstereo/pyramid.hpp"
 #include "pstereo/spatial_mask.hpp"
 #include "pstereo/window_posterior.hpp"
@@ -480,6 +481,29 @@ int bo_run_pipeline(const bo_image* left, const bo_image* right,
     copy_stats(o.stats, out->stats, &out->n_levels);
     out->runtime_ms = o.runtime_ms;
   });
+}
+
+void bo_compute_metrics(int w, int h, const double* est, const uint8_t* est_valid,
+                        const double* ref, const uint8_t* ref_valid, const double* sigma,
+                        const uint8_t* sigma_valid, bo_frame_metrics* out) {
+  auto field = [&](const double* v, const uint8_t* ok) {
+    ScalarField f = ScalarField::sized(w, h);
+    std::memcpy(f.values.data(), v, f.values.size() * sizeof(double));
+    std::memcpy(f.valid.data(), ok, f.valid.size());
+    return f;
+  };
+  const ScalarField e = field(est, est_valid), r = field(ref, ref_valid);
+  ScalarField sg;
+  if (sigma) sg = field(sigma, sigma_valid);
+  const FrameMetrics m = compute_metrics(e, r, sigma ? &sg : nullptr, 0.0, "");  // src/metrics.cpp:10-52
+  out->valid_px = m.valid_px;
+  long long compared = 0;
+  for (std::size_t i = 0; i < e.valid.size(); ++i) compared += (e.valid[i] && r.valid[i]) ? 1 : 0;
+  out->compared = compared;
+  out->has_errors = m.has_errors ? 1 : 0;
+  out->mean_err = m.mean_err;
+  out->median_err = m.median_err;
+  out->coverage_rate = m.coverage_rate;
 }
 
 }  // extern "C"

@@ -73,6 +73,13 @@ class PatchEstimate(C.Structure):
                 ("prob", C.c_double), ("posterior", C.c_double), ("sigma_k", C.c_double)]
 
 
+class FrameMetricsC(C.Structure):
+    """pstereo_frame_metrics (FrameMetrics, inc/metrics.hpp:14-25)."""
+    _fields_ = [("valid_px", C.c_longlong), ("compared", C.c_longlong), ("has_errors", C.c_int),
+                ("mean_err", C.c_double), ("median_err", C.c_double),
+                ("coverage_rate", C.c_double)]
+
+
 class _Outputs(C.Structure):
     _fields_ = [
         ("dtype", C.c_int), ("on_device", C.c_int), ("disparity", C.c_void_p),
@@ -119,6 +126,10 @@ def lib() -> C.CDLL:
                                             C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
                                             C.c_double, C.c_double, C.POINTER(_Outputs),
                                             C.c_void_p]
+        L.pstereo_gpu_metrics.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p,
+                                          C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                          C.c_void_p, C.c_int, C.POINTER(FrameMetricsC),
+                                          C.c_void_p]
         L.pstereo_validate.argtypes = [C.POINTER(_Params), C.c_char_p, C.c_size_t]
         L.pstereo_level_dims.argtypes = [C.POINTER(_Params), C.c_int, C.c_int, i32p, i32p,
                                          i32p, i32p]
@@ -165,6 +176,7 @@ ABI_SYMBOLS = [
     "pstereo_gpu_match_f32", "pstereo_gpu_last_launch_count", "pstereo_gpu_set_profiling",
     "pstereo_gpu_stage_times", "pstereo_gpu_stage_name", "pstereo_synth_default",
     "pstereo_synth_pair", "pstereo_synth_batch", "pstereo_debug_eval_residual",
+    "pstereo_gpu_metrics",
 ]
 
 
@@ -418,6 +430,39 @@ class Matcher:
         return res
 
     # ---- device-pointer batched API (the zero-copy path used by bench.py)
+    def metrics(self, estimate, estimate_valid, reference, reference_valid, sigma=None,
+                sigma_valid=None):
+        """compute_metrics (src/metrics.cpp:10-52) on the GPU for [n,h,w] (or [h,w])
+        double fields + u8 validity; returns one dict per frame (FrameMetrics)."""
+        est = np.ascontiguousarray(estimate, np.float64)
+        single = est.ndim == 2
+        if single:
+            est = est[None]
+        n, h, w = est.shape
+
+        def prep(a, dt):
+            a = np.ascontiguousarray(a, dt)
+            return a[None] if a.ndim == 2 else a
+
+        ev = prep(estimate_valid, np.uint8)
+        ref = prep(reference, np.float64)
+        rv = prep(reference_valid, np.uint8)
+        sg = None if sigma is None else prep(sigma, np.float64)
+        sv = None if sigma is None else prep(sigma_valid, np.uint8)
+        for a in (ev, ref, rv) + ((sg, sv) if sg is not None else ()):
+            if a.shape != (n, h, w):
+                raise ValueError("metrics: field shapes differ")
+        out = (FrameMetricsC * max(n, 1))()
+        ptr = (lambda a: a.ctypes.data if a is not None else None)
+        rc = lib().pstereo_gpu_metrics(self._h, n, w, h, ptr(est), ptr(ev), ptr(ref), ptr(rv),
+                                       ptr(sg), ptr(sv), 0, out, None)
+        if rc:
+            _raise(rc, self.last_error())
+        res = [{k: getattr(out[i], k) for k, _ in FrameMetricsC._fields_} for i in range(n)]
+        for r in res:
+            r["has_errors"] = bool(r["has_errors"])
+        return res[0] if single else res
+
     def run_device_u8(self, n, width, height, channels, left_ptr, right_ptr, outputs: dict,
                       dtype=F32, focal=1.0, baseline=1.0, stream=None, invalid_value=None):
         o = _Outputs()
@@ -512,3 +557,12 @@ def match_stereo(left, right, cfg: PipelineConfig, dtype=F64, finest_cap=1 << 16
     if cfg.estimate_variance:
         res["var_disp"] = out["var_disp"][0]
     return res
+
+
+def compute_metrics(estimate, estimate_valid, reference, reference_valid, sigma=None,
+                    sigma_valid=None):
+    """compute_metrics (src/metrics.cpp:10-52) on the GPU; see Matcher.metrics."""
+    est = np.asarray(estimate)
+    h, w = est.shape[-2], est.shape[-1]
+    return _matcher_for(PipelineConfig(coarsest_exp=0, finest_exp=0, patch_size=2), w, h).metrics(
+        estimate, estimate_valid, reference, reference_valid, sigma, sigma_valid)

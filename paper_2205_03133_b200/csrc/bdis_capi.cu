@@ -226,6 +226,11 @@ struct pstereo_ctx {
   // host-buffer pipeline (chunked H2D / compute / D2H)
   int chunk_pairs = 0;
   cudaStream_t s_in = nullptr, s_out = nullptr, s_comp = nullptr;
+  // compute_metrics staging
+  DevBuf<double> met_f64;
+  DevBuf<uint8_t> met_u8;
+  DevBuf<unsigned long long> met_keys;
+  DevBuf<pstereo_frame_metrics_dev> met_out;
   std::vector<cudaEvent_t> chunk_events;
 };
 
@@ -412,6 +417,10 @@ void pstereo_gpu_destroy(pstereo_ctx* ctx) {
   for (auto& b : ctx->full) b.release();
   for (auto& b : ctx->full_valid) b.release();
   for (auto& sc : ctx->scr) sc.release();
+  ctx->met_f64.release();
+  ctx->met_u8.release();
+  ctx->met_keys.release();
+  ctx->met_out.release();
   for (auto& b : ctx->out_stage) b.release();
   for (auto e : ctx->chunk_events) cudaEventDestroy(e);
   if (ctx->s_in) cudaStreamDestroy(ctx->s_in);
@@ -429,6 +438,58 @@ const char* pstereo_gpu_last_error(const pstereo_ctx* ctx) {
 }
 
 int pstereo_gpu_last_launch_count(const pstereo_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+static_assert(sizeof(pstereo_frame_metrics) == sizeof(bdis::pstereo_frame_metrics_dev),
+              "frame metrics layouts differ");
+
+int pstereo_gpu_metrics(pstereo_ctx* ctx, int n, int w, int h, const double* est,
+                        const uint8_t* est_valid, const double* ref, const uint8_t* ref_valid,
+                        const double* sigma, const uint8_t* sigma_valid, int inputs_on_device,
+                        pstereo_frame_metrics* out, void* stream) {
+  if (!ctx) return PSTEREO_EINTERNAL;
+  if (n < 0 || w <= 0 || h <= 0 || !out || !est || !est_valid || !ref || !ref_valid ||
+      (sigma && !sigma_valid))
+    return fail(ctx, PSTEREO_EINTERNAL, "pstereo_gpu_metrics: bad arguments");
+  if (n == 0) return PSTEREO_OK;
+  if (cudaSetDevice(ctx->device) != cudaSuccess) return fail(ctx, PSTEREO_EINTERNAL, "no device");
+  cudaStream_t s = stream ? (cudaStream_t)stream : ctx->stream;
+  const size_t px = size_t(w) * h * n;
+  MetricsArgs a;
+  a.w = w;
+  a.h = h;
+  a.est = est;
+  a.est_valid = est_valid;
+  a.ref = ref;
+  a.ref_valid = ref_valid;
+  a.sigma = sigma;
+  a.sigma_valid = sigma_valid;
+  if (!inputs_on_device) {
+    const int nf = sigma ? 3 : 2;
+    CK(ctx->met_f64.ensure(px * nf));
+    CK(ctx->met_u8.ensure(px * nf));
+    const double* fs[3] = {est, ref, sigma};
+    const uint8_t* vs[3] = {est_valid, ref_valid, sigma_valid};
+    for (int q = 0; q < nf; ++q) {
+      CK(cudaMemcpyAsync(ctx->met_f64.p + px * q, fs[q], px * 8, cudaMemcpyHostToDevice, s));
+      CK(cudaMemcpyAsync(ctx->met_u8.p + px * q, vs[q], px, cudaMemcpyHostToDevice, s));
+    }
+    a.est = ctx->met_f64.p;
+    a.ref = ctx->met_f64.p + px;
+    a.sigma = sigma ? ctx->met_f64.p + 2 * px : nullptr;
+    a.est_valid = ctx->met_u8.p;
+    a.ref_valid = ctx->met_u8.p + px;
+    a.sigma_valid = sigma ? ctx->met_u8.p + 2 * px : nullptr;
+  }
+  CK(ctx->met_keys.ensure(px));
+  CK(ctx->met_out.ensure(size_t(n)));
+  a.scratch = ctx->met_keys.p;
+  a.out = ctx->met_out.p;
+  CK(launch_metrics(a, n, s));
+  CK(cudaMemcpyAsync(out, ctx->met_out.p, sizeof(pstereo_frame_metrics) * n,
+                     cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return PSTEREO_OK;
+}
 
 int pstereo_gpu_set_profiling(pstereo_ctx* ctx, int enable) {
   if (!ctx) return PSTEREO_EINTERNAL;

@@ -187,6 +187,25 @@ cudaError_t launch_debug_eval(const Level& L, int size, int all_valid, int nq, c
                               const int* qy, const double* qu, double* msq, double* jr, int* n,
                               cudaStream_t s);
 void launch_output(const OutputArgs& a, int f64, int n_pairs, cudaStream_t s);
+
+// compute_metrics (src/metrics.cpp:10-52), one CTA per frame (bdis_metrics.cu)
+struct pstereo_frame_metrics_dev {
+  long long valid_px, compared;
+  int has_errors;
+  double mean_err, median_err, coverage_rate;
+};
+struct MetricsArgs {
+  int w, h;
+  const double* est;
+  const uint8_t* est_valid;
+  const double* ref;
+  const uint8_t* ref_valid;
+  const double* sigma;  // nullable (with sigma_valid)
+  const uint8_t* sigma_valid;
+  unsigned long long* scratch;  // w*h keys per frame
+  pstereo_frame_metrics_dev* out;
+};
+cudaError_t launch_metrics(const MetricsArgs& a, int n_frames, cudaStream_t s);
 void launch_stats(const StatsArgs& a, int n_pairs, cudaStream_t s);
 
 }  // namespace bdis

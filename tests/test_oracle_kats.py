@@ -401,3 +401,61 @@ def test_gn_recovery_rate(orc):
         f = orc.estimate_variance(offs, [c * math.exp(-o * o / (2 * s * s)) for o in offs])
         ok += f["accepted"] and abs(f["sigma_k"] - s) < 1e-4 * s
     assert ok >= 990
+
+
+# ---- compute_metrics (tests/test_metrics.cpp:9-84) ----
+
+def _fields(vals, valid=None):
+    v = np.asarray(vals, np.float64)[None, :]
+    ok = np.ones_like(v, np.uint8) if valid is None else np.asarray(valid, np.uint8)[None, :]
+    return v, ok
+
+
+def test_metrics_kats(orc):
+    est, ok = _fields([1.0, 2.0, 9.0])
+    z = np.zeros_like(est)
+    m = orc.compute_metrics(est, ok, z, ok)  # :9-23
+    assert m["has_errors"] and m["mean_err"] == 4.0 and m["median_err"] == 2.0
+    assert m["valid_px"] == 3 and np.isnan(m["coverage_rate"])
+    est, ok = _fields([1.0, 2.0, 4.0, 9.0])  # :25-34 even count
+    assert orc.compute_metrics(est, ok, np.zeros_like(est), ok)["median_err"] == 3.0
+    e = np.full((8, 8), 3.0)  # :36-43 exact
+    ok8 = np.ones((8, 8), np.uint8)
+    m = orc.compute_metrics(e, ok8, e, ok8)
+    assert m["mean_err"] == 0.0 and m["median_err"] == 0.0 and m["valid_px"] == 64
+    est, ev = _fields([100.0, 5.0, 5.0], [0, 1, 1])  # :45-55 masks
+    ref, rv = _fields([5.0, 5.0, 5.0], [1, 0, 1])
+    m = orc.compute_metrics(est, ev, ref, rv)
+    assert m["mean_err"] == 0.0 and m["valid_px"] == 2
+    est, ev = _fields([1.0, 1.0], [0, 0])  # :57-65 nothing comparable
+    m = orc.compute_metrics(est, ev, est, np.ones_like(ev))
+    assert not m["has_errors"] and np.isnan(m["mean_err"]) and np.isnan(m["median_err"])
+    assert m["valid_px"] == 0
+    est, ok = _fields([1.0, -1.5, 2.5, 1.96])  # :67-76 coverage, boundary inclusive
+    m = orc.compute_metrics(est, ok, np.zeros_like(est), ok, np.ones_like(est), ok)
+    assert m["coverage_rate"] == 0.75
+    est, ok = _fields([0.5, 0.5])  # :78-84 missing sigma counts as a miss
+    m = orc.compute_metrics(est, ok, np.zeros_like(est), ok, np.ones_like(est),
+                            np.array([[1, 0]], np.uint8))
+    assert m["coverage_rate"] == 0.5
+
+
+def test_metrics_port_matches_reference():
+    if not pyoracle.available("reference"):
+        pytest.skip("oracle/_ref not built")
+    port, ref = pyoracle.load("port"), pyoracle.load("reference")
+    rng = np.random.default_rng(5)
+    for h, w in ((1, 1), (7, 9), (64, 48), (240, 320)):
+        for quant in (None, 0.25):
+            est = rng.normal(0, 3, (h, w))
+            gt = rng.normal(0, 3, (h, w))
+            if quant:
+                est, gt = np.round(est / quant) * quant, np.round(gt / quant) * quant  # ties
+            sig = np.abs(rng.normal(1, 1, (h, w)))
+            ev = (rng.random((h, w)) < 0.8).astype(np.uint8)
+            rv = (rng.random((h, w)) < 0.9).astype(np.uint8)
+            sv = (rng.random((h, w)) < 0.7).astype(np.uint8)
+            a = port.compute_metrics(est, ev, gt, rv, sig, sv)
+            b = ref.compute_metrics(est, ev, gt, rv, sig, sv)
+            for k in a:
+                assert (np.isnan(a[k]) and np.isnan(b[k])) or a[k] == b[k], (h, w, k)
