@@ -125,6 +125,12 @@ typedef struct pstereo_outputs {
    * for disparity alone). */
   int fill_invalid;
   double invalid_value;
+  /* Host output buffers only: when async_host != 0 the call returns once its
+   * work is queued; the host planes are complete after pstereo_gpu_wait (or
+   * a device synchronize). Consecutive calls then overlap (the next batch's
+   * uploads and kernels run under this batch's downloads). Ignored when
+   * stats or finest records are requested (those are finished on the host). */
+  int async_host;
 } pstereo_outputs;
 
 typedef struct pstereo_ctx pstereo_ctx;
@@ -201,6 +207,9 @@ int pstereo_gpu_metrics(pstereo_ctx* ctx, int n_frames, int width, int height,
                         const double* reference, const uint8_t* reference_valid,
                         const double* sigma, const uint8_t* sigma_valid,
                         int inputs_on_device, pstereo_frame_metrics* out, void* stream);
+
+/* Waits for every stream of the context and for `stream` (may be NULL). */
+int pstereo_gpu_wait(pstereo_ctx* ctx, void* stream);
 
 int pstereo_gpu_last_launch_count(const pstereo_ctx* ctx);
 

@@ -88,7 +88,7 @@ class _Outputs(C.Structure):
         ("match_disparity", C.c_void_p), ("match_valid", C.c_void_p), ("var_disp", C.c_void_p),
         ("stats", C.POINTER(LevelStats)), ("finest", C.POINTER(PatchEstimate)),
         ("finest_count", i32p), ("finest_cap", C.c_int), ("fill_invalid", C.c_int),
-        ("invalid_value", C.c_double),
+        ("invalid_value", C.c_double), ("async_host", C.c_int),
     ]
 
 
@@ -130,6 +130,7 @@ def lib() -> C.CDLL:
                                           C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                           C.c_void_p, C.c_int, C.POINTER(FrameMetricsC),
                                           C.c_void_p]
+        L.pstereo_gpu_wait.argtypes = [C.c_void_p, C.c_void_p]
         L.pstereo_validate.argtypes = [C.POINTER(_Params), C.c_char_p, C.c_size_t]
         L.pstereo_level_dims.argtypes = [C.POINTER(_Params), C.c_int, C.c_int, i32p, i32p,
                                          i32p, i32p]
@@ -176,7 +177,7 @@ ABI_SYMBOLS = [
     "pstereo_gpu_match_f32", "pstereo_gpu_last_launch_count", "pstereo_gpu_set_profiling",
     "pstereo_gpu_stage_times", "pstereo_gpu_stage_name", "pstereo_synth_default",
     "pstereo_synth_pair", "pstereo_synth_batch", "pstereo_debug_eval_residual",
-    "pstereo_gpu_metrics",
+    "pstereo_gpu_metrics", "pstereo_gpu_wait",
 ]
 
 
@@ -430,6 +431,12 @@ class Matcher:
         return res
 
     # ---- device-pointer batched API (the zero-copy path used by bench.py)
+    def wait(self, stream=None):
+        """pstereo_gpu_wait: every stream of the context (and `stream`) done."""
+        rc = lib().pstereo_gpu_wait(self._h, stream)
+        if rc:
+            _raise(rc, self.last_error())
+
     def metrics(self, estimate, estimate_valid, reference, reference_valid, sigma=None,
                 sigma_valid=None):
         """compute_metrics (src/metrics.cpp:10-52) on the GPU for [n,h,w] (or [h,w])
@@ -478,11 +485,14 @@ class Matcher:
             _raise(rc, self.last_error())
 
     def run_host_u8(self, n, width, height, channels, left_ptr, right_ptr, outputs: dict,
-                    dtype=F32, focal=1.0, baseline=1.0, stream=None, invalid_value=None):
-        """Host (ideally pinned) buffers in and out; H2D/D2H inside the call."""
+                    dtype=F32, focal=1.0, baseline=1.0, stream=None, invalid_value=None,
+                    async_host=False):
+        """Host (ideally pinned) buffers in and out; H2D/D2H inside the call.
+        async_host: return once queued; outputs complete after wait()."""
         o = _Outputs()
         o.dtype = dtype
         o.on_device = 0
+        o.async_host = int(bool(async_host))
         if invalid_value is not None:
             o.fill_invalid, o.invalid_value = 1, float(invalid_value)
         for k, ptr in outputs.items():

@@ -222,7 +222,12 @@ struct pstereo_ctx {
   DevBuf<uint8_t> full_valid[2];
   Scratch scr[2];  // [0]: the call's stream, [1]: the pipeline's second compute stream
   // staging for host outputs
-  DevBuf<uint8_t> out_stage[10];
+  DevBuf<uint8_t> out_stage[2][10];  // alternating per call (async host outputs)
+  // PSTEREO_DEBUG_TIMELINE=1: timed events at the pipeline's chunk boundaries,
+  // printed (ms from the first) by pstereo_gpu_wait -- a debugging aid
+  bool timeline = false;
+  std::vector<std::pair<std::string, cudaEvent_t>> tl;
+  int out_parity = 0;
   // host-buffer pipeline (chunked H2D / compute / D2H)
   int chunk_pairs = 0;
   cudaStream_t s_in = nullptr, s_out = nullptr, s_comp = nullptr;
@@ -404,6 +409,7 @@ int pstereo_gpu_create(int device, const pstereo_params* p, int max_width, int m
   }
   for (auto& sc : ctx->scr) sc.levels.resize(size_t(p->coarsest_exp) + 1);
   if (const char* v = getenv("PSTEREO_CHUNK_PAIRS")) ctx->chunk_pairs = atoi(v);
+  if (const char* v = getenv("PSTEREO_DEBUG_TIMELINE")) ctx->timeline = atoi(v) != 0;
   *out = ctx;
   return PSTEREO_OK;
 }
@@ -421,7 +427,8 @@ void pstereo_gpu_destroy(pstereo_ctx* ctx) {
   ctx->met_u8.release();
   ctx->met_keys.release();
   ctx->met_out.release();
-  for (auto& b : ctx->out_stage) b.release();
+  for (auto& set : ctx->out_stage)
+    for (auto& b : set) b.release();
   for (auto e : ctx->chunk_events) cudaEventDestroy(e);
   if (ctx->s_in) cudaStreamDestroy(ctx->s_in);
   if (ctx->s_out) cudaStreamDestroy(ctx->s_out);
@@ -438,6 +445,23 @@ const char* pstereo_gpu_last_error(const pstereo_ctx* ctx) {
 }
 
 int pstereo_gpu_last_launch_count(const pstereo_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int pstereo_gpu_wait(pstereo_ctx* ctx, void* stream) {
+  if (!ctx) return PSTEREO_EINTERNAL;
+  if (cudaSetDevice(ctx->device) != cudaSuccess) return fail(ctx, PSTEREO_EINTERNAL, "no device");
+  for (cudaStream_t t : {ctx->s_in, ctx->s_comp, ctx->s_out, ctx->stream, (cudaStream_t)stream})
+    if (t) CK(cudaStreamSynchronize(t));
+  if (!ctx->tl.empty()) {
+    for (auto& m : ctx->tl) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ctx->tl.front().second, m.second);
+      std::fprintf(stderr, "timeline %9.3f ms  %s\n", ms, m.first.c_str());
+    }
+    for (auto& m : ctx->tl) cudaEventDestroy(m.second);
+    ctx->tl.clear();
+  }
+  return PSTEREO_OK;
+}
 
 static_assert(sizeof(pstereo_frame_metrics) == sizeof(bdis::pstereo_frame_metrics_dev),
               "frame metrics layouts differ");
@@ -928,8 +952,8 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
   for (int q = 0; q < 10; ++q) {
     dev_out[q] = user_ptr[q];
     if (user_ptr[q] && host_out) {
-      CK(ctx->out_stage[q].ensure(size_t(n_full) * n * sizes[q]));
-      dev_out[q] = ctx->out_stage[q].p;
+      CK(ctx->out_stage[ctx->out_parity][q].ensure(size_t(n_full) * n * sizes[q]));
+      dev_out[q] = ctx->out_stage[ctx->out_parity][q].p;
     }
   }
   if (pipelined && !ctx->s_in) {
@@ -957,6 +981,13 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
   cudaEvent_t* ev = ctx->chunk_events.data();
   cudaEvent_t ev_start = ev[2 * n_chunks], ev_comp = ev[2 * n_chunks + 1],
               ev_out = ev[2 * n_chunks + 2];
+  auto mark = [&](const std::string& what, cudaStream_t t) {
+    if (!ctx->timeline) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, t);
+    ctx->tl.emplace_back(what, e);
+  };
   if (pipelined) {
     // the helper streams start behind the work already queued on the caller's stream
     CK(cudaEventRecord(ev_start, s));
@@ -987,6 +1018,7 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
         }
       }
       if (sc != cs) {
+        mark("h2d done c" + std::to_string(c), sc);
         CK(cudaEventRecord(ev[2 * c], sc));
         CK(cudaStreamWaitEvent(cs, ev[2 * c], 0));
       }
@@ -1017,12 +1049,15 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
                     cout, hc, cs);
     if (rc) return rc;
     if (host_out) {
+      mark("compute done c" + std::to_string(c) + (slot ? " (s2)" : " (s1)"), cs);
       CK(cudaEventRecord(ev[2 * c + 1], cs));
       CK(cudaStreamWaitEvent(ctx->s_out, ev[2 * c + 1], 0));
+      mark("d2h start c" + std::to_string(c), ctx->s_out);
       for (int q = 0; q < 10; ++q)
         if (user_ptr[q])
           CK(cudaMemcpyAsync((uint8_t*)user_ptr[q] + px0 * sizes[q], cout[q], pxc * sizes[q],
                              cudaMemcpyDeviceToHost, ctx->s_out));
+      mark("d2h done c" + std::to_string(c), ctx->s_out);
     }
   }
   // everything the call queued completes before later work on the caller's stream
@@ -1030,12 +1065,16 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
     CK(cudaEventRecord(ev_comp, ctx->s_comp));
     CK(cudaStreamWaitEvent(s, ev_comp, 0));
   }
+  // async host outputs: the downloads stay queued on s_out (staging sets
+  // alternate per call, so the next call's kernels never touch them)
+  const bool async = host_out && out->async_host && hstats.empty() && !want_finest;
   if (host_out) {
+    ctx->out_parity ^= 1;
     CK(cudaEventRecord(ev_out, ctx->s_out));
-    CK(cudaStreamWaitEvent(s, ev_out, 0));
+    if (!async) CK(cudaStreamWaitEvent(s, ev_out, 0));
   }
-  const bool need_sync = host_out || !hstats.empty() || want_finest;
-  if (host_out) CK(cudaStreamSynchronize(ctx->s_out));
+  const bool need_sync = !async && (host_out || !hstats.empty() || want_finest);
+  if (need_sync && host_out) CK(cudaStreamSynchronize(ctx->s_out));
   if (need_sync) CK(cudaStreamSynchronize(s));
   if (!hstats.empty()) {
     for (int p = 0; p < n; ++p)

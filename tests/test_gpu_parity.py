@@ -238,6 +238,35 @@ def test_chunked_host_pipeline(gpu, monkeypatch):
         assert np.array_equal(whole[k], parts[k]), k
 
 
+def test_async_host_calls_overlap_safely(gpu):
+    """async_host: back-to-back calls return once queued and overlap; after
+    wait() every host plane equals the synchronous result."""
+    import torch
+
+    P = gpu
+    n, w, h = 12, 160, 120
+    cfg = P.PipelineConfig(coarsest_exp=2, finest_exp=1, patch_size=8, overlap=0.5)
+    batches = [P.synth_batch(0, n, seed0=100 * k, width=w, height=h) for k in range(3)]
+    with P.Matcher(cfg, w, h, n) as m:
+        sync = []
+        for left, right in batches:
+            d = np.empty((n, h, w), np.float32)
+            m.run_host_u8(n, w, h, 1, left.ctypes.data, right.ctypes.data,
+                          {"disparity": d.ctypes.data}, invalid_value=float("nan"))
+            sync.append(d)
+        pinned = [(torch.from_numpy(l).pin_memory(), torch.from_numpy(r).pin_memory())
+                  for l, r in batches]
+        outs = [torch.empty((n, h, w), dtype=torch.float32).pin_memory() for _ in batches]
+        for (hl, hr), d in zip(pinned, outs):
+            m.run_host_u8(n, w, h, 1, hl.data_ptr(), hr.data_ptr(), {"disparity": d.data_ptr()},
+                          invalid_value=float("nan"), async_host=True)
+        m.wait()
+    for a, b in zip(sync, outs):
+        b = b.numpy()
+        assert np.array_equal(np.isnan(a), np.isnan(b))
+        assert np.array_equal(np.nan_to_num(a), np.nan_to_num(b))
+
+
 def test_invalid_value_fill(gpu):
     """fill_invalid writes the PFM-style sentinel (src/io.cpp:297-310) into
     invalid disparity/depth pixels and leaves valid ones untouched."""
