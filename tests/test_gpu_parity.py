@@ -2,6 +2,8 @@
 (oracle/bdis_oracle.c, itself pinned bit-exact to the reference build) on the
 same seeded inputs. Bit-exact except var_disp / depth sigma (1e-3 rel, see
 tests/parity.py)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -285,3 +287,40 @@ def test_invalid_value_fill(gpu):
         assert (b[plane][~v] == -1.0).all()
     assert np.array_equal(a["match_disparity"], b["match_disparity"])
     assert (~a["disparity_valid"].astype(bool)).any()
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("PSTEREO_RANDOM_CASES", "16"))))
+def test_randomized_configs(gpu, port, seed):
+    """Random valid PipelineConfigs and frame sizes (patch sizes 2..20, any
+    stride, 1..4 levels, window offsets, thresholds, variance on/off, gray or
+    RGB): bit-exact against the oracle every time."""
+    P = gpu
+    rng = np.random.default_rng(1000 + seed)
+    size = int(rng.integers(2, 21))
+    stride = int(rng.integers(1, size + 1))
+    fe = int(rng.integers(0, 2))
+    ce = fe + int(rng.integers(0, 4))
+    minw = size << ce
+    w = int(rng.integers(minw, minw + 120))
+    h = int(rng.integers(minw, minw + 90))
+    offs = sorted(set(float(x) for x in rng.choice([0.25, 0.5, 0.75, 1.0, 1.5, 2.0],
+                                                   size=int(rng.integers(1, 4)), replace=False)))
+    cfg = P.PipelineConfig(coarsest_exp=ce, finest_exp=fe, patch_size=size,
+                           overlap=1.0 - stride / size,
+                           min_iterations=int(rng.integers(1, 6)), max_iterations=12,
+                           window_offsets=offs,
+                           pixel_threshold=float(rng.uniform(0.05, 0.4)),
+                           gamma=float(rng.uniform(0.1, 1.0)),
+                           valid_patch_ratio=float(rng.uniform(0.5, 1.0)),
+                           estimate_variance=bool(rng.integers(0, 2)))
+    ch = int(rng.choice([1, 3, 4]))
+    l, r = P.synth_pair(0, seed=seed, width=w, height=h, channels=min(ch, 3),
+                        d_range=float(rng.uniform(2, 12)), d_min=float(rng.uniform(0, 3)))
+    if ch == 4:  # RGBA: alpha == 0 marks invalid pixels (src/image.cpp:32-34)
+        alpha = [np.full((h, w, 1), 255, np.uint8) for _ in range(2)]
+        for a in alpha:
+            a[rng.random((h, w)) < rng.uniform(0, 0.05)] = 0
+            y0, x0 = int(rng.integers(0, h)), int(rng.integers(0, w))
+            a[y0:y0 + int(rng.integers(1, h // 2 + 2)), x0:x0 + int(rng.integers(1, w // 2 + 2))] = 0
+        l, r = np.concatenate([l, alpha[0]], axis=2), np.concatenate([r, alpha[1]], axis=2)
+    _check(P, port, cfg, l[None], r[None])
