@@ -642,6 +642,10 @@ BandPlan plan_bands(const Level& L, const PatchParams& pp, int max_smem_per_cta)
   const size_t per_sm = size_t(max_smem_per_cta) / ctas - 1024;
   int rb = std::max(1, std::min(g.ny, (ppl10 * threads / 10 + g.nx / 2) / g.nx));
   while (rb > 1 && bytes_for(rb) > per_sm) --rb;
+  // small batches: a CTA's rounds are a latency chain, so spread the level
+  // over more, smaller bands until every SM has a CTA (single-frame latency)
+  const int sms = env("PSTEREO_SMS", 148);
+  while (rb > 1 && (long long)((g.ny + rb - 1) / rb) * pp.n_pairs < sms) --rb;
   bp.use_smem = bytes_for(rb) <= size_t(max_smem_per_cta);
   bp.rb = rb;
   bp.n_bands = (g.ny + rb - 1) / rb;
