@@ -559,6 +559,37 @@ __global__ void __launch_bounds__(kFuseThreads) k_fuse_ccl_local(
     }
   }
   __syncthreads();
+  const long long tid = pair * gridDim.x + tile;
+  const int full = 1 << cb.e;
+  // ---- dense tiles (every in-image pixel kept): one component rooted at the
+  // tile's first pixel -- no unions, no finds
+  bool mine_full = true;
+  const unsigned in_cols = wl >= 31 ? 0xffffffffu : ((2u << wl) - 1u);
+  for (int i = 0; i < kFuseRows; ++i) {
+    const int ly = warp + i * kFuseWarps;
+    mine_full = mine_full && s_bits[ly] == (ty0 + ly < h ? in_cols : 0u);
+  }
+  if (__syncthreads_and(mine_full)) {
+    const int root_gi = ty0 * w + tx0;
+    int a = 0;
+    for (int i = 0; i < kFuseRows; ++i) {
+      const int ly = warp + i * kFuseWarps, y = ty0 + ly;
+      if (y >= h || x >= w) continue;
+      cb.label[pbase + (long long)y * w + x] = root_gi;
+      a += min(full, cb.full_w - (x << cb.e)) * min(full, cb.full_h - (y << cb.e));
+    }
+    a = __reduce_add_sync(0xffffffffu, a);
+    if (t == 0) s_area[0] = 0;
+    __syncthreads();
+    if (lane == 0) atomicAdd(&s_area[0], a);
+    __syncthreads();
+    if (t == 0) {
+      cb.larea[pbase + root_gi] = s_area[0];
+      cb.roots[tid * kTilePx] = root_gi;
+      cb.nroots[tid] = 1;
+    }
+    return;
+  }
   // one union per column segment where a run overlaps the run above it
   volatile int* vl = sl;
   for (int i = 0; i < kFuseRows; ++i) {
@@ -592,7 +623,6 @@ __global__ void __launch_bounds__(kFuseThreads) k_fuse_ccl_local(
   }
   __syncthreads();
   // labels and run areas (weights: full-resolution pixels per finest pixel)
-  const int full = 1 << cb.e;
   for (int i = 0; i < kFuseRows; ++i) {
     const int ly = warp + i * kFuseWarps, y = ty0 + ly;
     const unsigned bits = s_bits[ly];
@@ -610,7 +640,6 @@ __global__ void __launch_bounds__(kFuseThreads) k_fuse_ccl_local(
     }
   }
   __syncthreads();
-  const long long tid = pair * gridDim.x + tile;
   for (int i = 0; i < kFuseRows; ++i) {
     const int ly = warp + i * kFuseWarps;
     const int idx = ly * kTileW + lane;
