@@ -563,11 +563,16 @@ __global__ void __launch_bounds__(kFuseThreads) k_fuse_ccl_local(
   const int full = 1 << cb.e;
   // ---- dense tiles (every in-image pixel kept): one component rooted at the
   // tile's first pixel -- no unions, no finds
-  bool mine_full = true;
+  bool mine_full = true, mine_empty = true;
   const unsigned in_cols = wl >= 31 ? 0xffffffffu : ((2u << wl) - 1u);
   for (int i = 0; i < kFuseRows; ++i) {
     const int ly = warp + i * kFuseWarps;
     mine_full = mine_full && s_bits[ly] == (ty0 + ly < h ? in_cols : 0u);
+    mine_empty = mine_empty && s_bits[ly] == 0u;
+  }
+  if (__syncthreads_and(mine_empty)) {  // nothing kept: no components
+    if (t == 0) cb.nroots[tid] = 0;
+    return;
   }
   if (__syncthreads_and(mine_full)) {
     const int root_gi = ty0 * w + tx0;
