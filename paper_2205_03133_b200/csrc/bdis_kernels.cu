@@ -148,7 +148,6 @@ __device__ __forceinline__ float down4(float a, float b, float c, float d) {
 template <bool kU8>
 __global__ void __launch_bounds__(256) k_pyramid(PyrArgs a) {
   extern __shared__ __align__(16) float sbuf[];
-  const int band = blockIdx.x;
   const long long pair = blockIdx.y;
   const int tid = threadIdx.x, nt = blockDim.x;
   const int ce = a.ce, fe = a.fe;
@@ -220,91 +219,96 @@ __global__ void __launch_bounds__(256) k_pyramid(PyrArgs a) {
       if (x == w - 1) rp[w] = rv;
     }
   };
-  // ---- level 0 rows of the band (stored only when finest_exp == 0)
-  if (fe == 0) {
-    const int r0 = band << ce, r1 = min(r0 + (1 << ce), a.H);
-    const int W = a.W;
-    const long long pl = pair * (long long)W * a.H, pr = pair * (long long)(W + 1) * a.H;
-    for (int q = tid; q < (r1 - r0) * W; q += nt) {
-      const int y = r0 + q / W, x = q % W;
-      const float l = src_px<kU8>(a, lut, 0, pair, x, y);
-      float g = 0.0f;
-      if (W >= 2) {
-        if (x == 0) g = __fsub_rn(src_px<kU8>(a, lut, 0, pair, 1, y), l);
-        else if (x == W - 1) g = __fsub_rn(l, src_px<kU8>(a, lut, 0, pair, W - 2, y));
-        else g = __fmul_rn(0.5f, __fsub_rn(src_px<kU8>(a, lut, 0, pair, x + 1, y),
-                                           src_px<kU8>(a, lut, 0, pair, x - 1, y)));
-      }
-      const long long o = pl + (long long)y * W + x;
-      a.L[0][o] = l;
-      a.G[0][o] = g;
-      const float rv = src_px<kU8>(a, lut, 1, pair, x, y);
-      float* rp = a.Rp[0] + pr + (long long)y * (W + 1);
-      rp[x] = rv;
-      if (x == W - 1) rp[W] = rv;
-    }
-  }
-  if (ce == 0) return;
-  // ---- level 1 from the source
-  {
-    const int w = a.ws[1], h = a.hs[1];
-    const int y0 = band << (ce - 1), rows = min(1 << (ce - 1), h - y0);
-    float* Lb = buf[0];
-    float* Rb = buf[0] + a.buf_floats;
-    if (kU8 && a.vec8) {
-      // gray rasters, W % 8 == 0, even H: 8 source bytes of two rows per view
-      // give 4 level-1 pixels (down4 of the grayscale values, as below)
-      const int qw = w >> 2;
-      for (int q = tid; q < rows * qw; q += nt) {
-        const int r = q / qw, xq = q - r * qw;
-        const long long base = pair * (long long)a.W * a.H + (long long)(2 * (y0 + r)) * a.W + 8 * xq;
-#pragma unroll
-        for (int v = 0; v < 2; ++v) {
-          const uint8_t* src = (v ? a.u8r : a.u8l) + base;
-          const uint2 t = __ldg((const uint2*)src);
-          const uint2 b = __ldg((const uint2*)(src + a.W));
-          const unsigned tw[2] = {t.x, t.y}, bw[2] = {b.x, b.y};
-          float o[4];
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const unsigned ts = tw[k >> 1] >> (16 * (k & 1)), bs = bw[k >> 1] >> (16 * (k & 1));
-            o[k] = down4(g1[ts & 255u], g1[(ts >> 8) & 255u], g1[bs & 255u], g1[(bs >> 8) & 255u]);
-          }
-          *(float4*)((v ? Rb : Lb) + r * w + 4 * xq) = make_float4(o[0], o[1], o[2], o[3]);
+  // several bands per CTA (grid-stride): amortises the LUT set-up and keeps
+  // every thread busy at the narrow coarse levels
+  for (int band = blockIdx.x; band < a.hs[a.ce]; band += gridDim.x) {
+    if (band != (int)blockIdx.x) __syncthreads();  // level buffers are reused
+    // ---- level 0 rows of the band (stored only when finest_exp == 0)
+    if (fe == 0) {
+      const int r0 = band << ce, r1 = min(r0 + (1 << ce), a.H);
+      const int W = a.W;
+      const long long pl = pair * (long long)W * a.H, pr = pair * (long long)(W + 1) * a.H;
+      for (int q = tid; q < (r1 - r0) * W; q += nt) {
+        const int y = r0 + q / W, x = q % W;
+        const float l = src_px<kU8>(a, lut, 0, pair, x, y);
+        float g = 0.0f;
+        if (W >= 2) {
+          if (x == 0) g = __fsub_rn(src_px<kU8>(a, lut, 0, pair, 1, y), l);
+          else if (x == W - 1) g = __fsub_rn(l, src_px<kU8>(a, lut, 0, pair, W - 2, y));
+          else g = __fmul_rn(0.5f, __fsub_rn(src_px<kU8>(a, lut, 0, pair, x + 1, y),
+                                             src_px<kU8>(a, lut, 0, pair, x - 1, y)));
         }
+        const long long o = pl + (long long)y * W + x;
+        a.L[0][o] = l;
+        a.G[0][o] = g;
+        const float rv = src_px<kU8>(a, lut, 1, pair, x, y);
+        float* rp = a.Rp[0] + pr + (long long)y * (W + 1);
+        rp[x] = rv;
+        if (x == W - 1) rp[W] = rv;
       }
-    } else
-    for (int q = tid; q < rows * w; q += nt) {
-      const int y = y0 + q / w, x = q % w;
-      const int sx0 = 2 * x, sx1 = min(2 * x + 1, a.W - 1);
-      const int sy0 = 2 * y, sy1 = min(2 * y + 1, a.H - 1);
-      Lb[q] = down4(src_px<kU8>(a, lut, 0, pair, sx0, sy0), src_px<kU8>(a, lut, 0, pair, sx1, sy0),
-                    src_px<kU8>(a, lut, 0, pair, sx0, sy1), src_px<kU8>(a, lut, 0, pair, sx1, sy1));
-      Rb[q] = down4(src_px<kU8>(a, lut, 1, pair, sx0, sy0), src_px<kU8>(a, lut, 1, pair, sx1, sy0),
-                    src_px<kU8>(a, lut, 1, pair, sx0, sy1), src_px<kU8>(a, lut, 1, pair, sx1, sy1));
     }
-    __syncthreads();
-    if (1 >= fe) store(1, y0, rows, Lb, Rb);
-  }
-  // ---- levels 2..ce from the previous level in shared memory
-  for (int e = 2; e <= ce; ++e) {
-    const int pw = a.ws[e - 1], ph = a.hs[e - 1];
-    const int py0 = band << (ce - e + 1);
-    const float* PL = buf[(e - 2) & 1];
-    const float* PR = PL + a.buf_floats;
-    const int w = a.ws[e], h = a.hs[e];
-    const int y0 = band << (ce - e), rows = min(1 << (ce - e), h - y0);
-    float* Lb = buf[(e - 1) & 1];
-    float* Rb = Lb + a.buf_floats;
-    for (int q = tid; q < rows * w; q += nt) {
-      const int y = y0 + q / w, x = q % w;
-      const int x0 = 2 * x, x1 = min(2 * x + 1, pw - 1);
-      const int r0 = 2 * y - py0, r1 = min(2 * y + 1, ph - 1) - py0;
-      Lb[q] = down4(PL[r0 * pw + x0], PL[r0 * pw + x1], PL[r1 * pw + x0], PL[r1 * pw + x1]);
-      Rb[q] = down4(PR[r0 * pw + x0], PR[r0 * pw + x1], PR[r1 * pw + x0], PR[r1 * pw + x1]);
+    if (ce == 0) continue;
+    // ---- level 1 from the source
+    {
+      const int w = a.ws[1], h = a.hs[1];
+      const int y0 = band << (ce - 1), rows = min(1 << (ce - 1), h - y0);
+      float* Lb = buf[0];
+      float* Rb = buf[0] + a.buf_floats;
+      if (kU8 && a.vec8) {
+        // gray rasters, W % 8 == 0, even H: 8 source bytes of two rows per view
+        // give 4 level-1 pixels (down4 of the grayscale values, as below)
+        const int qw = w >> 2;
+        for (int q = tid; q < rows * qw; q += nt) {
+          const int r = q / qw, xq = q - r * qw;
+          const long long base = pair * (long long)a.W * a.H + (long long)(2 * (y0 + r)) * a.W + 8 * xq;
+  #pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            const uint8_t* src = (v ? a.u8r : a.u8l) + base;
+            const uint2 t = __ldg((const uint2*)src);
+            const uint2 b = __ldg((const uint2*)(src + a.W));
+            const unsigned tw[2] = {t.x, t.y}, bw[2] = {b.x, b.y};
+            float o[4];
+  #pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const unsigned ts = tw[k >> 1] >> (16 * (k & 1)), bs = bw[k >> 1] >> (16 * (k & 1));
+              o[k] = down4(g1[ts & 255u], g1[(ts >> 8) & 255u], g1[bs & 255u], g1[(bs >> 8) & 255u]);
+            }
+            *(float4*)((v ? Rb : Lb) + r * w + 4 * xq) = make_float4(o[0], o[1], o[2], o[3]);
+          }
+        }
+      } else
+      for (int q = tid; q < rows * w; q += nt) {
+        const int y = y0 + q / w, x = q % w;
+        const int sx0 = 2 * x, sx1 = min(2 * x + 1, a.W - 1);
+        const int sy0 = 2 * y, sy1 = min(2 * y + 1, a.H - 1);
+        Lb[q] = down4(src_px<kU8>(a, lut, 0, pair, sx0, sy0), src_px<kU8>(a, lut, 0, pair, sx1, sy0),
+                      src_px<kU8>(a, lut, 0, pair, sx0, sy1), src_px<kU8>(a, lut, 0, pair, sx1, sy1));
+        Rb[q] = down4(src_px<kU8>(a, lut, 1, pair, sx0, sy0), src_px<kU8>(a, lut, 1, pair, sx1, sy0),
+                      src_px<kU8>(a, lut, 1, pair, sx0, sy1), src_px<kU8>(a, lut, 1, pair, sx1, sy1));
+      }
+      __syncthreads();
+      if (1 >= fe) store(1, y0, rows, Lb, Rb);
     }
-    __syncthreads();
-    if (e >= fe) store(e, y0, rows, Lb, Rb);
+    // ---- levels 2..ce from the previous level in shared memory
+    for (int e = 2; e <= ce; ++e) {
+      const int pw = a.ws[e - 1], ph = a.hs[e - 1];
+      const int py0 = band << (ce - e + 1);
+      const float* PL = buf[(e - 2) & 1];
+      const float* PR = PL + a.buf_floats;
+      const int w = a.ws[e], h = a.hs[e];
+      const int y0 = band << (ce - e), rows = min(1 << (ce - e), h - y0);
+      float* Lb = buf[(e - 1) & 1];
+      float* Rb = Lb + a.buf_floats;
+      for (int q = tid; q < rows * w; q += nt) {
+        const int y = y0 + q / w, x = q % w;
+        const int x0 = 2 * x, x1 = min(2 * x + 1, pw - 1);
+        const int r0 = 2 * y - py0, r1 = min(2 * y + 1, ph - 1) - py0;
+        Lb[q] = down4(PL[r0 * pw + x0], PL[r0 * pw + x1], PL[r1 * pw + x0], PL[r1 * pw + x1]);
+        Rb[q] = down4(PR[r0 * pw + x0], PR[r0 * pw + x1], PR[r1 * pw + x0], PR[r1 * pw + x1]);
+      }
+      __syncthreads();
+      if (e >= fe) store(e, y0, rows, Lb, Rb);
+    }
   }
 }
 
@@ -315,7 +319,7 @@ size_t pyramid_smem_bytes(const PyrArgs& a) {
 
 cudaError_t launch_pyramid(const PyrArgs& a, bool u8, cudaStream_t s) {
   const size_t smem = pyramid_smem_bytes(a);
-  dim3 grid(a.hs[a.ce], a.n_pairs);
+  dim3 grid((a.hs[a.ce] + 1) / 2, a.n_pairs);  // two bands per CTA
   if (u8) {
     cudaFuncSetAttribute(k_pyramid<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_pyramid<true><<<grid, 256, smem, s>>>(a);
