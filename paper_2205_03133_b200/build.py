@@ -19,7 +19,7 @@ CSRC = PKG / "csrc"
 LIB = PKG / "libpstereo_gpu.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-CUDA_SOURCES = ["bdis_kernels.cu", "bdis_patches.cu", "bdis_patches_rt.cu", "bdis_metrics.cu", "bdis_capi.cu"]
+CUDA_SOURCES = ["bdis_kernels.cu", "bdis_patches.cu", "bdis_metrics.cu", "bdis_capi.cu"]
 C_SOURCES = ["synth.c"]
 HEADERS = ["bdis_device.cuh", "bdis_kernels.h"]
 

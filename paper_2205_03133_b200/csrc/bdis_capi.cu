@@ -771,13 +771,8 @@ int run_device(pstereo_ctx* ctx, Scratch& sc, const std::vector<LevelGeom>& geo,
     pp.want_var = prm.estimate_variance && lv[li].e == fe;
     pp.have_prev = li > 0;
     const Level& P = li > 0 ? lv[li - 1] : lv[li];
-    BandPlan bp;
-    if (plan_bands_rt(lv[li], pp, ctx->max_smem, &bp)) {
-      CK(launch_patches_rt(lv[li], P, pp, bp, s));
-    } else {
-      bp = plan_bands(lv[li], pp, ctx->max_smem);
-      CK(launch_patches(lv[li], P, pp, bp, s));
-    }
+    const BandPlan bp = plan_bands(lv[li], pp, ctx->max_smem);
+    CK(launch_patches(lv[li], P, pp, bp, s));
     ++ctx->launches;
     CK(mark());
   }

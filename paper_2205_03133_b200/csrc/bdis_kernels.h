@@ -35,7 +35,6 @@ struct BandPlan {
   int fpitch;      // smem slots per left/gradient row (floats)
   int bpitch;      // bytes per validity row
   int use_smem;    // 0: read the level tables from global memory
-  int r64;         // right rows staged as fp64 (else fp32, converted per tap)
   int rpad;        // zero slots either side of a staged right row (= patch size)
   size_t smem_bytes;
   int npb;         // max patches per band = rb * nx
@@ -43,11 +42,6 @@ struct BandPlan {
 
 // Shared-memory layout of one k_patches CTA (byte offsets), shared by the
 // host planner and the kernel.
-// k_patches shared rows: padded (x + x/32 slots against stride-4 bank
-// conflicts) or plain (immediate tap offsets, 16-byte template loads)
-constexpr bool kPadRows = true;  // left / gradient rows
-constexpr bool kPadRight = true;  // right rows (taps at data-dependent x - u)
-
 struct BandLayout {
   size_t oR, oL, oG, oLQ, oRQ;
   size_t oMean, oHess, oTmsq, oU, oWres;
@@ -58,8 +52,7 @@ struct BandLayout {
 };
 
 __host__ __device__ inline BandLayout band_layout(int rows, int rpitch, int fpitch, int bpitch,
-                                                  int npb, int nwin, bool valid, bool r64,
-                                                  int nslots) {
+                                                  int npb, int nwin, bool valid, int nslots) {
   BandLayout l;
   size_t o = 0;
   auto take = [&](size_t bytes, size_t align) {
@@ -68,7 +61,7 @@ __host__ __device__ inline BandLayout band_layout(int rows, int rpitch, int fpit
     o += bytes;
     return r;
   };
-  l.oR = take(size_t(rows) * rpitch * (r64 ? 8 : 4), 16);
+  l.oR = take(size_t(rows) * rpitch * 4, 16);
   l.oL = take(size_t(rows) * fpitch * 4, 16);
   l.oG = take(size_t(rows) * fpitch * 4, 16);
   l.oLQ = take(valid ? size_t(rows) * bpitch : 0, 16);
@@ -94,10 +87,6 @@ __host__ __device__ inline BandLayout band_layout(int rows, int rpitch, int fpit
 }
 
 BandPlan plan_bands(const Level& L, const PatchParams& pp, int max_smem_per_cta);
-// register-template variant for 8x8 patches of fully valid inputs (bdis_patches_rt.cu)
-bool plan_bands_rt(const Level& L, const PatchParams& pp, int max_smem_per_cta, BandPlan* out);
-cudaError_t launch_patches_rt(const Level& L, const Level& P, const PatchParams& pp,
-                              const BandPlan& bp, cudaStream_t s);
 
 // Fused pyramid (all-valid inputs): levels are indexed by exponent.
 struct PyrArgs {

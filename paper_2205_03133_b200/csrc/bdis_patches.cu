@@ -8,21 +8,20 @@
 //
 // B200 mapping
 //   * one CTA per (pair, band of `rb` patch rows); the band's rows of the
-//     right view (converted to fp64 once), left view and gradient (fp32) are
-//     staged in shared memory, padded (x + x/16 for 8-byte, x + x/32 for
-//     4-byte slots) so the stride-`stride` accesses of neighbouring patches hit
-//     distinct banks;
+//     right view, left view and gradient (fp32) are staged in shared memory,
+//     padded (slot x + x/32) so the stride-`stride` accesses of neighbouring
+//     patches hit distinct banks;
 //   * a thread owns one patch at a time and sums its samples in the
 //     reference's sequential row-major order -- that is what makes every sum
 //     bit-identical to the CPU (a warp tree reduction would reorder them);
 //   * phases: (1) balanced setup of every band patch (extract, Hessian, u0
-//     gather from the coarser level's records); (2) persistent lanes: each
-//     lane runs one residual evaluation per loop trip for its current patch
-//     -- an LK iteration or one of the window samples -- and takes the next
-//     patch from the CTA's pool when it is done, so the 1..12 iteration spread
-//     between patches costs no lockstep waiting and there is no barrier until
-//     the pool is drained; (3) balanced finish (posterior, local-minimum test,
-//     inherited probability, variance fit, records);
+//     gather from the coarser level's records); (2) rounds of one residual
+//     evaluation per busy lane: running LK solves packed into the lowest slots
+//     and refilled from the CTA's pool, the remaining lanes taking window
+//     samples of patches that converged in earlier rounds -- a long solve
+//     keeps one warp busy, not a quarter of every warp; (3) balanced finish
+//     (posterior, local-minimum test, inherited probability, variance fit,
+//     records);
 //   * the right-sample position x = (cx + offset(i)) - u of column i does not
 //     depend on the row, so each evaluation computes the exact per-column
 //     truncation x0_i and weight fx_i once (s conversions instead of s*s) and
@@ -49,29 +48,25 @@ struct Ev {
   int n;
 };
 
-template <bool kSmem, bool kR64 = false>
+template <bool kSmem>
 struct Rows {
-  // right view rows: in shared memory fp64 (kR64: converted once at staging)
-  // or fp32; fp32 rows of (w+1) in global. Unpadded (kPadRows == false): tap
-  // i of a row sits at a per-row base + i, so its address is an immediate
-  // offset, and the template rows load as 16-byte vectors.
-  using RT = typename std::conditional<kSmem && kR64, double, float>::type;
-  const RT* R;
+  // fp32 rows in shared memory, padded (slot x + x/32: neighbouring patches
+  // read columns 4 apart, which unpadded is a 4-way bank conflict), or the
+  // level planes in global memory (right view as rows of w+1).
+  const float* R;    // right view
   const float* Lf;   // left view
   const float* Gf;   // gradient of the left view
   const uint8_t* lq; // 4-tap validity (kValid only)
   const uint8_t* rq;
   int rp, fp, bp;    // row pitches (slots)
-  __device__ __forceinline__ static int s4(int x) { return (kSmem && kPadRows) ? x + (x >> 5) : x; }
-  __device__ __forceinline__ static int s8(int x) {
-    return !(kSmem && kPadRight) ? x : (kR64 ? x + (x >> 4) : x + (x >> 5));
-  }
+  __device__ __forceinline__ static int s4(int x) { return kSmem ? x + (x >> 5) : x; }
+  __device__ __forceinline__ static int s8(int x) { return s4(x); }
 };
 
 // eval_patch_residual (src/lk_solver.cpp:38-81) of a lattice patch whose
 // footprint starts at column x0 and row r0 of `rw`, at disparity u.
-template <int S, bool kSmem, bool kValid, bool kR64, bool kJr = true>
-__device__ __forceinline__ Ev eval_patch(const Rows<kSmem, kR64>& rw, int w, int s_rt, int x0,
+template <int S, bool kSmem, bool kValid, bool kJr = true>
+__device__ __forceinline__ Ev eval_patch(const Rows<kSmem>& rw, int w, int s_rt, int x0,
                                          int r0, int rpad, double mean, double u) {
   constexpr int SA = S > 0 ? S : kMaxPatch;
   const int s = S > 0 ? S : s_rt;
@@ -147,8 +142,8 @@ __device__ __forceinline__ Ev eval_patch(const Rows<kSmem, kR64>& rw, int w, int
     auto pass2 = [&](auto masked) {
       constexpr bool kMask = decltype(masked)::value;
       const auto* rr = rw.R + r0 * rw.rp;
-      const float* lr = rw.Lf + r0 * rw.fp + (kPadRows ? 0 : x0);
-      const float* gr = rw.Gf + r0 * rw.fp + (kPadRows ? 0 : x0);
+      const float* lr = rw.Lf + r0 * rw.fp;
+      const float* gr = rw.Gf + r0 * rw.fp;
 #pragma unroll 1
       for (int j = 0; j < SA; ++j, rr += rw.rp, lr += rw.fp, gr += rw.fp) {
         double a = (double)rr[rw.s8(xb)];
@@ -157,12 +152,12 @@ __device__ __forceinline__ Ev eval_patch(const Rows<kSmem, kR64>& rw, int w, int
           const double b = (double)rr[rw.s8(xb + i + 1)];
           const double v = __dadd_rn(__dmul_rn(mo[i], a), __dmul_rn(mf[i], b));
           a = b;
-          const double t = __dsub_rn((double)lr[kPadRows ? offT[i] : i], mean);
+          const double t = __dsub_rn((double)lr[offT[i]], mean);
           double r = __dsub_rn(__dsub_rn(v, rmean), t);
           // masked columns: r * 0 = +-0 adds nothing to ssr / jr
           if (kMask) r = __dmul_rn(r, mk[i]);
           ssr = __dadd_rn(ssr, __dmul_rn(r, r));
-          if (kJr) jr = __dadd_rn(jr, __dmul_rn((double)gr[kPadRows ? offT[i] : i], r));
+          if (kJr) jr = __dadd_rn(jr, __dmul_rn((double)gr[offT[i]], r));
         }
       }
     };
@@ -235,7 +230,7 @@ __device__ __forceinline__ Ev eval_patch(const Rows<kSmem, kR64>& rw, int w, int
 }  // namespace
 
 
-template <int S, bool kSmem, bool kValid, bool kR64>
+template <int S, bool kSmem, bool kValid>
 __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams pp, BandPlan bp) {
   extern __shared__ __align__(16) unsigned char smem[];
   const Grid& g = L.g;
@@ -254,9 +249,8 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
 
   // ---- shared-memory carve-up (mirrors band_layout on the host)
   const BandLayout lay = band_layout(bp.use_smem ? bp.smem_rows : 0, bp.rpitch, bp.fpitch,
-                                     bp.bpitch, bp.npb, nwin, kValid, kR64, bp.threads);
-  using RT = typename Rows<kSmem, kR64>::RT;
-  RT* sR = (RT*)(smem + lay.oR);
+                                     bp.bpitch, bp.npb, nwin, kValid, bp.threads);
+  float* sR = (float*)(smem + lay.oR);
   const int rpad = kSmem ? bp.rpad : 0;
   float* sL = (float*)(smem + lay.oL);
   float* sG = (float*)(smem + lay.oG);
@@ -280,7 +274,7 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
   uint8_t* st_wok = smem + lay.oWok;
 
   const long long pbase = pair * L.plane;
-  Rows<kSmem, kR64> rw;
+  Rows<kSmem> rw;
   int rofs;  // row index of image row y in rw is y - rofs
   if constexpr (kSmem) {
     // ---- stage the band (coalesced global reads, padded shared writes)
@@ -290,8 +284,8 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
 #pragma unroll 4
     for (int q = tid; q < nrows * rw2; q += nt) {
       const int r = q / rw2, x = q - r * rw2 - rpad;
-      sR[r * bp.rpitch + Rows<true, kR64>::s8(x + rpad)] =
-          (x >= 0 && x <= w) ? (RT)__ldg(gR + (long long)r * (w + 1) + x) : (RT)0;
+      sR[r * bp.rpitch + Rows<true>::s8(x + rpad)] =
+          (x >= 0 && x <= w) ? __ldg(gR + (long long)r * (w + 1) + x) : 0.0f;
     }
     const float* gl0 = L.left + pbase + (long long)ylo * w;
     const float* gg0 = L.grad + pbase + (long long)ylo * w;
@@ -448,9 +442,9 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
       if (busy) {
         // one code path per warp for both kinds of job: a warp costs one evaluation
         const int ex0 = col_start(p % g.nx), er0 = row_start(ky0 + p / g.nx) - rofs;
-        const Ev ev = warp_lk ? eval_patch<S, kSmem, kValid, kR64, true>(rw, w, s, ex0, er0, rpad,
+        const Ev ev = warp_lk ? eval_patch<S, kSmem, kValid, true>(rw, w, s, ex0, er0, rpad,
                                                                          st_mean[p], ue)
-                              : eval_patch<S, kSmem, kValid, kR64, false>(rw, w, s, ex0, er0, rpad,
+                              : eval_patch<S, kSmem, kValid, false>(rw, w, s, ex0, er0, rpad,
                                                                           st_mean[p], ue);
         if (!lk) {
           // sample_window: valid iff every template pixel was sampled (:31-36)
@@ -611,7 +605,6 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
 // ---------------------------------------------------------------------------
 
 static inline int pad4_host(int x) { return x + (x >> 5); }
-static inline int pad8_host(int x) { return x + (x >> 4); }
 
 BandPlan plan_bands(const Level& L, const PatchParams& pp, int max_smem_per_cta) {
   const Grid& g = L.g;
@@ -621,18 +614,15 @@ BandPlan plan_bands(const Level& L, const PatchParams& pp, int max_smem_per_cta)
     const char* v = getenv(k);
     return v ? atoi(v) : d;
   };
-  bp.r64 = env("PSTEREO_TUNE_R64", 0);
   bp.rpad = g.size;
-  bp.rpitch = kPadRight ? (bp.r64 ? pad8_host(L.w + 2 * bp.rpad) : pad4_host(L.w + 2 * bp.rpad)) + 1
-                        : L.w + 1 + 2 * bp.rpad;  // x in [-rpad, w + rpad]
-  bp.fpitch = kPadRows ? (L.w - 1 + ((L.w - 1) >> 5)) + 1  // slots for x in [0, w-1]
-                       : (L.w + 3) / 4 * 4;                // 16-byte aligned rows
+  bp.rpitch = pad4_host(L.w + 2 * bp.rpad) + 1;  // x in [-rpad, w + rpad]
+  bp.fpitch = pad4_host(L.w - 1) + 1;            // x in [0, w - 1]
   bp.bpitch = valid ? L.w : 0;
   const int threads = env("PSTEREO_TUNE_THREADS", 192);
   auto bytes_for = [&](int rb) {
     const int rows = (rb - 1) * g.stride + g.size;
     return band_layout(rows, bp.rpitch, bp.fpitch, bp.bpitch, rb * g.nx, pp.nwin, valid,
-                       bp.r64, threads).total;
+                       threads).total;
   };
   // up to ~2 patches per slot of a 192-thread CTA, while two CTAs fit an SM
   // (measured best of a T x ppl x CTAs sweep at the bench workload;
@@ -653,7 +643,7 @@ BandPlan plan_bands(const Level& L, const PatchParams& pp, int max_smem_per_cta)
   bp.smem_rows = (rb - 1) * g.stride + g.size;
   bp.smem_bytes = bp.use_smem ? bytes_for(rb)
                               : band_layout(0, bp.rpitch, bp.fpitch, bp.bpitch, bp.npb, pp.nwin,
-                                            valid, bp.r64, threads).total;
+                                            valid, threads).total;
   bp.threads = std::min(threads, std::max(32, ((bp.npb + 31) / 32) * 32));
   return bp;
 }
@@ -661,7 +651,7 @@ BandPlan plan_bands(const Level& L, const PatchParams& pp, int max_smem_per_cta)
 template <int S, bool kSmem, bool kValid>
 static cudaError_t launch_t(const Level& L, const Level& P, const PatchParams& pp,
                             const BandPlan& bp, cudaStream_t s) {
-  auto kern = (kSmem && bp.r64) ? k_patches<S, kSmem, kValid, true> : k_patches<S, kSmem, kValid, false>;
+  auto kern = k_patches<S, kSmem, kValid>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)bp.smem_bytes);
   if (e != cudaSuccess) return e;
@@ -721,7 +711,7 @@ __global__ void k_debug_eval(Level L, int size, int nq, const int* __restrict__ 
       ++cnt;
     }
   const double mean = cnt ? __ddiv_rn(sum, (double)cnt) : 0.0;
-  const Ev ev = eval_patch<0, false, kValid, false>(rw, L.w, size, x0, y0, 0, mean, qu[q]);
+  const Ev ev = eval_patch<0, false, kValid>(rw, L.w, size, x0, y0, 0, mean, qu[q]);
   msq[q] = ev.msq;
   jr[q] = ev.jr;
   n[q] = ev.n;
