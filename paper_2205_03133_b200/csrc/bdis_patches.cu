@@ -43,6 +43,14 @@ namespace bdis {
 
 namespace {
 
+__device__ __forceinline__ void cp_async4(void* smem_dst, const void* gsrc) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+}
+
 struct Ev {
   double msq, jr;
   int n;
@@ -281,20 +289,24 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
     const float* gR = L.rpad + pair * (long long)(w + 1) * h + (long long)ylo * (w + 1);
     // right rows with rpad zero slots either side (x in [-rpad, w + rpad])
     const int rw2 = w + 1 + 2 * rpad;
+    // asynchronous copies (cp.async): every thread queues all of its
+    // elements before waiting once, instead of a few loads in flight
 #pragma unroll 4
     for (int q = tid; q < nrows * rw2; q += nt) {
       const int r = q / rw2, x = q - r * rw2 - rpad;
-      sR[r * bp.rpitch + Rows<true>::s8(x + rpad)] =
-          (x >= 0 && x <= w) ? __ldg(gR + (long long)r * (w + 1) + x) : 0.0f;
+      float* dst = sR + r * bp.rpitch + Rows<true>::s8(x + rpad);
+      if (x >= 0 && x <= w) cp_async4(dst, gR + (long long)r * (w + 1) + x);
+      else *dst = 0.0f;
     }
     const float* gl0 = L.left + pbase + (long long)ylo * w;
     const float* gg0 = L.grad + pbase + (long long)ylo * w;
 #pragma unroll 4
     for (int q = tid; q < nrows * w; q += nt) {
       const int r = q / w, x = q - r * w;
-      sL[r * bp.fpitch + Rows<true>::s4(x)] = __ldg(gl0 + q);
-      sG[r * bp.fpitch + Rows<true>::s4(x)] = __ldg(gg0 + q);
+      cp_async4(sL + r * bp.fpitch + Rows<true>::s4(x), gl0 + q);
+      cp_async4(sG + r * bp.fpitch + Rows<true>::s4(x), gg0 + q);
     }
+    cp_async_wait_all();
     for (int r = 0; r < nrows; ++r) {
       if (kValid) {
         const uint8_t* lq = L.lq + pbase + (long long)(ylo + r) * w;
