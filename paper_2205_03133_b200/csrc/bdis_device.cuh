@@ -110,8 +110,11 @@ __device__ __forceinline__ Fused gather_cover(const Grid& g, const Rec& rec, int
                                               const double* __restrict__ mask) {
   const int s = g.size, st = g.stride;
   Fused f{0.0, 0.0, 0.0, 0.0};
+  // fuse_level visits accepted patches only (src/coarse_to_fine.cpp:120-135);
+  // the records of the others hold prob = u = sigma = 0 (k_patches phase 3),
+  // so they add w = +0.0, which leaves every sum bit-identical (the sums start
+  // at +0.0 and never become -0.0) -- no dependent stage load
   auto add = [&](int ky, int kx, double m) {
-    if (rec.stage(ky, kx) != kAccepted) return;
     const double pr = rec.prob(ky, kx);
     const double w = __dmul_rn(pr, m);
     f.sw = __dadd_rn(f.sw, w);
