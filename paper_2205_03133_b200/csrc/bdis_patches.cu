@@ -630,7 +630,7 @@ BandPlan plan_bands(const Level& L, const PatchParams& pp, int max_smem_per_cta)
   bp.rpitch = pad4_host(L.w + 2 * bp.rpad) + 1;  // x in [-rpad, w + rpad]
   bp.fpitch = pad4_host(L.w - 1) + 1;            // x in [0, w - 1]
   bp.bpitch = valid ? L.w : 0;
-  const int threads = env("PSTEREO_TUNE_THREADS", 192);
+  const int threads = env("PSTEREO_TUNE_THREADS", g.nx < 60 ? 256 : 192);  // measured per width
   auto bytes_for = [&](int rb) {
     const int rows = (rb - 1) * g.stride + g.size;
     return band_layout(rows, bp.rpitch, bp.fpitch, bp.bpitch, rb * g.nx, pp.nwin, valid,
