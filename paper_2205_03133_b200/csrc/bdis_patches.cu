@@ -381,12 +381,14 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
       const double cx = kx == g.nx - 1 ? g.cmax_x : __dadd_rn(g.c0, (double)kx * g.stride);
       const double cy = ky == g.ny - 1 ? g.cmax_y : __dadd_rn(g.c0, (double)ky * g.stride);
       double u = 0.0;
+      bool weak = false;  // no confident prior: the long LK solves (measured)
       if (pp.have_prev) {
         const int ix = clampi(lround_i(cx), 0, w - 1);
         const int iy = clampi(lround_i(cy), 0, h - 1);
         const Fused f = gather<false, false>(P, pair, min(ix / 2, P.w - 1), min(iy / 2, P.h - 1),
                                             pp.prev_mask);
         if (!(f.sw <= 0.0)) u = __dmul_rn(2.0, __ddiv_rn(f.swu, f.sw));
+        weak = !(f.sw >= 1.0);
       }
       st_mean[p] = mean;
       st_hess[p] = hess;
@@ -394,11 +396,28 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
       st_u[p] = u;
       st_cnt[p] = count;
       const double xc = __dsub_rn(cx, u);  // in_bounds(cx - u0, cy), lk_solver.cpp:89
-      if (xc >= 0.0 && xc <= (double)(w - 1)) pool[atomicAdd(&counters[0], 1)] = p;  // cNPool
+      // pool order: patches without a confident coarse prior first -- they
+      // take ~11 LK iterations against ~2-3 for the rest, so starting them in
+      // the first round shortens the CTA's critical path (order never changes
+      // a result); the rest are parked in wlist (unused until phase 2)
+      if (xc >= 0.0 && xc <= (double)(w - 1)) {
+        if (weak) pool[atomicAdd(&counters[0], 1)] = p;  // cNPool
+        else wlist[atomicAdd(&counters[1], 1)] = p;
+      }
     }
     st_stage[p] = stage;
   }
   __syncthreads();
+  {
+    const int nw = counters[0], ns = counters[1];
+    for (int q = tid; q < ns; q += nt) pool[nw + q] = wlist[q];
+    __syncthreads();
+    if (tid == 0) {
+      counters[0] = nw + ns;
+      counters[1] = 0;
+    }
+    __syncthreads();
+  }
 
   // ---- phase 2: rounds of one residual evaluation per busy lane. Slots
   // [0, n_act) hold the running LK solves (src/lk_solver.cpp:83-132), packed to
