@@ -649,7 +649,11 @@ BandPlan plan_bands(const Level& L, const PatchParams& pp, int max_smem_per_cta)
   bp.rpitch = pad4_host(L.w + 2 * bp.rpad) + 1;  // x in [-rpad, w + rpad]
   bp.fpitch = pad4_host(L.w - 1) + 1;            // x in [0, w - 1]
   bp.bpitch = valid ? L.w : 0;
-  const int threads = env("PSTEREO_TUNE_THREADS", g.nx < 60 ? 256 : 192);  // measured per width
+  // measured per level width (patch columns): 192-slot CTAs, two per SM, for
+  // wide levels; 128-slot CTAs, three per SM, for medium ones; 256-slot CTAs
+  // for the narrowest (whole-level bands, one CTA carries all of a pair)
+  const bool medium = g.nx >= 30 && g.nx < 60;
+  const int threads = env("PSTEREO_TUNE_THREADS", g.nx < 30 ? 256 : medium ? 128 : 192);
   auto bytes_for = [&](int rb) {
     const int rows = (rb - 1) * g.stride + g.size;
     return band_layout(rows, bp.rpitch, bp.fpitch, bp.bpitch, rb * g.nx, pp.nwin, valid,
@@ -659,7 +663,7 @@ BandPlan plan_bands(const Level& L, const PatchParams& pp, int max_smem_per_cta)
   // (measured best of a T x ppl x CTAs sweep at the bench workload;
   // PSTEREO_TUNE_THREADS / _PPL10 / _CTAS override, for tuning runs only)
   const int ppl10 = env("PSTEREO_TUNE_PPL10", 20);
-  const int ctas = env("PSTEREO_TUNE_CTAS", 2);
+  const int ctas = env("PSTEREO_TUNE_CTAS", medium ? 3 : 2);
   const size_t per_sm = size_t(max_smem_per_cta) / ctas - 1024;
   int rb = std::max(1, std::min(g.ny, (ppl10 * threads / 10 + g.nx / 2) / g.nx));
   while (rb > 1 && bytes_for(rb) > per_sm) --rb;
