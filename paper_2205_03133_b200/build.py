@@ -78,6 +78,8 @@ def build_oracle(verbose: bool = False) -> None:
     _run(["make", "-s", "-C", str(ROOT / "oracle")], verbose)
     if Path("/root/reference/proj/src").is_dir():
         _run(["make", "-s", "-j8", "-C", str(ROOT / "oracle"), "ref"], verbose)
+        # the C++ drop-in check (reference + shim from one caller), test infra
+        _run(["sh", str(ROOT / "tests" / "cpp" / "build.sh")], verbose)
 
 
 def build_all(verbose: bool = False, force: bool = False) -> None:

@@ -1,0 +1,27 @@
+"""The drop-in in the reference's own language: tests/cpp/dropin_parity.cpp
+calls the reference's run_pipeline / match_stereo (its unmodified sources) and
+this repo's C++ shim (include/pstereo_gpu.hpp) from the same C++ caller code
+on identical GrayImages and requires identical outputs (depth sigma 1e-3 rel).
+The binary is built where /root/reference exists (build()) and travels to the
+GPU box with the snapshot."""
+import subprocess
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+EXE = Path(__file__).resolve().parent.parent / "build" / "dropin_parity"
+
+
+@pytest.mark.parametrize("config,seed,size", [
+    (0, 0, None), (1, 1, None), (0, 7, (320, 240)), (4, 3, (160, 120)),
+    (3, 0, (640, 512)),
+])
+def test_cpp_dropin_matches_reference(gpu, config, seed, size):
+    if not EXE.exists():
+        pytest.skip("build/dropin_parity not built (needs /root/reference at build time)")
+    args = [str(EXE), str(config), str(seed)] + ([str(size[0]), str(size[1])] if size else [])
+    r = subprocess.run(args, capture_output=True, text=True, timeout=600)
+    print(r.stdout, r.stderr)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "identical" in r.stdout
