@@ -47,6 +47,12 @@ __device__ __forceinline__ void cp_async4(void* smem_dst, const void* gsrc) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(gsrc) : "memory");
 }
+// programmatic dependent launch: wait for the preceding grid's completion /
+// let the following grid start launching (sm_90+ griddepcontrol)
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
@@ -282,6 +288,11 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
   uint8_t* st_wok = smem + lay.oWok;
 
   const long long pbase = pair * L.plane;
+  // Levels after the first are launched programmatically behind the previous
+  // level: their band staging reads only the pyramid (complete before that
+  // level passed its own wait), so it overlaps the previous level's tail; the
+  // records of the coarser level are read only after griddep_wait below.
+  if (!pp.have_prev) griddep_wait();
   Rows<kSmem> rw;
   int rofs;  // row index of image row y in rw is y - rofs
   if constexpr (kSmem) {
@@ -337,6 +348,8 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
     rw.bp = w;
     rofs = 0;
   }
+  if (pp.have_prev) griddep_wait();
+  griddep_launch();  // our predecessors are complete: the next level may start staging
   if (tid < 24) counters[tid] = 0;
   __syncthreads();
 
@@ -690,9 +703,17 @@ static cudaError_t launch_t(const Level& L, const Level& P, const PatchParams& p
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)bp.smem_bytes);
   if (e != cudaSuccess) return e;
-  dim3 grid(bp.n_bands, pp.n_pairs);
-  kern<<<grid, bp.threads, bp.smem_bytes, s>>>(L, P, pp, bp);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(bp.n_bands, pp.n_pairs);
+  cfg.blockDim = dim3(bp.threads);
+  cfg.dynamicSmemBytes = bp.smem_bytes;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pp.have_prev ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, L, P, pp, bp);
 }
 
 template <bool kSmem, bool kValid>
