@@ -255,6 +255,20 @@ int pstereo_synth_batch(const pstereo_synth_spec* s, int n_pairs,
                         uint64_t seed0, uint8_t* left, uint8_t* right,
                         int threads);
 
+/* The same generator on the device: pairs seed0 ..
+ * seed0+n_pairs-1 written to DEVICE buffers left/right
+ * [n_pairs][height][width][channels] and, when non-NULL, the ground-truth
+ * disparity [n_pairs][height][width] -- byte-for-byte what
+ * pstereo_synth_pair produces on the host for the same (spec, seed): both
+ * evaluate csrc/synth_core.h with IEEE-exact operations only. Enqueued on
+ * `stream` (a cudaStream_t, NULL = legacy default); scratch comes from the
+ * stream-ordered allocator. Returns PSTEREO_OK, PSTEREO_ECONFIG (bad spec)
+ * or PSTEREO_EINTERNAL; the message is in pstereo_synth_last_error(). */
+int pstereo_gpu_synth(int device, const pstereo_synth_spec* s, int n_pairs,
+                      uint64_t seed0, uint8_t* left, uint8_t* right,
+                      float* disparity, void* stream);
+const char* pstereo_synth_last_error(void);
+
 #ifdef __cplusplus
 }
 #endif

@@ -138,6 +138,9 @@ def lib() -> C.CDLL:
         L.pstereo_synth_pair.argtypes = [C.POINTER(SynthSpec), C.c_uint64, u8p, u8p, f32p]
         L.pstereo_synth_batch.argtypes = [C.POINTER(SynthSpec), C.c_int, C.c_uint64, u8p, u8p,
                                           C.c_int]
+        L.pstereo_gpu_synth.argtypes = [C.c_int, C.POINTER(SynthSpec), C.c_int, C.c_uint64,
+                                        C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.pstereo_synth_last_error.restype = C.c_char_p
         L.pstereo_debug_eval_residual.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p,
                                                   C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
                                                   C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
@@ -176,6 +179,7 @@ ABI_SYMBOLS = [
     "pstereo_gpu_destroy", "pstereo_gpu_last_error", "pstereo_gpu_match_u8",
     "pstereo_gpu_match_f32", "pstereo_gpu_last_launch_count", "pstereo_gpu_set_profiling",
     "pstereo_gpu_stage_times", "pstereo_gpu_stage_name", "pstereo_synth_default",
+    "pstereo_gpu_synth", "pstereo_synth_last_error",
     "pstereo_synth_pair", "pstereo_synth_batch", "pstereo_debug_eval_residual",
     "pstereo_gpu_metrics", "pstereo_gpu_wait",
 ]
@@ -300,6 +304,28 @@ def synth_batch(config: int, n: int, seed0: int = 0, threads: int = 8, **overrid
     if rc:
         _raise(rc, "synth_batch")
     return left, right
+
+
+def synth_batch_gpu(config: int, n: int, seed0: int = 0, device: int = 0, with_disparity=False,
+                    stream=None, **overrides):
+    """The generator on the device (pstereo_gpu_synth): the same bytes as
+    synth_batch for the same (config, seeds, overrides), returned as CUDA uint8
+    tensors [n, H, W(, C)] (and the float32 ground-truth disparity)."""
+    import torch
+    s = synth_spec(config, **overrides)
+    shape = (n, s.height, s.width) if s.channels == 1 else (n, s.height, s.width, s.channels)
+    dev = torch.device("cuda", device)
+    left = torch.empty(shape, dtype=torch.uint8, device=dev)
+    right = torch.empty(shape, dtype=torch.uint8, device=dev)
+    disp = torch.empty((n, s.height, s.width), dtype=torch.float32, device=dev) \
+        if with_disparity else None
+    st = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
+    rc = lib().pstereo_gpu_synth(device, C.byref(s), n, seed0, left.data_ptr() if n else None,
+                                 right.data_ptr() if n else None,
+                                 disp.data_ptr() if disp is not None and n else None, st)
+    if rc:
+        _raise(rc, lib().pstereo_synth_last_error().decode())
+    return (left, right, disp) if with_disparity else (left, right)
 
 
 class Matcher:

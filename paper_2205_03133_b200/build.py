@@ -19,9 +19,10 @@ CSRC = PKG / "csrc"
 LIB = PKG / "libpstereo_gpu.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-CUDA_SOURCES = ["bdis_kernels.cu", "bdis_patches.cu", "bdis_metrics.cu", "bdis_capi.cu"]
+CUDA_SOURCES = ["bdis_kernels.cu", "bdis_patches.cu", "bdis_metrics.cu", "bdis_capi.cu",
+                "bdis_synth.cu"]
 C_SOURCES = ["synth.c"]
-HEADERS = ["bdis_device.cuh", "bdis_kernels.h"]
+HEADERS = ["bdis_device.cuh", "bdis_kernels.h", "synth_core.h"]
 
 # Bit-exact parity with the x86-64 SSE2 reference needs IEEE double with no
 # FMA contraction anywhere (--fmad=false); the kernels also spell the critical

@@ -1,0 +1,329 @@
+// bdis_synth.cu -- on-device BASELINE.json pair generator.
+//
+// Produces, for pairs seed0 .. seed0+n-1, the same bytes as the host generator
+// pstereo_synth_pair (csrc/synth.c): both evaluate the per-element arithmetic
+// of csrc/synth_core.h (integer hashing + IEEE-exact double/float operations,
+// no FMA contraction: this TU builds with --fmad=false like the rest), and
+// the float blur accumulates its taps in the same order. The generator lets a
+// multi-GPU run fill its inputs in HBM instead of generating on the host and
+// crossing PCIe.
+//
+// Per chunk of pairs, four launches:
+//   k_syn_hblur   CTA per (row, pair): the row's white noise (edge-clamped,
+//                 r extra columns either side) into smem, horizontal taps
+//   k_syn_vblur   32x8 pixels per CTA: vertical taps through L1, per-pair
+//                 min/max of the blurred field (order-free: exact)
+//   k_syn_discs   (stress only) CTA per pair: the sequential disc placement
+//                 loop with a per-pair coverage map, one disc per iteration
+//   k_syn_views   CTA per (row, pair): texture row into smem (left view),
+//                 then the right view sampled from it at x + d plus noise
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/pstereo_gpu.h"
+#include "synth_core.h"
+
+namespace {
+
+thread_local std::string g_synth_error;
+
+struct SynthDev {
+  int w, h, C;
+  int octaves;
+  double wavelength, d_min, d_range, noise_sigma;
+  int stress;
+  int r;                 // blur radius
+  uint64_t seed0;        // seed of the chunk's first pair
+  const float* weights;  // 2r+1 blur taps
+  float* tmp;            // [pair][h][w] horizontal pass
+  float* fld;            // [pair][h][w] blurred field
+  unsigned* minmax;      // [pair][2]: ~bits(min), bits(max) (non-negative floats)
+  uint8_t* cov;          // [pair][h][w] disc coverage (stress)
+  double* discs;         // [pair][SYN_MAX_DISCS][4]
+  int* n_discs;          // [pair]
+  uint8_t* left;         // [pair][h][w][C]
+  uint8_t* right;
+  float* disparity;      // [pair][h][w] or null
+};
+
+__global__ void k_syn_hblur(SynthDev S) {
+  extern __shared__ float sm_h[];
+  const int y = blockIdx.x, p = blockIdx.y;
+  const int w = S.w, r = S.r, taps = 2 * r + 1;
+  float* kw = sm_h;
+  float* line = sm_h + taps;
+  const uint64_t key = syn_pair_key(S.seed0 + (uint64_t)p);
+  for (int i = threadIdx.x; i < taps; i += blockDim.x) kw[i] = S.weights[i];
+  for (int i = threadIdx.x; i < w + 2 * r; i += blockDim.x) {
+    int xs = i - r;
+    xs = xs < 0 ? 0 : (xs >= w ? w - 1 : xs);
+    line[i] = syn_white(key, xs, y);
+  }
+  __syncthreads();
+  float* out = S.tmp + ((size_t)p * S.h + y) * w;
+  for (int x = threadIdx.x; x < w; x += blockDim.x) {
+    float acc = 0.0f;
+    const float* src = line + x;
+    for (int i = 0; i < taps; ++i) acc = __fadd_rn(acc, __fmul_rn(kw[i], src[i]));
+    out[x] = acc;
+  }
+}
+
+__global__ void k_syn_vblur(SynthDev S) {
+  extern __shared__ float sm_v[];
+  const int p = blockIdx.z;
+  const int x = blockIdx.x * 32 + threadIdx.x;
+  const int y = blockIdx.y * blockDim.y + threadIdx.y;
+  const int w = S.w, h = S.h, r = S.r, taps = 2 * r + 1;
+  const int tid = threadIdx.y * 32 + threadIdx.x, nt = 32 * blockDim.y;
+  for (int i = tid; i < taps; i += nt) sm_v[i] = S.weights[i];
+  __syncthreads();
+  unsigned mn_inv = 0u, mx = 0u;
+  if (x < w && y < h) {
+    const float* col = S.tmp + (size_t)p * h * w + x;
+    float acc = 0.0f;
+    for (int i = 0; i < taps; ++i) {
+      int ys = y + i - r;
+      ys = ys < 0 ? 0 : (ys >= h ? h - 1 : ys);
+      acc = __fadd_rn(acc, __fmul_rn(sm_v[i], __ldg(col + (size_t)ys * w)));
+    }
+    S.fld[((size_t)p * h + y) * w + x] = acc;
+    const unsigned b = __float_as_uint(acc);  // acc >= 0: bit order = value order
+    mn_inv = ~b;
+    mx = b;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    mn_inv = max(mn_inv, __shfl_xor_sync(0xffffffffu, mn_inv, o));
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  if (threadIdx.x == 0) {
+    atomicMax(S.minmax + 2 * p, mn_inv);
+    atomicMax(S.minmax + 2 * p + 1, mx);
+  }
+}
+
+// pstereo_synth_discs (csrc/synth.c): discs are placed one after another
+// until 30% of the pixels are covered; a disc's newly covered pixels are
+// counted in parallel (each pixel belongs to one thread, so the count equals
+// the sequential scan's).
+__global__ void k_syn_discs(SynthDev S) {
+  __shared__ unsigned long long covered;
+  __shared__ unsigned added;
+  const int p = blockIdx.x;
+  const int w = S.w, h = S.h;
+  const size_t n = (size_t)w * h;
+  const size_t limit = (size_t)(0.30 * (double)n);
+  const uint64_t key = syn_pair_key(S.seed0 + (uint64_t)p);
+  uint8_t* cov = S.cov + (size_t)p * n;
+  double* rec = S.discs + (size_t)p * SYN_MAX_DISCS * 4;
+  if (threadIdx.x == 0) covered = 0;
+  __syncthreads();
+  int nd = 0;
+  for (int k = 0; k < SYN_MAX_DISCS; ++k) {
+    if (covered >= limit) break;
+    double cx, cy, r, val;
+    syn_disc(key, k, w, h, &cx, &cy, &r, &val);
+    if (threadIdx.x == 0) {
+      rec[4 * k + 0] = cx;
+      rec[4 * k + 1] = cy;
+      rec[4 * k + 2] = r;
+      rec[4 * k + 3] = val;
+      added = 0;
+    }
+    ++nd;
+    const int x0 = (int)fmax(0.0, cx - r), x1 = (int)fmin(w - 1.0, cx + r);
+    const int y0 = (int)fmax(0.0, cy - r), y1 = (int)fmin(h - 1.0, cy + r);
+    const int bw = x1 - x0 + 1, bh = y1 - y0 + 1;
+    unsigned mine = 0;
+    __syncthreads();
+    if (bw > 0 && bh > 0) {
+      for (int q = threadIdx.x; q < bw * bh; q += blockDim.x) {
+        const int x = x0 + q % bw, y = y0 + q / bw;
+        const double dx = x - cx, dy = y - cy;
+        if (dx * dx + dy * dy <= r * r && !cov[(size_t)y * w + x]) {
+          cov[(size_t)y * w + x] = 1;
+          ++mine;
+        }
+      }
+    }
+    if (mine) atomicAdd(&added, mine);
+    __syncthreads();
+    if (threadIdx.x == 0) covered += added;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) S.n_discs[p] = nd;
+}
+
+__global__ void k_syn_views(SynthDev S) {
+  extern __shared__ double sm_d[];
+  const int y = blockIdx.x, p = blockIdx.y;
+  const int w = S.w, h = S.h, C = S.C;
+  const uint64_t key = syn_pair_key(S.seed0 + (uint64_t)p);
+  const int nd = S.stress ? S.n_discs[p] : 0;
+  double* tex = sm_d;                              // [w][C]
+  double* dsc = tex + (size_t)w * C;               // [4][nd] (cx, cy, r, val planes)
+  double* blob = dsc + 4 * SYN_MAX_DISCS;          // [2 views][3][SYN_BLOBS]
+  __shared__ double hp[3];
+  if (S.stress) {
+    const double* rec = S.discs + (size_t)p * SYN_MAX_DISCS * 4;
+    for (int i = threadIdx.x; i < 4 * nd; i += blockDim.x)
+      dsc[(i & 3) * SYN_MAX_DISCS + (i >> 2)] = rec[i];
+    if (threadIdx.x < 2 * SYN_BLOBS) {
+      const int v = threadIdx.x / SYN_BLOBS, b = threadIdx.x % SYN_BLOBS;
+      double* bb = blob + v * 3 * SYN_BLOBS;
+      syn_blob(key, v, b, w, h, &bb[b], &bb[SYN_BLOBS + b], &bb[2 * SYN_BLOBS + b]);
+    }
+    if (threadIdx.x == 2 * SYN_BLOBS) syn_half_plane(key, w, h, &hp[0], &hp[1], &hp[2]);
+  }
+  __syncthreads();
+  const double* dcx = dsc;
+  const double* dcy = dsc + SYN_MAX_DISCS;
+  const double* drr = dsc + 2 * SYN_MAX_DISCS;
+  const double* dvl = dsc + 3 * SYN_MAX_DISCS;
+  // left view = the texture row
+  const double gain0 = syn_gain(key, S.stress, 0), gain1 = syn_gain(key, S.stress, 1);
+  const size_t row0 = ((size_t)p * h + y) * w;
+  for (int x = threadIdx.x; x < w; x += blockDim.x) {
+    double spec = 0.0, dark = 1.0;
+    if (S.stress) {
+      spec = syn_specular(blob, blob + SYN_BLOBS, blob + 2 * SYN_BLOBS, x, y);
+      if (hp[0] * x + hp[1] * y > hp[2]) dark = 0.4;
+    }
+    for (int c = 0; c < C; ++c) {
+      const double v = syn_texture(x, y, syn_channel_key(key, c), S.octaves, S.wavelength, nd,
+                                   dcx, dcy, drr, dvl);
+      tex[(size_t)x * C + c] = v;
+      S.left[(row0 + x) * C + c] = syn_finish(v, gain0, dark, spec);
+    }
+  }
+  __syncthreads();
+  // right view: texture at x + d, plus sensor noise
+  const float lo = __uint_as_float(~S.minmax[2 * p]);
+  const float hi = __uint_as_float(S.minmax[2 * p + 1]);
+  const float span = hi > lo ? __fsub_rn(hi, lo) : 1.0f;
+  const double* b1 = blob + 3 * SYN_BLOBS;
+  for (int x = threadIdx.x; x < w; x += blockDim.x) {
+    const size_t i = (size_t)y * w + x;
+    const float d = syn_normalise(S.fld[row0 + x], lo, span, S.d_min, S.d_range);
+    if (S.disparity) S.disparity[row0 + x] = d;
+    double spec = 0.0, dark = 1.0;
+    if (S.stress) {
+      spec = syn_specular(b1, b1 + SYN_BLOBS, b1 + 2 * SYN_BLOBS, x, y);
+      if (hp[0] * x + hp[1] * y > hp[2]) dark = 0.4;
+    }
+    for (int c = 0; c < C; ++c) {
+      double v = syn_right_tex(tex, w, C, c, x, d);
+      v += S.noise_sigma * syn_gauss3(key ^ 0xA015Eull, (uint64_t)c, i);
+      S.right[(row0 + x) * C + c] = syn_finish(v, gain1, dark, spec);
+    }
+  }
+}
+
+int fail(int code, const std::string& msg) {
+  g_synth_error = msg;
+  return code;
+}
+
+}  // namespace
+
+extern "C" int pstereo_synth_check(const pstereo_synth_spec* s);
+
+extern "C" const char* pstereo_synth_last_error(void) { return g_synth_error.c_str(); }
+
+extern "C" int pstereo_gpu_synth(int device, const pstereo_synth_spec* s, int n_pairs,
+                                 uint64_t seed0, uint8_t* left, uint8_t* right,
+                                 float* disparity, void* stream) {
+  if (pstereo_synth_check(s)) return fail(PSTEREO_ECONFIG, "pstereo_gpu_synth: bad spec");
+  if (n_pairs < 0 || (n_pairs > 0 && (!left || !right)))
+    return fail(PSTEREO_EINTERNAL, "pstereo_gpu_synth: bad arguments");
+  if (n_pairs == 0) return PSTEREO_OK;
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return fail(PSTEREO_EINTERNAL, cudaGetErrorString(e));
+  int major = 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
+  if (major != 10) return fail(PSTEREO_EINTERNAL, "pstereo_gpu_synth: needs an sm_100 device");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int w = s->width, h = s->height, C = s->channels;
+  const size_t px = (size_t)w * h;
+  const int r = pstereo_synth_blur_weights(s->blur_sigma, nullptr, 0);
+  std::vector<float> kw((size_t)(2 * r + 1));
+  pstereo_synth_blur_weights(s->blur_sigma, kw.data(), 2 * r + 1);
+  const size_t smem_h = sizeof(float) * ((size_t)(2 * r + 1) + (size_t)(w + 2 * r));
+  const size_t smem_v = sizeof(float) * (size_t)(2 * r + 1);
+  const size_t smem_views =
+      sizeof(double) * ((size_t)w * C + 4 * SYN_MAX_DISCS + 2 * 3 * SYN_BLOBS);
+  const size_t smem_cap = 227 * 1024;
+  if (smem_h > smem_cap || smem_views > smem_cap)
+    return fail(PSTEREO_ECONFIG, "pstereo_gpu_synth: width or blur radius too large");
+  cudaFuncSetAttribute(k_syn_hblur, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_h);
+  cudaFuncSetAttribute(k_syn_vblur, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_v);
+  cudaFuncSetAttribute(k_syn_views, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)smem_views);
+
+  // chunked so the scratch stays bounded (~8.1 B per pixel per pair in flight)
+  const int chunk = n_pairs < 64 ? n_pairs : 64;
+  SynthDev S;
+  std::memset(&S, 0, sizeof S);
+  S.w = w;
+  S.h = h;
+  S.C = C;
+  S.octaves = s->octaves;
+  S.wavelength = s->base_wavelength;
+  S.d_min = s->d_min;
+  S.d_range = s->d_range;
+  S.noise_sigma = s->noise_sigma;
+  S.stress = s->stress;
+  S.r = r;
+  void* base = nullptr;
+  const size_t b_w = sizeof(float) * kw.size();
+  const size_t b_field = sizeof(float) * px * chunk;
+  const size_t b_mm = sizeof(unsigned) * 2 * chunk;
+  const size_t b_cov = s->stress ? px * chunk : 0;
+  const size_t b_disc = s->stress ? sizeof(double) * SYN_MAX_DISCS * 4 * chunk : 0;
+  const size_t b_nd = sizeof(int) * chunk;
+  auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+  const size_t total = al(b_w) + 2 * al(b_field) + al(b_mm) + al(b_cov) + al(b_disc) + al(b_nd);
+  e = cudaMallocAsync(&base, total, st);
+  if (e != cudaSuccess) return fail(PSTEREO_EINTERNAL, cudaGetErrorString(e));
+  char* q = (char*)base;
+  S.weights = (const float*)q;
+  float* dw = (float*)q;
+  q += al(b_w);
+  S.tmp = (float*)q;
+  q += al(b_field);
+  S.fld = (float*)q;
+  q += al(b_field);
+  S.minmax = (unsigned*)q;
+  q += al(b_mm);
+  S.cov = (uint8_t*)q;
+  q += al(b_cov);
+  S.discs = (double*)q;
+  q += al(b_disc);
+  S.n_discs = (int*)q;
+  e = cudaMemcpyAsync(dw, kw.data(), b_w, cudaMemcpyHostToDevice, st);
+  // the blur taps live in pageable host memory: wait before `kw` goes away
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  for (int p0 = 0; p0 < n_pairs && e == cudaSuccess; p0 += chunk) {
+    const int m = n_pairs - p0 < chunk ? n_pairs - p0 : chunk;
+    S.seed0 = seed0 + (uint64_t)p0;
+    S.left = left + (size_t)p0 * px * C;
+    S.right = right + (size_t)p0 * px * C;
+    S.disparity = disparity ? disparity + (size_t)p0 * px : nullptr;
+    e = cudaMemsetAsync(S.minmax, 0, sizeof(unsigned) * 2 * m, st);
+    if (e == cudaSuccess && s->stress) e = cudaMemsetAsync(S.cov, 0, px * m, st);
+    if (e != cudaSuccess) break;
+    k_syn_hblur<<<dim3(h, m), 256, smem_h, st>>>(S);
+    k_syn_vblur<<<dim3((w + 31) / 32, (h + 7) / 8, m), dim3(32, 8), smem_v, st>>>(S);
+    if (s->stress) k_syn_discs<<<m, 512, 0, st>>>(S);
+    k_syn_views<<<dim3(h, m), 128, smem_views, st>>>(S);
+    e = cudaGetLastError();
+  }
+  cudaError_t e2 = cudaFreeAsync(base, st);
+  if (e == cudaSuccess) e = e2;
+  if (e != cudaSuccess) return fail(PSTEREO_EINTERNAL, cudaGetErrorString(e));
+  return PSTEREO_OK;
+}

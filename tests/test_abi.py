@@ -148,3 +148,20 @@ def test_generator_right_view_follows_disparity(built):
     f = xs - x0
     expect = (1 - f) * float(l[y, x0]) + f * float(l[y, x0 + 1])
     assert abs(float(r[y, x]) - expect) <= 0.6
+
+
+def test_generator_noise_and_stress_statistics(built):
+    """The portable Box-Muller (synth_core.h: polynomial log/cos) yields N(0, sigma):
+    right - warped left has the configured spread; config-1 stress discs cover ~30%."""
+    import paper_2205_03133_b200 as P
+
+    l, r, d = P.synth_pair(0, seed=5, width=320, height=240, with_disparity=True)
+    lq, rq = P.synth_pair(0, seed=5, width=320, height=240, noise_sigma=0.0)
+    assert np.array_equal(l, lq)
+    diff = r.astype(np.float64) - rq.astype(np.float64)
+    assert abs(diff.mean()) < 0.05 and 1.9 < diff.std() < 2.15
+    l1, r1 = P.synth_pair(1, seed=1, width=320, height=240)
+    assert not np.array_equal(l1, P.synth_pair(0, seed=1, width=320, height=240)[0])
+    # textureless discs: many constant 3x3 neighbourhoods
+    flat = (np.abs(np.diff(l1.astype(int), axis=1)) == 0).mean()
+    assert flat > 0.2
