@@ -39,6 +39,7 @@ extern "C" {
 #define PSTEREO_OK 0
 #define PSTEREO_EINTERNAL 1
 #define PSTEREO_ECONFIG 2
+#define PSTEREO_EIO 3 /* IoError (kExitIoError, inc/runner.hpp:18) */
 #define PSTEREO_EDEGENERATE 4
 
 #define PSTEREO_MAX_OFFSETS 16
@@ -268,6 +269,96 @@ int pstereo_gpu_synth(int device, const pstereo_synth_spec* s, int n_pairs,
                       uint64_t seed0, uint8_t* left, uint8_t* right,
                       float* disparity, void* stream);
 const char* pstereo_synth_last_error(void);
+
+/* ---- analytic test scenes ----
+ * SceneSpec (inc/pstereo/synth.hpp:20-50) as a POD, enums as ints. */
+#define PSTEREO_SURFACE_PLANE 0
+#define PSTEREO_SURFACE_SLANTED 1
+#define PSTEREO_SURFACE_SPHERE 2
+#define PSTEREO_TEXTURE_PERLIN 0
+#define PSTEREO_TEXTURE_CHECKER 1
+#define PSTEREO_TEXTURE_CONSTANT 2
+#define PSTEREO_SHADING_DIFFUSE 0
+#define PSTEREO_SHADING_NONLAMBERTIAN 1
+typedef struct pstereo_scene_spec {
+  char name[64];
+  int surface;
+  double disparity, disparity0, disparity_gradient;
+  double sphere_depth, sphere_radius, background_depth;
+  int texture;
+  double texture_scale;
+  int texture_octaves;
+  int shading;
+  double ambient, highlight_strength, highlight_falloff;
+  double noise_std;
+  uint64_t seed;
+  int seed_explicit;
+  double focal_px, baseline;
+  int width, height;
+} pstereo_scene_spec;
+
+/* SceneSpec's member defaults (inc/pstereo/synth.hpp:20-50). */
+void pstereo_scene_default(pstereo_scene_spec* s);
+/* The value checks of load_scene_spec (src/synth.cpp:365-390). */
+int pstereo_scene_validate(const pstereo_scene_spec* s, char* msg, size_t msg_cap);
+/* load_scene_spec (src/synth.cpp:301-393): "key = value" file, '#'
+ * comments, unknown / duplicate keys and bad values are PSTEREO_ECONFIG, an
+ * unreadable file PSTEREO_EIO. */
+int pstereo_load_scene_spec(const char* path, pstereo_scene_spec* out, char* msg,
+                            size_t msg_cap);
+/* render_scene (src/synth.cpp:209-284) for n_scenes scenes of one size on
+ * the device: DEVICE buffers left/right fp32 [n][h][w] (GrayImage, all
+ * valid) and, when non-NULL, the reference disparity / depth fields as
+ * doubles [n][h][w] (all valid). Enqueued on `stream`. */
+int pstereo_gpu_render(int device, const pstereo_scene_spec* specs, int n_scenes,
+                       float* left, float* right, double* ref_disparity,
+                       double* ref_depth, void* stream);
+const char* pstereo_render_last_error(void);
+
+/* ---- caller-side formats (src/io.cpp) ----
+ * Host functions; return PSTEREO_OK, PSTEREO_ECONFIG or PSTEREO_EIO with the
+ * message in msg. */
+/* load_calibration (src/io.cpp:266-281) */
+int pstereo_load_calibration(const char* path, double* focal_px, double* baseline_mm,
+                             int* width, int* height, char* msg, size_t msg_cap);
+/* load_image (src/io.cpp:253-263) for binary PGM/PPM (decode_pnm :151-198)
+ * and 8-bit PNG (gray, gray+alpha -> RGBA, RGB, RGBA, palette -> RGB,
+ * tRNS -> alpha; 16-bit samples stripped to their high byte, as
+ * decode_png :200-249 configures libpng). Two calls: pixels == NULL returns
+ * the dimensions; then pixels (capacity cap bytes) receives
+ * [height][width][channels]. */
+int pstereo_load_image(const char* path, int* width, int* height, int* channels,
+                       uint8_t* pixels, size_t cap, char* msg, size_t msg_cap);
+/* write_pfm (src/io.cpp:297-310): "Pf\n<w> <h>\n-1.0\n" then little-endian
+ * float rows bottom to top. `values` holds [height][width] floats in the
+ * order rows_bottom_up says (1 = already bottom to top, as a match call with
+ * pstereo_outputs.flip_rows writes them); `valid` (NULL = all valid) turns
+ * invalid pixels into the -1 sentinel. */
+int pstereo_write_pfm(const char* path, int width, int height, const float* values,
+                      const uint8_t* valid, int rows_bottom_up, char* msg, size_t msg_cap);
+/* read_pfm (src/io.cpp:312-341): values [height][width] top to bottom;
+ * values == NULL returns the dimensions only. */
+int pstereo_read_pfm(const char* path, int* width, int* height, float* values, size_t cap,
+                     char* msg, size_t msg_cap);
+/* metrics CSV (src/io.cpp:346-439): header, rows formatted with the
+ * shortest round-trip representation (std::to_chars), nan for unavailable. */
+typedef struct pstereo_metrics_row {
+  char frame[128];
+  double mean_err;
+  double median_err;
+  long long valid_px;
+  double runtime_ms;
+  double coverage_rate;
+  int has_errors;
+} pstereo_metrics_row;
+const char* pstereo_metrics_csv_header(void);
+/* writes the row's CSV text (no newline) into buf; returns its length or -1 */
+int pstereo_format_metrics_row(const pstereo_metrics_row* row, char* buf, size_t cap);
+int pstereo_write_metrics_csv(const char* path, const pstereo_metrics_row* rows, int n_rows,
+                              char* msg, size_t msg_cap);
+/* rows == NULL: *n_rows receives the row count */
+int pstereo_read_metrics_csv(const char* path, pstereo_metrics_row* rows, int cap,
+                             int* n_rows, char* msg, size_t msg_cap);
 
 #ifdef __cplusplus
 }

@@ -1429,3 +1429,194 @@ void bo_compute_metrics(int w, int h, const double* est, const uint8_t* est_vali
   if (sigma) out->coverage_rate = (double)covered / (double)m;
   free(errs);
 }
+
+/* ========================================================================
+ * Analytic scene renderer, SURVEY.md 8f row 4 (src/synth.cpp). Plain-C
+ * restatement of scene_depth_at / scene_intensity_at / render_scene; pinned
+ * against the reference's own render_scene (oracle/_ref) bit for bit in
+ * tests/test_oracle_kats.py.
+ * ======================================================================== */
+
+/* splitmix (src/synth.cpp:16-21) */
+static uint64_t sc_splitmix(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+/* hash_unit (src/synth.cpp:24-27) */
+static double sc_hash_unit(uint64_t a, uint64_t b, uint64_t c) {
+  const uint64_t h = sc_splitmix(a ^ sc_splitmix(b ^ sc_splitmix(c)));
+  return (double)(h >> 11) * 0x1.0p-53;
+}
+
+/* gaussian_noise (src/synth.cpp:33-41) */
+double bo_gaussian_noise(uint64_t seed, uint64_t stream, uint64_t index) {
+  const double u1 = 1.0 - sc_hash_unit(seed, stream * 2 + 1, index);
+  const double u2 = sc_hash_unit(seed, stream * 2 + 2, index);
+  return sqrt(-2.0 * log(u1)) * cos(2.0 * 3.14159265358979323846 * u2);
+}
+
+/* value_noise (src/synth.cpp:43-72) */
+double bo_value_noise(double x, double y, uint64_t seed, int octaves, double base_scale) {
+  double sum = 0.0, norm = 0.0, amp = 1.0, wavelength = base_scale;
+  for (int o = 0; o < octaves; ++o) {
+    const double gx = x / wavelength, gy = y / wavelength;
+    const double fx = floor(gx), fy = floor(gy);
+    const int64_t ix = (int64_t)fx, iy = (int64_t)fy;
+    const double tx = (gx - fx) * (gx - fx) * (3.0 - 2.0 * (gx - fx));
+    const double ty = (gy - fy) * (gy - fy) * (3.0 - 2.0 * (gy - fy));
+    const uint64_t os = sc_splitmix(seed + (uint64_t)o);
+    const double v00 = sc_hash_unit(os, (uint64_t)ix, (uint64_t)iy);
+    const double v10 = sc_hash_unit(os, (uint64_t)(ix + 1), (uint64_t)iy);
+    const double v01 = sc_hash_unit(os, (uint64_t)ix, (uint64_t)(iy + 1));
+    const double v11 = sc_hash_unit(os, (uint64_t)(ix + 1), (uint64_t)(iy + 1));
+    const double v = (1.0 - ty) * ((1.0 - tx) * v00 + tx * v10) + ty * ((1.0 - tx) * v01 + tx * v11);
+    sum += amp * v;
+    norm += amp;
+    amp *= 0.5;
+    wavelength *= 0.5;
+  }
+  return sum / norm;
+}
+
+/* reference_depth (src/synth.cpp:84-95) */
+static double sc_reference_depth(const bo_scene* s) {
+  const double fb = s->focal_px * s->baseline;
+  if (s->surface == 1) return fb / s->disparity0;
+  if (s->surface == 2) return s->background_depth;
+  return fb / s->disparity;
+}
+
+/* sphere_hit (src/synth.cpp:104-113) on the ray (rx, ry, 1) */
+static double sc_sphere_hit(const bo_scene* s, double rx, double ry, double rz) {
+  const double zc = s->sphere_depth + s->sphere_radius;
+  const double dd = rx * rx + ry * ry + rz * rz;
+  const double dc = rz * zc;
+  const double disc = dc * dc - dd * (zc * zc - s->sphere_radius * s->sphere_radius);
+  if (disc < 0.0) return -1.0;
+  const double t = (dc - sqrt(disc)) / dd;
+  if (t <= 0.0) return -1.0;
+  return t * rz;
+}
+
+/* scene_depth_at (src/synth.cpp:117-129); pixel_ray :98-101 */
+static double sc_depth_at(const bo_scene* s, double x, double y) {
+  const double fb = s->focal_px * s->baseline;
+  if (s->surface == 1) return fb / (s->disparity0 + s->disparity_gradient * x);
+  if (s->surface == 2) {
+    const double rx = (x - 0.5 * (s->width - 1)) / s->focal_px;
+    const double ry = (y - 0.5 * (s->height - 1)) / s->focal_px;
+    const double z = sc_sphere_hit(s, rx, ry, 1.0);
+    return z > 0.0 ? z : s->background_depth;
+  }
+  return fb / s->disparity;
+}
+
+/* scene_disparity_at (src/synth.cpp:131-133) */
+double bo_scene_disparity_at(const bo_scene* s, double x, double y) {
+  return s->focal_px * s->baseline / sc_depth_at(s, x, y);
+}
+
+/* texture_at (src/synth.cpp:137-158) */
+static double sc_texture_at(const bo_scene* s, double wx, double wy) {
+  const double wavelength = s->texture_scale * sc_reference_depth(s) / s->focal_px;
+  if (s->texture == 0) {
+    const double t = bo_value_noise(wx / wavelength * s->texture_scale,
+                                    wy / wavelength * s->texture_scale, s->seed,
+                                    s->texture_octaves, s->texture_scale);
+    return 0.1 + 0.8 * t;
+  }
+  if (s->texture == 1) {
+    const int64_t cx = (int64_t)floor(wx / wavelength);
+    const int64_t cy = (int64_t)floor(wy / wavelength);
+    return ((cx + cy) & 1) ? 0.8 : 0.2;
+  }
+  return 0.5;
+}
+
+/* facing_cos (src/synth.cpp:161-188) */
+static double sc_facing_cos(const bo_scene* s, double x, double y, double z) {
+  if (s->surface == 1) {
+    const double d = s->disparity0 + s->disparity_gradient * x;
+    const double fb = s->focal_px * s->baseline;
+    const double dzdx = -fb * s->disparity_gradient / (d * d);
+    const double xc = x - 0.5 * (s->width - 1);
+    const double a = z / s->focal_px + xc / s->focal_px * dzdx;
+    const double c = a / sqrt(a * a + dzdx * dzdx);
+    return c > 0.0 ? c : 0.0; /* std::max(0.0, c) */
+  }
+  if (s->surface == 2) {
+    const double rx = (x - 0.5 * (s->width - 1)) / s->focal_px;
+    const double ry = (y - 0.5 * (s->height - 1)) / s->focal_px;
+    const double zhit = sc_sphere_hit(s, rx, ry, 1.0);
+    if (zhit <= 0.0) return 1.0;
+    const double zc = s->sphere_depth + s->sphere_radius;
+    const double nz = (zhit - zc) / s->sphere_radius;
+    return -nz > 0.0 ? -nz : 0.0;
+  }
+  return 1.0;
+}
+
+static double sc_clamp01(double v) { return v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v); }
+
+/* scene_intensity_at (src/synth.cpp:192-207) */
+double bo_scene_intensity_at(const bo_scene* s, double x, double y) {
+  const double z = sc_depth_at(s, x, y);
+  const double rx = (x - 0.5 * (s->width - 1)) / s->focal_px;
+  const double ry = (y - 0.5 * (s->height - 1)) / s->focal_px;
+  double v = sc_texture_at(s, rx * z, ry * z);
+  const double cosa = sc_facing_cos(s, x, y, z);
+  v *= s->ambient + (1.0 - s->ambient) * cosa;
+  if (s->shading == 1) {
+    const double hl = s->highlight_strength * pow(cosa, s->highlight_falloff);
+    v = v * (1.0 - hl) + hl * 0.95;
+  }
+  return sc_clamp01(v);
+}
+
+/* render_scene (src/synth.cpp:209-284) */
+int bo_render_scene(const bo_scene* s, float* left, float* right, double* ref_disparity,
+                    double* ref_depth) {
+  const int w = s->width, h = s->height;
+  const double fb = s->focal_px * s->baseline;
+  double dmax = 0.0;
+  if (s->surface == 0) {
+    dmax = s->disparity + 1.0;
+  } else if (s->surface == 1) {
+    const double g = s->disparity_gradient;
+    dmax = g > 0.0 ? (s->disparity0 + g * (w - 1) + 1.0) / (1.0 - g) : s->disparity0 + 1.0;
+  } else {
+    dmax = fb / s->sphere_depth + 1.0;
+  }
+  for (int y = 0; y < h; ++y)
+    for (int x = 0; x < w; ++x) {
+      const size_t idx = (size_t)y * w + x;
+      const double d_ref = bo_scene_disparity_at(s, x, y);
+      ref_disparity[idx] = d_ref;
+      ref_depth[idx] = fb / d_ref;
+      double v = bo_scene_intensity_at(s, x, y);
+      if (s->noise_std > 0.0) v += s->noise_std * bo_gaussian_noise(s->seed, 0, idx);
+      left[idx] = (float)sc_clamp01(v);
+      double hi = dmax, lo = 0.0;
+      const double step = 0.25;
+      for (double d = dmax - step; d > 0.0; d -= step) {
+        if (d - bo_scene_disparity_at(s, x + d, y) <= 0.0) {
+          lo = d;
+          break;
+        }
+        hi = d;
+      }
+      for (int it = 0; it < 50; ++it) {
+        const double mid = 0.5 * (lo + hi);
+        if (mid - bo_scene_disparity_at(s, x + mid, y) <= 0.0) lo = mid;
+        else hi = mid;
+      }
+      const double d_star = 0.5 * (lo + hi);
+      double rv = bo_scene_intensity_at(s, x + d_star, y);
+      if (s->noise_std > 0.0) rv += s->noise_std * bo_gaussian_noise(s->seed, 1, idx);
+      right[idx] = (float)sc_clamp01(rv);
+    }
+  return 0;
+}

@@ -205,6 +205,36 @@ void bo_compute_metrics(int w, int h, const double* est, const uint8_t* est_vali
                         const double* ref, const uint8_t* ref_valid, const double* sigma,
                         const uint8_t* sigma_valid, bo_frame_metrics* out);
 
+/* ---- analytic scene renderer (src/synth.cpp) ----
+ * SceneSpec (inc/pstereo/synth.hpp:20-50) as a POD; enums as ints
+ * (surface 0 plane / 1 slanted_plane / 2 sphere, texture 0 perlin /
+ * 1 checker / 2 constant, shading 0 diffuse / 1 nonlambertian). Same layout
+ * as the product's pstereo_scene_spec. */
+typedef struct bo_scene {
+  char name[64];
+  int surface;
+  double disparity, disparity0, disparity_gradient;
+  double sphere_depth, sphere_radius, background_depth;
+  int texture;
+  double texture_scale;
+  int texture_octaves;
+  int shading;
+  double ambient, highlight_strength, highlight_falloff;
+  double noise_std;
+  uint64_t seed;
+  int seed_explicit;
+  double focal_px, baseline;
+  int width, height;
+} bo_scene;
+double bo_scene_disparity_at(const bo_scene* s, double x, double y);
+double bo_scene_intensity_at(const bo_scene* s, double x, double y);
+double bo_value_noise(double x, double y, uint64_t seed, int octaves, double base_scale);
+double bo_gaussian_noise(uint64_t seed, uint64_t stream, uint64_t index);
+/* render_scene (src/synth.cpp:209-284): left/right fp32 [h][w] (GrayImage,
+ * all valid), reference disparity / depth doubles [h][w] (all valid). */
+int bo_render_scene(const bo_scene* s, float* left, float* right, double* ref_disparity,
+                    double* ref_depth);
+
 /* ---- whole path ---- */
 int bo_match_stereo(const bo_image* left, const bo_image* right,
                     const bo_config* cfg, bo_match_outputs* out, char* msg,

@@ -109,6 +109,21 @@ class Config:
         return c
 
 
+class BoScene(C.Structure):
+    """bo_scene = SceneSpec (inc/pstereo/synth.hpp:20-50), same layout as the
+    product's pstereo_scene_spec."""
+    _fields_ = [("name", C.c_char * 64), ("surface", C.c_int), ("disparity", C.c_double),
+                ("disparity0", C.c_double), ("disparity_gradient", C.c_double),
+                ("sphere_depth", C.c_double), ("sphere_radius", C.c_double),
+                ("background_depth", C.c_double), ("texture", C.c_int),
+                ("texture_scale", C.c_double), ("texture_octaves", C.c_int),
+                ("shading", C.c_int), ("ambient", C.c_double),
+                ("highlight_strength", C.c_double), ("highlight_falloff", C.c_double),
+                ("noise_std", C.c_double), ("seed", C.c_uint64), ("seed_explicit", C.c_int),
+                ("focal_px", C.c_double), ("baseline", C.c_double), ("width", C.c_int),
+                ("height", C.c_int)]
+
+
 class OracleError(RuntimeError):
     def __init__(self, code: int, msg: str):
         super().__init__(msg)
@@ -132,6 +147,14 @@ class Oracle:
         L.bo_propagate_probability.argtypes = [C.c_double, C.c_double, C.c_int, C.c_int, i32p]
         L.bo_level_weight.argtypes = [C.c_int, C.c_int, i32p]
         L.bo_dynamic_sigma.argtypes = [C.c_int, f64p, u8p, C.c_double]
+        for fn in ("bo_scene_disparity_at", "bo_scene_intensity_at"):
+            getattr(L, fn).restype = C.c_double
+            getattr(L, fn).argtypes = [C.POINTER(BoScene), C.c_double, C.c_double]
+        L.bo_value_noise.restype = C.c_double
+        L.bo_value_noise.argtypes = [C.c_double, C.c_double, C.c_uint64, C.c_int, C.c_double]
+        L.bo_gaussian_noise.restype = C.c_double
+        L.bo_gaussian_noise.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64]
+        L.bo_render_scene.argtypes = [C.POINTER(BoScene), f32p, f32p, f64p, f64p]
 
     # ---- helpers
     @staticmethod
@@ -143,6 +166,42 @@ class Oracle:
         img = BoImage(w, h, _p(data, f32p), _p(valid, u8p))
         img._keep = (data, valid)
         return img
+
+    # ---- analytic scenes (src/synth.cpp)
+    @staticmethod
+    def scene(spec) -> "BoScene":
+        """A bo_scene from a layout-identical ctypes struct (the product's
+        SceneSpec) or a dict of fields."""
+        if isinstance(spec, dict):
+            b = BoScene()
+            for k, v in spec.items():
+                setattr(b, k, v.encode() if k == "name" else v)
+            return b
+        return BoScene.from_buffer_copy(bytes(spec))
+
+    def render_scene(self, spec):
+        b = self.scene(spec)
+        n = b.width * b.height
+        left = np.zeros((b.height, b.width), np.float32)
+        right = np.zeros_like(left)
+        disp = np.zeros((b.height, b.width), np.float64)
+        depth = np.zeros_like(disp)
+        self.lib.bo_render_scene(C.byref(b), _p(left, f32p), _p(right, f32p), _p(disp, f64p),
+                                 _p(depth, f64p))
+        assert n == left.size
+        return left, right, disp, depth
+
+    def scene_disparity_at(self, spec, x, y) -> float:
+        return self.lib.bo_scene_disparity_at(C.byref(self.scene(spec)), x, y)
+
+    def scene_intensity_at(self, spec, x, y) -> float:
+        return self.lib.bo_scene_intensity_at(C.byref(self.scene(spec)), x, y)
+
+    def value_noise(self, x, y, seed, octaves, base) -> float:
+        return self.lib.bo_value_noise(x, y, seed, octaves, base)
+
+    def gaussian_noise(self, seed, stream, index) -> float:
+        return self.lib.bo_gaussian_noise(seed, stream, index)
 
     # ---- numerics
     def fast_exp(self, x: float) -> float:

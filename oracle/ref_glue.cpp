@@ -29,6 +29,8 @@
 #include "pstereo/metrics.hpp"
 #include "pstereo/pyramid.hpp"
 #include "pstereo/spatial_mask.hpp"
+#include "pstereo/synth.hpp"
+#include "pstereo/kv.hpp"
 #include "pstereo/window_posterior.hpp"
 
 using namespace pstereo;
@@ -506,4 +508,74 @@ void bo_compute_metrics(int w, int h, const double* est, const uint8_t* est_vali
   out->coverage_rate = m.coverage_rate;
 }
 
+
+// ---- analytic scene renderer (src/synth.cpp) ----
+
+static SceneSpec to_scene(const bo_scene* b) {
+  SceneSpec s;
+  s.name = b->name;
+  s.surface = b->surface == 1 ? SurfaceKind::slanted_plane
+              : b->surface == 2 ? SurfaceKind::sphere : SurfaceKind::plane;
+  s.disparity = b->disparity;
+  s.disparity0 = b->disparity0;
+  s.disparity_gradient = b->disparity_gradient;
+  s.sphere_depth = b->sphere_depth;
+  s.sphere_radius = b->sphere_radius;
+  s.background_depth = b->background_depth;
+  s.texture = b->texture == 1 ? TextureKind::checker
+              : b->texture == 2 ? TextureKind::constant : TextureKind::perlin;
+  s.texture_scale = b->texture_scale;
+  s.texture_octaves = b->texture_octaves;
+  s.shading = b->shading == 1 ? ShadingKind::nonlambertian : ShadingKind::diffuse;
+  s.ambient = b->ambient;
+  s.highlight_strength = b->highlight_strength;
+  s.highlight_falloff = b->highlight_falloff;
+  s.noise_std = b->noise_std;
+  s.seed = b->seed;
+  s.seed_explicit = b->seed_explicit != 0;
+  s.focal_px = b->focal_px;
+  s.baseline = b->baseline;
+  s.width = b->width;
+  s.height = b->height;
+  return s;
+}
+
+double bo_scene_disparity_at(const bo_scene* s, double x, double y) {
+  return scene_disparity_at(to_scene(s), x, y);  // src/synth.cpp:131-133
+}
+
+double bo_scene_intensity_at(const bo_scene* s, double x, double y) {
+  return scene_intensity_at(to_scene(s), x, y);  // src/synth.cpp:192-207
+}
+
+double bo_value_noise(double x, double y, uint64_t seed, int octaves, double base_scale) {
+  return value_noise(x, y, seed, octaves, base_scale);  // src/synth.cpp:43-72
+}
+
+double bo_gaussian_noise(uint64_t seed, uint64_t stream, uint64_t index) {
+  return gaussian_noise(seed, stream, index);  // src/synth.cpp:33-41
+}
+
+int bo_render_scene(const bo_scene* b, float* left, float* right, double* ref_disparity,
+                    double* ref_depth) {
+  const RenderedScene r = render_scene(to_scene(b));  // src/synth.cpp:209-284
+  std::memcpy(left, r.left.data.data(), r.left.data.size() * sizeof(float));
+  std::memcpy(right, r.right.data.data(), r.right.data.size() * sizeof(float));
+  std::memcpy(ref_disparity, r.ref_disparity.values.data(),
+              r.ref_disparity.values.size() * sizeof(double));
+  std::memcpy(ref_depth, r.ref_depth.values.data(), r.ref_depth.values.size() * sizeof(double));
+  return 0;
+}
+
 }  // extern "C"
+
+// synth.cpp links against the kv parser of io.cpp (libpng, not built here);
+// the oracle never parses scene files through the reference, so these are
+// link-time stubs only.
+namespace pstereo {
+const std::string* KvFile::find(const std::string&) const { return nullptr; }
+KvFile load_kv_file(const std::string& path) { throw ConfigError(path + ": kv parser not built"); }
+double kv_double_or(const KvFile&, const std::string&, double f) { return f; }
+long long kv_int_or(const KvFile&, const std::string&, long long f) { return f; }
+std::string kv_string_or(const KvFile&, const std::string&, const std::string& f) { return f; }
+}  // namespace pstereo

@@ -99,6 +99,37 @@ class SynthSpec(C.Structure):
                 ("noise_sigma", C.c_double), ("stress", C.c_int)]
 
 
+class SceneSpec(C.Structure):
+    """pstereo_scene_spec = SceneSpec (inc/pstereo/synth.hpp:20-50)."""
+    _fields_ = [("name", C.c_char * 64), ("surface", C.c_int), ("disparity", C.c_double),
+                ("disparity0", C.c_double), ("disparity_gradient", C.c_double),
+                ("sphere_depth", C.c_double), ("sphere_radius", C.c_double),
+                ("background_depth", C.c_double), ("texture", C.c_int),
+                ("texture_scale", C.c_double), ("texture_octaves", C.c_int),
+                ("shading", C.c_int), ("ambient", C.c_double),
+                ("highlight_strength", C.c_double), ("highlight_falloff", C.c_double),
+                ("noise_std", C.c_double), ("seed", C.c_uint64), ("seed_explicit", C.c_int),
+                ("focal_px", C.c_double), ("baseline", C.c_double), ("width", C.c_int),
+                ("height", C.c_int)]
+
+    SURFACES = {"plane": 0, "slanted_plane": 1, "sphere": 2}
+    TEXTURES = {"perlin": 0, "checker": 1, "constant": 2}
+    SHADINGS = {"diffuse": 0, "nonlambertian": 1}
+
+    def as_dict(self) -> dict:
+        d = {k: getattr(self, k) for k, _ in self._fields_}
+        d["name"] = self.name.decode()
+        return d
+
+
+class MetricsRow(C.Structure):
+    """pstereo_metrics_row = FrameMetrics as the CSV stores it (inc/metrics.hpp)."""
+    _fields_ = [("frame", C.c_char * 128), ("mean_err", C.c_double),
+                ("median_err", C.c_double), ("valid_px", C.c_longlong),
+                ("runtime_ms", C.c_double), ("coverage_rate", C.c_double),
+                ("has_errors", C.c_int)]
+
+
 _LIB = None
 
 
@@ -141,6 +172,28 @@ def lib() -> C.CDLL:
         L.pstereo_gpu_synth.argtypes = [C.c_int, C.POINTER(SynthSpec), C.c_int, C.c_uint64,
                                         C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.pstereo_synth_last_error.restype = C.c_char_p
+        L.pstereo_render_last_error.restype = C.c_char_p
+        L.pstereo_gpu_render.argtypes = [C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p,
+                                         C.c_void_p, C.c_void_p, C.c_void_p]
+        L.pstereo_scene_default.argtypes = [C.POINTER(SceneSpec)]
+        L.pstereo_scene_validate.argtypes = [C.POINTER(SceneSpec), C.c_char_p, C.c_size_t]
+        L.pstereo_load_scene_spec.argtypes = [C.c_char_p, C.POINTER(SceneSpec), C.c_char_p,
+                                              C.c_size_t]
+        L.pstereo_load_calibration.argtypes = [C.c_char_p, C.POINTER(C.c_double),
+                                               C.POINTER(C.c_double), i32p, i32p, C.c_char_p,
+                                               C.c_size_t]
+        L.pstereo_load_image.argtypes = [C.c_char_p, i32p, i32p, i32p, C.c_void_p, C.c_size_t,
+                                         C.c_char_p, C.c_size_t]
+        L.pstereo_write_pfm.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
+                                        C.c_int, C.c_char_p, C.c_size_t]
+        L.pstereo_read_pfm.argtypes = [C.c_char_p, i32p, i32p, C.c_void_p, C.c_size_t,
+                                       C.c_char_p, C.c_size_t]
+        L.pstereo_metrics_csv_header.restype = C.c_char_p
+        L.pstereo_format_metrics_row.argtypes = [C.POINTER(MetricsRow), C.c_char_p, C.c_size_t]
+        L.pstereo_write_metrics_csv.argtypes = [C.c_char_p, C.POINTER(MetricsRow), C.c_int,
+                                                C.c_char_p, C.c_size_t]
+        L.pstereo_read_metrics_csv.argtypes = [C.c_char_p, C.POINTER(MetricsRow), C.c_int,
+                                               i32p, C.c_char_p, C.c_size_t]
         L.pstereo_debug_eval_residual.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p,
                                                   C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
                                                   C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
@@ -179,7 +232,11 @@ ABI_SYMBOLS = [
     "pstereo_gpu_destroy", "pstereo_gpu_last_error", "pstereo_gpu_match_u8",
     "pstereo_gpu_match_f32", "pstereo_gpu_last_launch_count", "pstereo_gpu_set_profiling",
     "pstereo_gpu_stage_times", "pstereo_gpu_stage_name", "pstereo_synth_default",
-    "pstereo_gpu_synth", "pstereo_synth_last_error",
+    "pstereo_gpu_synth", "pstereo_synth_last_error", "pstereo_gpu_render",
+    "pstereo_render_last_error", "pstereo_scene_default", "pstereo_scene_validate",
+    "pstereo_load_scene_spec", "pstereo_load_calibration", "pstereo_load_image",
+    "pstereo_write_pfm", "pstereo_read_pfm", "pstereo_metrics_csv_header",
+    "pstereo_format_metrics_row", "pstereo_write_metrics_csv", "pstereo_read_metrics_csv",
     "pstereo_synth_pair", "pstereo_synth_batch", "pstereo_debug_eval_residual",
     "pstereo_gpu_metrics", "pstereo_gpu_wait",
 ]
@@ -326,6 +383,156 @@ def synth_batch_gpu(config: int, n: int, seed0: int = 0, device: int = 0, with_d
     if rc:
         _raise(rc, lib().pstereo_synth_last_error().decode())
     return (left, right, disp) if with_disparity else (left, right)
+
+
+# ---- analytic scenes and caller-side formats (row 3)
+
+class IoError(OSError):
+    """The reference's IoError (inc/pstereo/errors.hpp), exit code 3."""
+
+
+def _check_io(rc: int, msg) -> None:
+    if rc == 0:
+        return
+    text = msg.value.decode(errors="replace") if hasattr(msg, "value") else str(msg)
+    if rc == 3:
+        raise IoError(text)
+    _raise(rc, text)
+
+
+def scene_spec(**fields) -> SceneSpec:
+    """SceneSpec defaults (inc/pstereo/synth.hpp:20-50) with overrides; surface /
+    texture / shading may be given by name."""
+    s = SceneSpec()
+    lib().pstereo_scene_default(C.byref(s))
+    for k, v in fields.items():
+        if k == "name":
+            v = v.encode()
+        elif k == "surface" and isinstance(v, str):
+            v = SceneSpec.SURFACES[v]
+        elif k == "texture" and isinstance(v, str):
+            v = SceneSpec.TEXTURES[v]
+        elif k == "shading" and isinstance(v, str):
+            v = SceneSpec.SHADINGS[v]
+        setattr(s, k, v)
+    msg = C.create_string_buffer(256)
+    _check_io(lib().pstereo_scene_validate(C.byref(s), msg, 256), msg)
+    return s
+
+
+def load_scene_spec(path) -> SceneSpec:
+    """load_scene_spec (src/synth.cpp:301-393)."""
+    s = SceneSpec()
+    msg = C.create_string_buffer(512)
+    _check_io(lib().pstereo_load_scene_spec(str(path).encode(), C.byref(s), msg, 512), msg)
+    return s
+
+
+def render_scenes_gpu(specs, device: int = 0, stream=None, fields=True):
+    """render_scene (src/synth.cpp:209-284) on the device for scenes of one
+    size: CUDA tensors left/right float32 [n, h, w] and, with fields, the
+    reference disparity / depth float64 [n, h, w]."""
+    import torch
+    specs = [specs] if isinstance(specs, SceneSpec) else list(specs)
+    n = len(specs)
+    arr = (SceneSpec * max(n, 1))(*specs)
+    h, w = (specs[0].height, specs[0].width) if n else (0, 0)
+    dev = torch.device("cuda", device)
+    left = torch.empty((n, h, w), dtype=torch.float32, device=dev)
+    right = torch.empty((n, h, w), dtype=torch.float32, device=dev)
+    disp = torch.empty((n, h, w), dtype=torch.float64, device=dev) if fields else None
+    depth = torch.empty((n, h, w), dtype=torch.float64, device=dev) if fields else None
+    st = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
+    ptr = (lambda t: t.data_ptr() if t is not None and n else None)
+    rc = lib().pstereo_gpu_render(device, arr, n, ptr(left), ptr(right), ptr(disp), ptr(depth),
+                                  st)
+    if rc:
+        _raise(rc, lib().pstereo_render_last_error().decode())
+    return left, right, disp, depth
+
+
+def load_calibration(path) -> dict:
+    """load_calibration (src/io.cpp:266-281)."""
+    f, b = C.c_double(), C.c_double()
+    w, h = C.c_int(), C.c_int()
+    msg = C.create_string_buffer(512)
+    _check_io(lib().pstereo_load_calibration(str(path).encode(), C.byref(f), C.byref(b),
+                                             C.byref(w), C.byref(h), msg, 512), msg)
+    return {"focal_px": f.value, "baseline_mm": b.value, "width": w.value, "height": h.value}
+
+
+def load_image(path) -> np.ndarray:
+    """load_image (src/io.cpp:253-263): uint8 [h, w, channels] (PGM/PPM/PNG)."""
+    w, h, c = C.c_int(), C.c_int(), C.c_int()
+    msg = C.create_string_buffer(512)
+    p = str(path).encode()
+    _check_io(lib().pstereo_load_image(p, C.byref(w), C.byref(h), C.byref(c), None, 0, msg,
+                                       512), msg)
+    out = np.zeros((h.value, w.value, c.value), np.uint8)
+    _check_io(lib().pstereo_load_image(p, C.byref(w), C.byref(h), C.byref(c),
+                                       out.ctypes.data, out.nbytes, msg, 512), msg)
+    return out
+
+
+def write_pfm(path, values, valid=None, rows_bottom_up=False) -> None:
+    """write_pfm (src/io.cpp:297-310): -1 at invalid pixels, rows bottom to top."""
+    v = np.ascontiguousarray(values, np.float32)
+    ok = None if valid is None else np.ascontiguousarray(valid, np.uint8)
+    h, w = v.shape
+    msg = C.create_string_buffer(512)
+    _check_io(lib().pstereo_write_pfm(str(path).encode(), w, h, v.ctypes.data,
+                                      None if ok is None else ok.ctypes.data,
+                                      int(bool(rows_bottom_up)), msg, 512), msg)
+
+
+def read_pfm(path) -> np.ndarray:
+    """read_pfm (src/io.cpp:312-341): float32 [h, w], top row first."""
+    w, h = C.c_int(), C.c_int()
+    msg = C.create_string_buffer(512)
+    p = str(path).encode()
+    _check_io(lib().pstereo_read_pfm(p, C.byref(w), C.byref(h), None, 0, msg, 512), msg)
+    out = np.zeros((h.value, w.value), np.float32)
+    _check_io(lib().pstereo_read_pfm(p, C.byref(w), C.byref(h), out.ctypes.data, out.size,
+                                     msg, 512), msg)
+    return out
+
+
+def metrics_row(frame="", mean_err=float("nan"), median_err=float("nan"), valid_px=0,
+                runtime_ms=0.0, coverage_rate=float("nan")) -> MetricsRow:
+    r = MetricsRow()
+    r.frame = frame.encode()
+    r.mean_err, r.median_err, r.valid_px = mean_err, median_err, valid_px
+    r.runtime_ms, r.coverage_rate = runtime_ms, coverage_rate
+    r.has_errors = int(mean_err == mean_err)
+    return r
+
+
+def metrics_csv_header() -> str:
+    return lib().pstereo_metrics_csv_header().decode()
+
+
+def format_metrics_row(row: MetricsRow) -> str:
+    buf = C.create_string_buffer(1024)
+    n = lib().pstereo_format_metrics_row(C.byref(row), buf, 1024)
+    if n < 0:
+        raise GpuError("metrics row too long")
+    return buf.value.decode()
+
+
+def write_metrics_csv(path, rows) -> None:
+    arr = (MetricsRow * max(len(rows), 1))(*rows)
+    msg = C.create_string_buffer(512)
+    _check_io(lib().pstereo_write_metrics_csv(str(path).encode(), arr, len(rows), msg, 512), msg)
+
+
+def read_metrics_csv(path) -> list:
+    n = C.c_int()
+    msg = C.create_string_buffer(512)
+    p = str(path).encode()
+    _check_io(lib().pstereo_read_metrics_csv(p, None, 0, C.byref(n), msg, 512), msg)
+    arr = (MetricsRow * max(n.value, 1))()
+    _check_io(lib().pstereo_read_metrics_csv(p, arr, n.value, C.byref(n), msg, 512), msg)
+    return list(arr[: n.value])
 
 
 class Matcher:
@@ -496,6 +703,37 @@ class Matcher:
             r["has_errors"] = bool(r["has_errors"])
         return res[0] if single else res
 
+    def run_device_f32(self, n, width, height, left_ptr, right_ptr, outputs: dict, dtype=F32,
+                       focal=1.0, baseline=1.0, stream=None, left_valid_ptr=None,
+                       right_valid_ptr=None, invalid_value=None):
+        """GrayImage planes (fp32 [n,h,w] + optional u8 validity) and outputs in
+        device memory: only enqueues work on `stream`."""
+        o = _Outputs()
+        o.dtype = dtype
+        o.on_device = 1
+        if invalid_value is not None:
+            o.fill_invalid, o.invalid_value = 1, float(invalid_value)
+        for k, ptr in outputs.items():
+            setattr(o, k, ptr)
+        rc = lib().pstereo_gpu_match_f32(self._h, n, width, height, left_ptr, left_valid_ptr,
+                                         right_ptr, right_valid_ptr, 1, focal, baseline,
+                                         C.byref(o), stream)
+        if rc:
+            _raise(rc, self.last_error())
+
+    def metrics_device(self, n, width, height, est, est_valid, ref, ref_valid, sigma=None,
+                       sigma_valid=None, stream=None):
+        """compute_metrics on device-resident double fields (pointers)."""
+        out = (FrameMetricsC * max(n, 1))()
+        rc = lib().pstereo_gpu_metrics(self._h, n, width, height, est, est_valid, ref,
+                                       ref_valid, sigma, sigma_valid, 1, out, stream)
+        if rc:
+            _raise(rc, self.last_error())
+        res = [{k: getattr(out[i], k) for k, _ in FrameMetricsC._fields_} for i in range(n)]
+        for r in res:
+            r["has_errors"] = bool(r["has_errors"])
+        return res
+
     def run_device_u8(self, n, width, height, channels, left_ptr, right_ptr, outputs: dict,
                       dtype=F32, focal=1.0, baseline=1.0, stream=None, invalid_value=None):
         o = _Outputs()
@@ -602,3 +840,81 @@ def compute_metrics(estimate, estimate_valid, reference, reference_valid, sigma=
     h, w = est.shape[-2], est.shape[-1]
     return _matcher_for(PipelineConfig(coarsest_exp=0, finest_exp=0, patch_size=2), w, h).metrics(
         estimate, estimate_valid, reference, reference_valid, sigma, sigma_valid)
+
+
+def run_benchmark_gpu(scenes, cfg: "PipelineConfig", repetitions: int = 10, device: int = 0):
+    """run_benchmark (src/bench.cpp:11-67) on the device: every scene rendered
+    by pstereo_gpu_render, matched `repetitions` times (runtime_ms = mean CUDA
+    event time of one run_pipeline call), depth errors against the scene's
+    reference depth by pstereo_gpu_metrics; returns the per-scene FrameMetrics
+    rows plus the aggregate row ("average", NaN-aware means)."""
+    import math
+
+    import torch
+    if repetitions < 1:
+        raise ConfigError("benchmark repetitions must be >= 1")
+    scenes = list(scenes)
+    if not scenes:
+        raise ConfigError("benchmark needs at least one scene")
+    validate(cfg)
+    dev = torch.device("cuda", device)
+    stream = torch.cuda.Stream(dev)
+    sh = stream.cuda_stream
+    frames = []
+    with torch.cuda.stream(stream):
+        for spec in scenes:
+            w, h = spec.width, spec.height
+            left, right, _, ref_depth = render_scenes_gpu([spec], device=device, stream=sh)
+            ones = torch.ones((1, h, w), dtype=torch.uint8, device=dev)
+            depth = torch.empty((1, h, w), dtype=torch.float64, device=dev)
+            dvalid = torch.empty((1, h, w), dtype=torch.uint8, device=dev)
+            var = bool(cfg.estimate_variance)
+            sig = torch.empty_like(depth) if var else None
+            svalid = torch.empty_like(dvalid) if var else None
+            outs = {"depth": depth.data_ptr(), "depth_valid": dvalid.data_ptr()}
+            if var:
+                outs.update(depth_sigma=sig.data_ptr(), sigma_valid=svalid.data_ptr())
+            with Matcher(cfg, w, h, 1, device=device) as m:
+                total = 0.0
+                for _ in range(repetitions):
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                    m.run_device_f32(1, w, h, left.data_ptr(), right.data_ptr(), outs,
+                                     dtype=F64, focal=spec.focal_px, baseline=spec.baseline,
+                                     stream=sh)
+                    e1.record(stream)
+                    e1.synchronize()
+                    total += e0.elapsed_time(e1)
+                r = m.metrics_device(1, w, h, depth.data_ptr(), dvalid.data_ptr(),
+                                     ref_depth.data_ptr(), ones.data_ptr(),
+                                     sig.data_ptr() if var else None,
+                                     svalid.data_ptr() if var else None, stream=sh)[0]
+            frames.append({"frame": spec.name.decode(), "mean_err": r["mean_err"],
+                           "median_err": r["median_err"], "valid_px": r["valid_px"],
+                           "runtime_ms": total / repetitions,
+                           "coverage_rate": r["coverage_rate"] if var else float("nan"),
+                           "has_errors": r["has_errors"]})
+    # aggregate row, src/bench.cpp:37-65
+    err = [f for f in frames if f["has_errors"]]
+    cov = [f["coverage_rate"] for f in frames if not math.isnan(f["coverage_rate"])]
+    agg = {"frame": "average", "mean_err": float("nan"), "median_err": float("nan"),
+           "has_errors": False, "coverage_rate": float("nan")}
+    if err:
+        ms = ds = 0.0
+        for f in err:
+            ms += f["mean_err"]
+            ds += f["median_err"]
+        agg.update(mean_err=ms / len(err), median_err=ds / len(err), has_errors=True)
+    if cov:
+        c = 0.0
+        for v in cov:
+            c += v
+        agg["coverage_rate"] = c / len(cov)
+    px = ms_ = 0.0
+    for f in frames:
+        px += float(f["valid_px"])
+        ms_ += f["runtime_ms"]
+    agg["valid_px"] = int(px / len(frames) + 0.5)
+    agg["runtime_ms"] = ms_ / len(frames)
+    return frames, agg

@@ -20,7 +20,8 @@ LIB = PKG / "libpstereo_gpu.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 CUDA_SOURCES = ["bdis_kernels.cu", "bdis_patches.cu", "bdis_metrics.cu", "bdis_capi.cu",
-                "bdis_synth.cu"]
+                "bdis_synth.cu", "bdis_render.cu"]
+CXX_SOURCES = ["host_io.cpp"]
 C_SOURCES = ["synth.c"]
 HEADERS = ["bdis_device.cuh", "bdis_kernels.h", "synth_core.h"]
 
@@ -52,7 +53,7 @@ def _run(cmd: list[str], verbose: bool) -> str:
 
 
 def build_gpu_lib(verbose: bool = False, force: bool = False) -> Path:
-    deps = [CSRC / s for s in CUDA_SOURCES + C_SOURCES + HEADERS]
+    deps = [CSRC / s for s in CUDA_SOURCES + C_SOURCES + CXX_SOURCES + HEADERS]
     deps.append(ROOT / "include" / "pstereo_gpu.h")
     if not force and not _stale(LIB, deps):
         return LIB
@@ -69,8 +70,13 @@ def build_gpu_lib(verbose: bool = False, force: bool = False) -> Path:
         _run(["gcc", "-std=gnu11", "-O2", "-fPIC", "-ffp-contract=off", "-c",
               str(CSRC / src), "-o", str(obj)], verbose)
         objs.append(obj)
+    for src in CXX_SOURCES:
+        obj = objdir / (src + ".o")
+        _run(["g++", "-std=c++17", "-O2", "-fPIC", "-Wall", "-Wextra", "-c",
+              str(CSRC / src), "-o", str(obj)], verbose)
+        objs.append(obj)
     _run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static",
-          "-o", str(LIB), *map(str, objs), "-lpthread", "-lm"], verbose)
+          "-o", str(LIB), *map(str, objs), "-lpthread", "-lm", "-lz"], verbose)
     (ROOT / "build" / "ptxas.log").write_text("".join(log))
     return LIB
 
