@@ -132,6 +132,11 @@ typedef struct pstereo_outputs {
    * uploads and kernels run under this batch's downloads). Ignored when
    * stats or finest records are requested (those are finished on the host). */
   int async_host;
+  /* When flip_rows != 0 every output plane is written bottom row first --
+   * the row order of the PFM payload (write_pfm, src/io.cpp:297-310) -- so
+   * a disparity plane with fill_invalid / invalid_value -1 is the PFM body
+   * verbatim (pstereo_write_pfm with rows_bottom_up = 1). */
+  int flip_rows;
 } pstereo_outputs;
 
 typedef struct pstereo_ctx pstereo_ctx;
@@ -313,6 +318,10 @@ int pstereo_load_scene_spec(const char* path, pstereo_scene_spec* out, char* msg
 int pstereo_gpu_render(int device, const pstereo_scene_spec* specs, int n_scenes,
                        float* left, float* right, double* ref_disparity,
                        double* ref_depth, void* stream);
+/* The same with HOST buffers (blocking; device scratch inside). */
+int pstereo_render_host(int device, const pstereo_scene_spec* specs, int n_scenes,
+                        float* left, float* right, double* ref_disparity,
+                        double* ref_depth);
 const char* pstereo_render_last_error(void);
 
 /* ---- caller-side formats (src/io.cpp) ----

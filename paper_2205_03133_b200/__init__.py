@@ -88,7 +88,7 @@ class _Outputs(C.Structure):
         ("match_disparity", C.c_void_p), ("match_valid", C.c_void_p), ("var_disp", C.c_void_p),
         ("stats", C.POINTER(LevelStats)), ("finest", C.POINTER(PatchEstimate)),
         ("finest_count", i32p), ("finest_cap", C.c_int), ("fill_invalid", C.c_int),
-        ("invalid_value", C.c_double), ("async_host", C.c_int),
+        ("invalid_value", C.c_double), ("async_host", C.c_int), ("flip_rows", C.c_int),
     ]
 
 
@@ -594,7 +594,7 @@ class Matcher:
     # ---- host-memory batched API (numpy in, numpy out)
     def run_batch(self, left, right, focal=1.0, baseline=1.0, dtype=F32, left_valid=None,
                   right_valid=None, want=("disparity", "disparity_valid"), stats=False,
-                  finest_cap=0, invalid_value=None):
+                  finest_cap=0, invalid_value=None, flip_rows=False):
         """Batched run_pipeline. left/right: uint8 [n,h,w] / [n,h,w,c], or float32
         [n,h,w] GrayImage planes (+ optional u8 validity)."""
         left = np.ascontiguousarray(left)
@@ -615,6 +615,7 @@ class Matcher:
         o = _Outputs()
         o.dtype = dtype
         o.on_device = 0
+        o.flip_rows = int(bool(flip_rows))
         if invalid_value is not None:
             o.fill_invalid, o.invalid_value = 1, float(invalid_value)
         planes = {"disparity": vt, "disparity_valid": np.uint8, "probability": vt, "depth": vt,
@@ -705,12 +706,13 @@ class Matcher:
 
     def run_device_f32(self, n, width, height, left_ptr, right_ptr, outputs: dict, dtype=F32,
                        focal=1.0, baseline=1.0, stream=None, left_valid_ptr=None,
-                       right_valid_ptr=None, invalid_value=None):
+                       right_valid_ptr=None, invalid_value=None, flip_rows=False):
         """GrayImage planes (fp32 [n,h,w] + optional u8 validity) and outputs in
         device memory: only enqueues work on `stream`."""
         o = _Outputs()
         o.dtype = dtype
         o.on_device = 1
+        o.flip_rows = int(bool(flip_rows))
         if invalid_value is not None:
             o.fill_invalid, o.invalid_value = 1, float(invalid_value)
         for k, ptr in outputs.items():
@@ -735,10 +737,11 @@ class Matcher:
         return res
 
     def run_device_u8(self, n, width, height, channels, left_ptr, right_ptr, outputs: dict,
-                      dtype=F32, focal=1.0, baseline=1.0, stream=None, invalid_value=None):
+                      dtype=F32, focal=1.0, baseline=1.0, stream=None, invalid_value=None, flip_rows=False):
         o = _Outputs()
         o.dtype = dtype
         o.on_device = 1
+        o.flip_rows = int(bool(flip_rows))
         if invalid_value is not None:
             o.fill_invalid, o.invalid_value = 1, float(invalid_value)
         for k, ptr in outputs.items():

@@ -17,11 +17,13 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libpstereo_gpu.so"
+CLI = PKG / "pstereo_gpu_cli"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 CUDA_SOURCES = ["bdis_kernels.cu", "bdis_patches.cu", "bdis_metrics.cu", "bdis_capi.cu",
                 "bdis_synth.cu", "bdis_render.cu"]
 CXX_SOURCES = ["host_io.cpp"]
+TOOLS = ["cli.cpp"]
 C_SOURCES = ["synth.c"]
 HEADERS = ["bdis_device.cuh", "bdis_kernels.h", "synth_core.h"]
 
@@ -53,9 +55,10 @@ def _run(cmd: list[str], verbose: bool) -> str:
 
 
 def build_gpu_lib(verbose: bool = False, force: bool = False) -> Path:
-    deps = [CSRC / s for s in CUDA_SOURCES + C_SOURCES + CXX_SOURCES + HEADERS]
+    deps = [CSRC / s for s in CUDA_SOURCES + C_SOURCES + CXX_SOURCES + TOOLS + HEADERS]
     deps.append(ROOT / "include" / "pstereo_gpu.h")
-    if not force and not _stale(LIB, deps):
+    deps.append(ROOT / "include" / "pstereo_gpu.hpp")
+    if not force and not _stale(LIB, deps) and not _stale(CLI, deps):
         return LIB
     objdir = ROOT / "build" / "obj"
     objdir.mkdir(parents=True, exist_ok=True)
@@ -78,6 +81,9 @@ def build_gpu_lib(verbose: bool = False, force: bool = False) -> Path:
     _run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static",
           "-o", str(LIB), *map(str, objs), "-lpthread", "-lm", "-lz"], verbose)
     (ROOT / "build" / "ptxas.log").write_text("".join(log))
+    # the reference's command line (src/runner.cpp) over the shim
+    _run(["g++", "-std=c++17", "-O2", "-Wall", "-I", str(ROOT / "include"), str(CSRC / "cli.cpp"),
+          "-L", str(PKG), "-lpstereo_gpu", "-Wl,-rpath,$ORIGIN", "-o", str(CLI)], verbose)
     return LIB
 
 

@@ -578,7 +578,7 @@ struct HostCopies {
 
 int run_device(pstereo_ctx* ctx, Scratch& sc, const std::vector<LevelGeom>& geo, int n, int W,
                int H, int channels, const uint8_t* const src_u8_in[2], long long f32_offset,
-               bool have_f32_valid, double focal, double baseline, int f64, int fill_invalid,
+               bool have_f32_valid, double focal, double baseline, int f64, int out_flags,
                double invalid_value, void* const dev_ptr[10], const HostCopies& hc,
                cudaStream_t s) {
   const pstereo_params& prm = ctx->params;
@@ -844,7 +844,8 @@ int run_device(pstereo_ctx* ctx, Scratch& sc, const std::vector<LevelGeom>& geo,
   oa.out_mdisp = dev_ptr[7];
   oa.out_mvalid = (uint8_t*)dev_ptr[8];
   oa.out_var = dev_ptr[9];
-  oa.fill_invalid = fill_invalid;
+  oa.fill_invalid = out_flags & 1;      // pstereo_outputs.fill_invalid
+  oa.flip_rows = (out_flags >> 1) & 1;  // pstereo_outputs.flip_rows
   oa.invalid_value = invalid_value;
   launch_output(oa, f64, n, s);
   ++ctx->launches;
@@ -1040,7 +1041,8 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
       hc.fsg = fsg.data() + np_f * c0;
     }
     rc = run_device(ctx, ctx->scr[slot], geo, nc, W, H, channels, cu8, left_u8 ? 0 : c0,
-                    have_f32_valid, focal, baseline, f64, out->fill_invalid, out->invalid_value,
+                    have_f32_valid, focal, baseline, f64,
+                    (out->fill_invalid ? 1 : 0) | (out->flip_rows ? 2 : 0), out->invalid_value,
                     cout, hc, cs);
     if (rc) return rc;
     if (host_out) {

@@ -754,7 +754,7 @@ __global__ void k_output(OutputArgs a) {
     const uchar2 mv2{(unsigned char)mv, (unsigned char)mv};
     const uchar2 dv2{(unsigned char)dv, (unsigned char)dv};
     for (int y = y0; y < y1; ++y) {
-      const long long o = pbase + (long long)y * a.W + x0;
+      const long long o = pbase + (long long)(a.flip_rows ? a.H - 1 - y : y) * a.W + x0;
       if (a.out_disp) *(T2*)((T*)a.out_disp + o) = T2{d, d};
       if (a.out_dvalid) *(uchar2*)(a.out_dvalid + o) = kv;
       if (a.out_prob) *(T2*)((T*)a.out_prob + o) = T2{p, p};
@@ -770,7 +770,7 @@ __global__ void k_output(OutputArgs a) {
   }
   for (int y = y0; y < y1; ++y) {
     for (int x = x0; x < x1; ++x) {
-      const long long o = pbase + (long long)y * a.W + x;
+      const long long o = pbase + (long long)(a.flip_rows ? a.H - 1 - y : y) * a.W + x;
       if (a.out_disp) ((T*)a.out_disp)[o] = d;
       if (a.out_dvalid) a.out_dvalid[o] = keep ? 1 : 0;
       if (a.out_prob) ((T*)a.out_prob)[o] = p;
@@ -865,7 +865,8 @@ __global__ void __launch_bounds__(256) k_output_x4(OutputArgs a) {
   const long long pbase = pair * (long long)a.W * a.H;
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
-    const long long o = pbase + (long long)(2 * fy + r) * a.W + 2 * fx;
+    const int y = 2 * fy + r;
+    const long long o = pbase + (long long)(a.flip_rows ? a.H - 1 - y : y) * a.W + 2 * fx;
     if (a.out_disp) put_row8<T>(a.out_disp, o, d[0], d[1], d[2], d[3]);
     if (a.out_dvalid) put_row8_u8(a.out_dvalid, o, keep);
     if (a.out_prob) put_row8<T>(a.out_prob, o, p[0], p[1], p[2], p[3]);

@@ -151,6 +151,7 @@ struct OutputArgs {
   void* out_var;
   int fill_invalid;
   double invalid_value;
+  int flip_rows;  // output rows bottom to top (the PFM payload order)
 };
 
 struct StatsArgs {

@@ -281,3 +281,33 @@ extern "C" int pstereo_gpu_render(int device, const pstereo_scene_spec* specs, i
   if (e != cudaSuccess) return fail(PSTEREO_EINTERNAL, cudaGetErrorString(e));
   return PSTEREO_OK;
 }
+
+// Host-buffer variant: device scratch, render, copy back (blocking).
+extern "C" int pstereo_render_host(int device, const pstereo_scene_spec* specs, int n_scenes,
+                                   float* left, float* right, double* ref_disparity,
+                                   double* ref_depth) {
+  if (n_scenes <= 0) return n_scenes == 0 ? PSTEREO_OK : fail(PSTEREO_EINTERNAL, "bad count");
+  if (!specs) return fail(PSTEREO_EINTERNAL, "pstereo_render_host: bad arguments");
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return fail(PSTEREO_EINTERNAL, cudaGetErrorString(e));
+  const size_t px = (size_t)specs[0].width * specs[0].height * n_scenes;
+  char* buf = nullptr;
+  e = cudaMalloc(&buf, px * 24);
+  if (e != cudaSuccess) return fail(PSTEREO_EINTERNAL, cudaGetErrorString(e));
+  float* dl = (float*)buf;
+  float* dr = dl + px;
+  double* dd = (double*)(buf + px * 8);
+  double* dz = dd + px;
+  int rc = pstereo_gpu_render(device, specs, n_scenes, dl, dr, ref_disparity ? dd : nullptr,
+                              ref_depth ? dz : nullptr, nullptr);
+  if (rc == PSTEREO_OK) {
+    e = cudaMemcpy(left, dl, px * 4, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemcpy(right, dr, px * 4, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess && ref_disparity)
+      e = cudaMemcpy(ref_disparity, dd, px * 8, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess && ref_depth) e = cudaMemcpy(ref_depth, dz, px * 8, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) rc = fail(PSTEREO_EINTERNAL, cudaGetErrorString(e));
+  }
+  cudaFree(buf);
+  return rc;
+}
