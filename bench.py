@@ -253,7 +253,6 @@ def run_ours(args):
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
-    m.set_profiling(True)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
@@ -268,8 +267,20 @@ def run_ours(args):
         dist.barrier()
     clk = clocks.stop()
     ms = e0.elapsed_time(e1)
+    # per-stage device times from a separate, instrumented pass (the stage
+    # events serialise the launches, so they stay out of the timed region)
+    m.set_device_chunks(1)  # one launch per stage: per-launch durations for the roofline
+    step()  # (re)sizes the working set for the unsplit batch outside the profile
+    torch.cuda.synchronize(dev)
+    m.set_profiling(True)
+    prof_steps = min(args.steps, 10)
+    for _ in range(prof_steps):
+        step()
+    torch.cuda.synchronize(dev)
     stages, calls = m.stage_times()
     m.set_profiling(False)
+    # a step may run as several sub-batch calls (PSTEREO_DEVICE_CHUNKS)
+    pairs_per_call = B * prof_steps / max(calls, 1)
     ms_max = max_over_ranks(ms, device=dev)
     value = world * B * args.steps / (ms_max / 1e3)
 
@@ -314,7 +325,7 @@ def run_ours(args):
     npatch_f = len(_axis(w_f, s_, st_)) * len(_axis(h_f, s_, st_))
     # read the left/right/gradient fp32 planes (12 B/px)
     # and the coarser records (16 B/patch), write the records (32 B/patch)
-    alg_bytes = B * (12.0 * w_f * h_f + 48.0 * npatch_f)
+    alg_bytes = pairs_per_call * (12.0 * w_f * h_f + 48.0 * npatch_f)
     patch_ms = stages.get(f"patches_e{e_f}", 0.0) / max(calls, 1)
     achieved = alg_bytes / (patch_ms / 1e3) / 1e9 if patch_ms > 0 else 0.0
     traffic = None
@@ -322,7 +333,7 @@ def run_ours(args):
     tj = ROOT / "profiles" / "ncu_traffic.json"
     if tj.exists():
         t = json.loads(tj.read_text())["k_patches_finest"]
-        traffic = t["dram_bytes_per_launch"] / t["pairs_in_launch"] * B
+        traffic = t["dram_bytes_per_launch"] / t["pairs_in_launch"] * pairs_per_call
         if "fp64_inst_per_launch" in t and patch_ms > 0:
             # the pipes this kernel actually runs on: FP64 (DADD/DMUL/DFMA) and
             # XU (float<->double/int conversions); counts from ncu for the same
@@ -330,8 +341,10 @@ def run_ours(args):
             # are this box's measured per-SM rates (scripts/microbench.cu:
             # DADD 62.6, F2F 15.5 thread-ops/clk/SM) x 148 SMs x max clock
             sm_hz = 148 * 1965e6
-            f_ops = t["fp64_inst_per_launch"] / t["pairs_in_launch"] * B / (patch_ms / 1e3)
-            x_ops = t["conversion_inst_per_launch"] / t["pairs_in_launch"] * B / (patch_ms / 1e3)
+            f_ops = (t["fp64_inst_per_launch"] / t["pairs_in_launch"] * pairs_per_call
+                     / (patch_ms / 1e3))
+            x_ops = (t["conversion_inst_per_launch"] / t["pairs_in_launch"] * pairs_per_call
+                     / (patch_ms / 1e3))
             fp64 = {"unit": "T thread-inst/s",
                     "fp64_achieved": f_ops / 1e12, "fp64_peak": 62.6 * sm_hz / 1e12,
                     "fp64_frac": f_ops / (62.6 * sm_hz),
@@ -361,14 +374,17 @@ def run_ours(args):
                      "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                      "traffic": traffic, "peak_kind": peak_kind,
                      "alg_bytes_per_launch": alg_bytes, "launch_ms": patch_ms,
-                     "kernel_share_of_step": patch_ms / step_ms,
+                     "pairs_per_launch": pairs_per_call,
+                     "kernel_share_of_step": patch_ms * calls / prof_steps / step_ms,
                      "pipes": fp64,
                      "note": "not HBM-bound: a latency/issue-bound FP64 mirror of the "
                              "reference's double arithmetic (ncu: issue 47%, FP64 34%, XU 42%; "
                              "DESIGN.md section 4, profiles/r01)"},
         "path_roofline": {"bytes_per_pair": b_pair, "roofline_pairs_s": hbm * 1e9 / b_pair,
                           "frac": value / (world * hbm * 1e9 / b_pair)},
-        "stage_ms_per_step": {k: v / max(calls, 1) for k, v in stages.items()},
+        "stage_ms_per_step": {k: v / prof_steps for k, v in stages.items()},
+        "stage_note": "instrumented pass (stage events serialise launches), outside the timed "
+                      "region",
         "clocks": clk,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

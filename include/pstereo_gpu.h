@@ -226,6 +226,11 @@ int pstereo_gpu_last_launch_count(const pstereo_ctx* ctx);
  * *n_calls calls. Stages: h2d, pyramid, patches_e<exp> per level (coarsest
  * first), finalize, d2h; names via pstereo_gpu_stage_name. */
 int pstereo_gpu_set_profiling(pstereo_ctx* ctx, int enable);
+/* Device-buffer calls of n pairs run as `chunks` sub-batches alternating over
+ * two compute streams (their coarse levels and finalize overlap the other
+ * sub-batch's finest level); 0 or 1 = one launch sequence. Results are
+ * identical either way. Default: PSTEREO_DEVICE_CHUNKS or 2. */
+int pstereo_gpu_set_device_chunks(pstereo_ctx* ctx, int chunks);
 int pstereo_gpu_stage_times(pstereo_ctx* ctx, double* ms_total, int cap, int* n_calls);
 const char* pstereo_gpu_stage_name(const pstereo_ctx* ctx, int stage);
 

@@ -149,6 +149,7 @@ def lib() -> C.CDLL:
         L.pstereo_gpu_destroy.argtypes = [C.c_void_p]
         L.pstereo_gpu_last_launch_count.argtypes = [C.c_void_p]
         L.pstereo_gpu_set_profiling.argtypes = [C.c_void_p, C.c_int]
+        L.pstereo_gpu_set_device_chunks.argtypes = [C.c_void_p, C.c_int]
         L.pstereo_gpu_stage_times.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.c_int, i32p]
         L.pstereo_gpu_match_u8.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
                                            C.c_void_p, C.c_void_p, C.c_int, C.c_double,
@@ -232,7 +233,7 @@ ABI_SYMBOLS = [
     "pstereo_gpu_destroy", "pstereo_gpu_last_error", "pstereo_gpu_match_u8",
     "pstereo_gpu_match_f32", "pstereo_gpu_last_launch_count", "pstereo_gpu_set_profiling",
     "pstereo_gpu_stage_times", "pstereo_gpu_stage_name", "pstereo_synth_default",
-    "pstereo_gpu_synth", "pstereo_synth_last_error", "pstereo_gpu_render",
+    "pstereo_gpu_synth", "pstereo_synth_last_error", "pstereo_gpu_set_device_chunks", "pstereo_gpu_render",
     "pstereo_render_last_error", "pstereo_scene_default", "pstereo_scene_validate",
     "pstereo_load_scene_spec", "pstereo_load_calibration", "pstereo_load_image",
     "pstereo_write_pfm", "pstereo_read_pfm", "pstereo_metrics_csv_header",
@@ -578,6 +579,10 @@ class Matcher:
 
     def launch_count(self) -> int:
         return lib().pstereo_gpu_last_launch_count(self._h)
+
+    def set_device_chunks(self, chunks: int):
+        """Sub-batches per device call (pstereo_gpu_set_device_chunks)."""
+        lib().pstereo_gpu_set_device_chunks(self._h, int(chunks))
 
     def set_profiling(self, on: bool):
         lib().pstereo_gpu_set_profiling(self._h, int(on))

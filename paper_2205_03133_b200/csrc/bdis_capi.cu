@@ -230,6 +230,7 @@ struct pstereo_ctx {
   int out_parity = 0;
   // host-buffer pipeline (chunked H2D / compute / D2H)
   int chunk_pairs = 0;
+  int device_chunks = 2;  // sub-batches of a device call (PSTEREO_DEVICE_CHUNKS)
   cudaStream_t s_in = nullptr, s_out = nullptr, s_comp = nullptr;
   // compute_metrics staging
   DevBuf<double> met_f64;
@@ -409,6 +410,7 @@ int pstereo_gpu_create(int device, const pstereo_params* p, int max_width, int m
   }
   for (auto& sc : ctx->scr) sc.levels.resize(size_t(p->coarsest_exp) + 1);
   if (const char* v = getenv("PSTEREO_CHUNK_PAIRS")) ctx->chunk_pairs = atoi(v);
+  if (const char* v = getenv("PSTEREO_DEVICE_CHUNKS")) ctx->device_chunks = atoi(v);
   if (const char* v = getenv("PSTEREO_DEBUG_TIMELINE")) ctx->timeline = atoi(v) != 0;
   *out = ctx;
   return PSTEREO_OK;
@@ -512,6 +514,12 @@ int pstereo_gpu_metrics(pstereo_ctx* ctx, int n, int w, int h, const double* est
   CK(cudaMemcpyAsync(out, ctx->met_out.p, sizeof(pstereo_frame_metrics) * n,
                      cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  return PSTEREO_OK;
+}
+
+int pstereo_gpu_set_device_chunks(pstereo_ctx* ctx, int chunks) {
+  if (!ctx || chunks < 0) return PSTEREO_EINTERNAL;
+  ctx->device_chunks = chunks;
   return PSTEREO_OK;
 }
 
@@ -931,6 +939,12 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
     chunk = ctx->chunk_pairs > 0 ? ctx->chunk_pairs : 32;
     if (chunk > n) chunk = n;
   }
+  // device path: optionally split the batch into sub-batches alternating over
+  // two compute streams, so one sub-batch's latency-bound coarse levels and
+  // finalize overlap the other's finest level
+  const bool split = !pipelined && left_u8 && ctx->device_chunks > 1 &&
+                     n >= 16 * ctx->device_chunks;
+  if (split) chunk = (n + ctx->device_chunks - 1) / ctx->device_chunks;
   // device input regions
   const uint8_t* dev_u8[2] = {left_u8, right_u8};
   if (left_u8 && host_in)
@@ -952,7 +966,7 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
       dev_out[q] = ctx->out_stage[ctx->out_parity][q].p;
     }
   }
-  if (pipelined && !ctx->s_in) {
+  if ((pipelined || split) && !ctx->s_in) {
     CK(cudaStreamCreateWithFlags(&ctx->s_in, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&ctx->s_out, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&ctx->s_comp, cudaStreamNonBlocking));
@@ -984,7 +998,7 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
     cudaEventRecord(e, t);
     ctx->tl.emplace_back(what, e);
   };
-  if (pipelined) {
+  if (pipelined || split) {
     // the helper streams start behind the work already queued on the caller's stream
     CK(cudaEventRecord(ev_start, s));
     for (cudaStream_t t : {ctx->s_in, ctx->s_comp, ctx->s_out}) CK(cudaStreamWaitEvent(t, ev_start, 0));
@@ -994,7 +1008,7 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
     const int c0 = starts[size_t(c)], nc = starts[size_t(c) + 1] - c0;
     const size_t px0 = size_t(n_full) * c0, pxc = size_t(n_full) * nc;
     // consecutive chunks alternate between two compute streams / working sets
-    const int slot = pipelined ? (c & 1) : 0;
+    const int slot = (pipelined || split) ? (c & 1) : 0;
     cudaStream_t cs = slot ? ctx->s_comp : s;
     used_comp = used_comp || slot;
     if (pipelined) {
