@@ -14,4 +14,10 @@ g++ -std=gnu++20 -O2 -I"$REF/include" -I"$ROOT/include" "$ROOT/tests/cpp/dropin_
   "$O/spatial_mask.o" "$O/coarse_to_fine.o" "$O/depth_variance.o" "$O/pipeline.o" \
   -L"$ROOT/paper_2205_03133_b200" -lpstereo_gpu -Wl,-rpath,'$ORIGIN/../paper_2205_03133_b200' \
   -lpthread -o "$ROOT/build/dropin_parity"
-echo "built $ROOT/build/dropin_parity"
+g++ -std=gnu++20 -O2 -I"$REF/include" -I"$ROOT/include" "$ROOT/tests/cpp/dropin_bench.cpp" \
+  "$O/image.o" "$O/pyramid.o" "$O/patch.o" "$O/lk_solver.o" "$O/window_posterior.o" \
+  "$O/spatial_mask.o" "$O/coarse_to_fine.o" "$O/depth_variance.o" "$O/pipeline.o" \
+  "$O/metrics.o" "$O/synth.o" "$O/bench.o" "$O/ref_glue.o" \
+  -L"$ROOT/paper_2205_03133_b200" -lpstereo_gpu -Wl,-rpath,'$ORIGIN/../paper_2205_03133_b200' \
+  -lpthread -o "$ROOT/build/dropin_bench"
+echo "built $ROOT/build/dropin_parity $ROOT/build/dropin_bench"

@@ -25,3 +25,14 @@ def test_cpp_dropin_matches_reference(gpu, config, seed, size):
     print(r.stdout, r.stderr)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "identical" in r.stdout
+
+
+def test_cpp_dropin_caller_side_matches_reference(gpu):
+    """render_scene + run_benchmark: reference vs shim from one C++ caller."""
+    exe = EXE.parent / "dropin_bench"
+    if not exe.exists():
+        pytest.skip("build/dropin_bench not built (needs /root/reference at build time)")
+    r = subprocess.run([str(exe), "320", "240"], capture_output=True, text=True, timeout=600)
+    print(r.stdout, r.stderr)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "identical" in r.stdout
