@@ -11,12 +11,16 @@
 // Per chunk of pairs, four launches:
 //   k_syn_hblur   CTA per (row, pair): the row's white noise (edge-clamped,
 //                 r extra columns either side) into smem, horizontal taps
-//   k_syn_vblur   32x8 pixels per CTA: vertical taps through L1, per-pair
-//                 min/max of the blurred field (order-free: exact)
+//   k_syn_vblur_tile  32 columns x 64 rows per CTA: the column strip staged
+//                 in smem, sliding window of 8 outputs per thread (each input
+//                 row loaded once), per-pair min/max of the blurred field
+//                 (order-free: exact); k_syn_vblur (taps through L1) when the
+//                 strip does not fit
 //   k_syn_discs   (stress only) CTA per pair: the sequential disc placement
 //                 loop with a per-pair coverage map, one disc per iteration
-//   k_syn_views   CTA per (row, pair): texture row into smem (left view),
-//                 then the right view sampled from it at x + d plus noise
+//   k_syn_views   CTA per (row, pair): the row's value-noise lattice into
+//                 smem, texture row into smem (left view), then the right view
+//                 sampled from it at x + d plus noise
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -106,6 +110,69 @@ __global__ void k_syn_vblur(SynthDev S) {
   }
 }
 
+// The same vertical pass with the column strip staged in shared memory and
+// a sliding window: each thread produces kVR consecutive rows of one column,
+// loading each input row once; output o takes its taps in ascending order as
+// the input row advances, so every sum is the host's, rounding for rounding.
+constexpr int kVR = 8;   // rows per thread
+constexpr int kVW = 8;   // warps per CTA -> 64 rows per CTA
+
+__global__ void __launch_bounds__(32 * kVW) k_syn_vblur_tile(SynthDev S) {
+  extern __shared__ float sm_t[];
+  const int p = blockIdx.z;
+  const int lane = threadIdx.x, warp = threadIdx.y;
+  const int w = S.w, h = S.h, r = S.r, taps = 2 * r + 1;
+  const int tpad = (taps + 31) & ~31;
+  float* kw = sm_t;
+  float* tile = sm_t + tpad;  // [(kVR * kVW + 2r) rows][32]
+  const int tid = warp * 32 + lane, nt = 32 * kVW;
+  const int x0 = blockIdx.x * 32, y_cta = blockIdx.y * (kVR * kVW);
+  const int rows = kVR * kVW + 2 * r;
+  const float* src = S.tmp + (size_t)p * h * w;
+  for (int i = tid; i < taps; i += nt) kw[i] = S.weights[i];
+  for (int q = tid; q < rows * 32; q += nt) {
+    const int rr = q >> 5, c = q & 31;
+    int ys = y_cta - r + rr;
+    ys = ys < 0 ? 0 : (ys >= h ? h - 1 : ys);
+    const int xs = min(x0 + c, w - 1);
+    tile[q] = src[(size_t)ys * w + xs];
+  }
+  __syncthreads();
+  float acc[kVR];
+#pragma unroll
+  for (int o = 0; o < kVR; ++o) acc[o] = 0.0f;
+  const float* col = tile + warp * kVR * 32 + lane;
+  // input row jj (tile-relative to this warp) feeds output o with tap jj - o
+  for (int jj = 0; jj < kVR - 1 + taps; ++jj) {
+    const float v = col[jj * 32];
+#pragma unroll
+    for (int o = 0; o < kVR; ++o) {
+      const int i = jj - o;
+      if (i >= 0 && i < taps) acc[o] = __fadd_rn(acc[o], __fmul_rn(kw[i], v));
+    }
+  }
+  const int x = x0 + lane;
+  unsigned mn_inv = 0u, mx = 0u;
+#pragma unroll
+  for (int o = 0; o < kVR; ++o) {
+    const int y = y_cta + warp * kVR + o;
+    if (x < w && y < h) {
+      S.fld[((size_t)p * h + y) * w + x] = acc[o];
+      const unsigned b = __float_as_uint(acc[o]);  // acc >= 0: bit order = value order
+      mn_inv = max(mn_inv, ~b);
+      mx = max(mx, b);
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    mn_inv = max(mn_inv, __shfl_xor_sync(0xffffffffu, mn_inv, o));
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  if (lane == 0) {
+    atomicMax(S.minmax + 2 * p, mn_inv);
+    atomicMax(S.minmax + 2 * p + 1, mx);
+  }
+}
+
 // pstereo_synth_discs (csrc/synth.c): discs are placed one after another
 // until 30% of the pixels are covered; a disc's newly covered pixels are
 // counted in parallel (each pixel belongs to one thread, so the count equals
@@ -158,6 +225,53 @@ __global__ void k_syn_discs(SynthDev S) {
   if (threadIdx.x == 0) S.n_discs[p] = nd;
 }
 
+// Value-noise lattice of one image row, octave by octave: the corner values
+// syn_unit3(ok, ix, iy) and (ix, iy + 1) for every lattice column the row
+// touches, so each pixel reads four cached doubles instead of hashing twelve
+// splitmix rounds per octave. Same values, same arithmetic as syn_value_noise.
+struct Lattice {
+  int oct;                  // octaves
+  int off[16];              // first entry of octave o (entries of 2 doubles)
+  long long ixlo[16];       // lattice column of entry 0 of octave o
+};
+
+__host__ __device__ inline int lattice_entries(int w, int octaves, double base, Lattice* L) {
+  int total = 0;
+  double wl = base;
+  for (int o = 0; o < octaves; ++o) {
+    const long long lo = (long long)floor(0.5 / wl);
+    const long long hi = (long long)floor(((double)(w - 1) + 0.5) / wl);
+    if (L) {
+      L->off[o] = total;
+      L->ixlo[o] = lo;
+    }
+    total += (int)(hi - lo + 2);
+    wl *= 0.5;
+  }
+  if (L) L->oct = octaves;
+  return total;
+}
+
+__device__ __forceinline__ double value_noise_cached(double x, double y, const Lattice& L,
+                                                     const double* lat, double wavelength) {
+  double sum = 0.0, norm = 0.0, amp = 1.0;
+  for (int o = 0; o < L.oct; ++o) {
+    const double gx = x / wavelength, gy = y / wavelength;
+    const double fx = floor(gx), fy = floor(gy);
+    const double tx = syn_smooth(gx - fx), ty = syn_smooth(gy - fy);
+    const double* e = lat + 2 * (L.off[o] + (int)((long long)fx - L.ixlo[o]));
+    const double v00 = e[0], v01 = e[1], v10 = e[2], v11 = e[3];
+    const double v = (1.0 - ty) * ((1.0 - tx) * v00 + tx * v10) +
+                     ty * ((1.0 - tx) * v01 + tx * v11);
+    sum += amp * v;
+    norm += amp;
+    amp *= 0.5;
+    wavelength *= 0.5;
+  }
+  return sum / norm;
+}
+
+template <bool kCache>
 __global__ void k_syn_views(SynthDev S) {
   extern __shared__ double sm_d[];
   const int y = blockIdx.x, p = blockIdx.y;
@@ -167,7 +281,27 @@ __global__ void k_syn_views(SynthDev S) {
   double* tex = sm_d;                              // [w][C]
   double* dsc = tex + (size_t)w * C;               // [4][nd] (cx, cy, r, val planes)
   double* blob = dsc + 4 * SYN_MAX_DISCS;          // [2 views][3][SYN_BLOBS]
+  double* lat = blob + 2 * 3 * SYN_BLOBS;          // [C][entries][2] (kCache)
   __shared__ double hp[3];
+  Lattice L;
+  int n_ent = 0;
+  if (kCache) {
+    n_ent = lattice_entries(w, S.octaves, S.wavelength, &L);
+    const double yc = y + 0.5;
+    for (int q = threadIdx.x; q < C * n_ent; q += blockDim.x) {
+      const int c = q / n_ent, k = q - c * n_ent;
+      int o = 0;
+      while (o + 1 < L.oct && k >= L.off[o + 1]) ++o;
+      double wl = S.wavelength;
+      for (int t = 0; t < o; ++t) wl *= 0.5;
+      const long long ix = L.ixlo[o] + (k - L.off[o]);
+      const long long iy = (long long)floor(yc / wl);
+      const uint64_t ok = syn_mix64(syn_channel_key(key, c) + (uint64_t)o * 0x1000193ull);
+      double* e = lat + 2 * ((size_t)c * n_ent + k);
+      e[0] = syn_unit3(ok, (uint64_t)ix, (uint64_t)iy);
+      e[1] = syn_unit3(ok, (uint64_t)ix, (uint64_t)(iy + 1));
+    }
+  }
   if (S.stress) {
     const double* rec = S.discs + (size_t)p * SYN_MAX_DISCS * 4;
     for (int i = threadIdx.x; i < 4 * nd; i += blockDim.x)
@@ -194,8 +328,19 @@ __global__ void k_syn_views(SynthDev S) {
       if (hp[0] * x + hp[1] * y > hp[2]) dark = 0.4;
     }
     for (int c = 0; c < C; ++c) {
-      const double v = syn_texture(x, y, syn_channel_key(key, c), S.octaves, S.wavelength, nd,
-                                   dcx, dcy, drr, dvl);
+      double v;
+      if (kCache) {
+        // syn_texture with the cached lattice
+        v = 255.0 * value_noise_cached(x + 0.5, y + 0.5, L, lat + 2 * (size_t)c * n_ent,
+                                       S.wavelength);
+        for (int k = 0; k < nd; ++k) {
+          const double dx = x - dcx[k], dy = y - dcy[k];
+          if (dx * dx + dy * dy <= drr[k] * drr[k]) v = dvl[k];
+        }
+      } else {
+        v = syn_texture(x, y, syn_channel_key(key, c), S.octaves, S.wavelength, nd, dcx, dcy,
+                        drr, dvl);
+      }
       tex[(size_t)x * C + c] = v;
       S.left[(row0 + x) * C + c] = syn_finish(v, gain0, dark, spec);
     }
@@ -254,15 +399,28 @@ extern "C" int pstereo_gpu_synth(int device, const pstereo_synth_spec* s, int n_
   pstereo_synth_blur_weights(s->blur_sigma, kw.data(), 2 * r + 1);
   const size_t smem_h = sizeof(float) * ((size_t)(2 * r + 1) + (size_t)(w + 2 * r));
   const size_t smem_v = sizeof(float) * (size_t)(2 * r + 1);
+  const size_t smem_vt =
+      sizeof(float) * ((size_t)((2 * r + 1 + 31) & ~31) + (size_t)(kVR * kVW + 2 * r) * 32);
   const size_t smem_views =
       sizeof(double) * ((size_t)w * C + 4 * SYN_MAX_DISCS + 2 * 3 * SYN_BLOBS);
+  const size_t smem_views_c =
+      smem_views + sizeof(double) * 2 * (size_t)C *
+                       (size_t)lattice_entries(w, s->octaves, s->base_wavelength, nullptr);
+  const bool vcache = s->octaves <= 16 && smem_views_c <= 200 * 1024;
   const size_t smem_cap = 227 * 1024;
   if (smem_h > smem_cap || smem_views > smem_cap)
     return fail(PSTEREO_ECONFIG, "pstereo_gpu_synth: width or blur radius too large");
   cudaFuncSetAttribute(k_syn_hblur, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_h);
   cudaFuncSetAttribute(k_syn_vblur, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_v);
-  cudaFuncSetAttribute(k_syn_views, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  const bool vtile = smem_vt <= smem_cap;
+  if (vtile)
+    cudaFuncSetAttribute(k_syn_vblur_tile, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem_vt);
+  cudaFuncSetAttribute(k_syn_views<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)smem_views);
+  if (vcache)
+    cudaFuncSetAttribute(k_syn_views<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem_views_c);
 
   // chunked so the scratch stays bounded (~8.1 B per pixel per pair in flight)
   const int chunk = n_pairs < 64 ? n_pairs : 64;
@@ -317,9 +475,14 @@ extern "C" int pstereo_gpu_synth(int device, const pstereo_synth_spec* s, int n_
     if (e == cudaSuccess && s->stress) e = cudaMemsetAsync(S.cov, 0, px * m, st);
     if (e != cudaSuccess) break;
     k_syn_hblur<<<dim3(h, m), 256, smem_h, st>>>(S);
-    k_syn_vblur<<<dim3((w + 31) / 32, (h + 7) / 8, m), dim3(32, 8), smem_v, st>>>(S);
+    if (vtile)
+      k_syn_vblur_tile<<<dim3((w + 31) / 32, (h + kVR * kVW - 1) / (kVR * kVW), m),
+                         dim3(32, kVW), smem_vt, st>>>(S);
+    else
+      k_syn_vblur<<<dim3((w + 31) / 32, (h + 7) / 8, m), dim3(32, 8), smem_v, st>>>(S);
     if (s->stress) k_syn_discs<<<m, 512, 0, st>>>(S);
-    k_syn_views<<<dim3(h, m), 128, smem_views, st>>>(S);
+    if (vcache) k_syn_views<true><<<dim3(h, m), 128, smem_views_c, st>>>(S);
+    else k_syn_views<false><<<dim3(h, m), 128, smem_views, st>>>(S);
     e = cudaGetLastError();
   }
   cudaError_t e2 = cudaFreeAsync(base, st);
