@@ -343,6 +343,7 @@ Raster decode_png(const std::string& path, const std::vector<uint8_t>& b) {
   }
   if (ctype < 0 || W == 0 || H == 0 || W > (1u << 24) || H > (1u << 24))
     fail("PNG decode failed (no IHDR)");
+  if (uint64_t(W) * H > (uint64_t(1) << 28)) fail("PNG decode failed (image too large)");
   int spp = 0;  // samples per pixel in the file
   switch (ctype) {
     case 0: spp = 1; break;
