@@ -824,6 +824,10 @@ int run_device(pstereo_ctx* ctx, Scratch& sc, const std::vector<LevelGeom>& geo,
   cb.full_w = W;
   cb.full_h = H;
   cb.e = fe;
+  {
+    const long long mp = llround(std::ceil(prm.gamma * double(S) * double(S) - 1e-9));
+    cb.min_px = std::max(mp, 1ll);  // src/depth_variance.cpp:87-90
+  }
   launch_fuse_ccl(F, fb, ctx->mask.p, prm.estimate_variance, f64, cb, n, s);
   ctx->launches += 3;
 

@@ -597,6 +597,11 @@ __global__ void __launch_bounds__(kFuseThreads) k_fuse_ccl_local(
       cb.roots[tid * kTilePx] = root_gi;
       cb.nroots[tid] = 1;
     }
+    if (s_area[0] >= cb.min_px)
+      for (int i = 0; i < kFuseRows; ++i) {
+        const int y = ty0 + warp + i * kFuseWarps;
+        if (y < h && x < w) fb.flags[pbase + (long long)y * w + x] |= kFlagSure;
+      }
     return;
   }
   // one union per column segment where a run overlaps the run above it
@@ -649,6 +654,14 @@ __global__ void __launch_bounds__(kFuseThreads) k_fuse_ccl_local(
     }
   }
   __syncthreads();
+  for (int i = 0; i < kFuseRows; ++i) {
+    const int ly = warp + i * kFuseWarps;
+    const unsigned bits = s_bits[ly];
+    if (!((bits >> lane) & 1u)) continue;
+    const int root = uf_find(sl, run_start(bits, ly, lane));
+    if (s_area[root] >= cb.min_px)
+      fb.flags[pbase + (long long)(ty0 + ly) * w + x] |= kFlagSure;
+  }
   for (int i = 0; i < kFuseRows; ++i) {
     const int ly = warp + i * kFuseWarps;
     const int idx = ly * kTileW + lane;
@@ -728,7 +741,9 @@ __global__ void k_output(OutputArgs a) {
   const uint8_t fl = a.fb.flags[f];
   const bool mv = fl & kFlagMatch;
   bool keep = false;
-  if (fl & kFlagKeep) {  // local root -> global root (k_ccl_merge) -> component area
+  if (fl & kFlagSure) {
+    keep = true;
+  } else if (fl & kFlagKeep) {  // local root -> global root (k_ccl_merge) -> component area
     const int* lab = a.label + pair * a.fplane;
     keep = a.area[pair * a.fplane + lab[lab[i]]] >= a.min_px;
   }
@@ -839,7 +854,7 @@ __global__ void __launch_bounds__(256) k_output_x4(OutputArgs a) {
   for (int k = 0; k < 4; ++k) {
     mv |= (unsigned)((fls[k] & kFlagMatch) != 0) << k;
     if (fls[k] & kFlagKeep) {  // local root -> global root -> component area
-      const bool kp = area[lab[lab[fy * a.fw + fx + k]]] >= a.min_px;
+      const bool kp = (fls[k] & kFlagSure) || area[lab[lab[fy * a.fw + fx + k]]] >= a.min_px;
       keep |= (unsigned)kp << k;
       dv |= (unsigned)(kp && (fls[k] & kFlagDepth)) << k;
     }

@@ -118,7 +118,10 @@ struct FinestBufs {
   uint8_t* flags;
   double scale_d, scale_v, fb, threshold;
 };
-enum FinestFlag : uint8_t { kFlagMatch = 1, kFlagKeep = 2, kFlagDepth = 4 };
+// kFlagSure: kept, and the pixel's tile-local component alone already meets
+// the area rule (its global component is a superset), so k_output needs no
+// label lookup for it
+enum FinestFlag : uint8_t { kFlagMatch = 1, kFlagKeep = 2, kFlagDepth = 4, kFlagSure = 8 };
 
 // component labelling state at the finest level (per pair: one plane of
 // labels and areas, ccl_tiles() root lists of ccl_tile_px() entries)
@@ -128,6 +131,7 @@ struct CclBufs {
   int* roots;   // [pair][tile][ccl_tile_px()] tile-local roots (global indices)
   int* nroots;  // [pair][tile]
   int full_w, full_h, e;
+  long long min_px;  // area rule of filter_validity, in full-resolution pixels
 };
 int ccl_tiles(int w, int h);
 int ccl_tile_px();
