@@ -534,7 +534,7 @@ __global__ void __launch_bounds__(kFuseThreads) k_fuse_ccl_local(
       }
       // upsample_to_full values (:166-180): scale 2^fe, 1, 4^fe where valid, else 0
       const double D = valid ? __dmul_rn(fb.scale_d, d) : 0.0;
-      const double Pv = valid ? __dmul_rn(1.0, p) : 0.0;
+      const double Pv = valid ? p : 0.0;  // scale 1: p * 1.0 == p exactly
       const double V = valid ? __dmul_rn(fb.scale_v, v) : 0.0;
       const bool deep = D >= 0.1;  // kMinDisparity (inc/depth_variance.hpp:13)
       keep = valid && !(Pv < fb.threshold);  // filter_validity threshold (:84)
