@@ -269,6 +269,35 @@ def test_async_host_calls_overlap_safely(gpu):
         assert np.array_equal(np.nan_to_num(a), np.nan_to_num(b))
 
 
+def test_device_sub_batches_are_invisible(gpu):
+    """A device call split into sub-batches over two compute streams
+    (pstereo_gpu_set_device_chunks, default 2 for >= 32 pairs) writes exactly
+    what one launch sequence writes, for any split."""
+    import torch
+
+    P = gpu
+    n, w, h = 70, 160, 120
+    cfg = P.PipelineConfig(coarsest_exp=3, finest_exp=1, patch_size=8, overlap=0.5,
+                           estimate_variance=True)
+    dl, dr = P.synth_batch_gpu(1, n, seed0=300, width=w, height=h)
+    names = ("disparity", "disparity_valid", "depth", "depth_sigma", "var_disp")
+    res = {}
+    with P.Matcher(cfg, w, h, n) as m:
+        for chunks in (1, 2, 3, 5):
+            m.set_device_chunks(chunks)
+            outs = {k: torch.full((n, h, w), 7, dtype=torch.uint8 if "valid" in k
+                                  else torch.float64, device="cuda") for k in names}
+            m.run_device_u8(n, w, h, 1, dl.data_ptr(), dr.data_ptr(),
+                            {k: v.data_ptr() for k, v in outs.items()}, dtype=P.F64,
+                            focal=500.0, baseline=5.0)
+            torch.cuda.synchronize()
+            res[chunks] = {k: v.cpu().numpy() for k, v in outs.items()}
+    for chunks in (2, 3, 5):
+        for k in names:
+            a, b = res[1][k], res[chunks][k]
+            assert np.array_equal(a.view(np.uint8), b.view(np.uint8)), (chunks, k)
+
+
 def test_invalid_value_fill(gpu):
     """fill_invalid writes the PFM-style sentinel (src/io.cpp:297-310) into
     invalid disparity/depth pixels and leaves valid ones untouched."""
