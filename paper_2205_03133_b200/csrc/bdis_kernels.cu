@@ -701,7 +701,13 @@ __global__ void k_ccl_border(int w, int h, long long plane, const uint8_t* __res
   int* l = lab + base;
   volatile int* vl = l;
   const int j = left ? i - 1 : i - w;
-  if (mask[base + j] & kFlagKeep) uf_union(vl, l, i, j);
+  if (!(mask[base + j] & kFlagKeep)) return;
+  // start from the tile-local roots; neighbouring border threads mostly join
+  // the same pair of components, so one lane per distinct pair does the union
+  const int a = l[i], b = l[j];
+  const unsigned long long key = ((unsigned long long)(unsigned)a << 32) | (unsigned)b;
+  const unsigned peers = __match_any_sync(__activemask(), key);
+  if ((threadIdx.x & 31) == __ffs(peers) - 1) uf_union(vl, l, a, b);
 }
 
 // one warp per tile: every tile-local root adds its area to its global root
