@@ -272,8 +272,9 @@ int pstereo_synth_batch(const pstereo_synth_spec* s, int n_pairs,
  * disparity [n_pairs][height][width] -- byte-for-byte what
  * pstereo_synth_pair produces on the host for the same (spec, seed): both
  * evaluate csrc/synth_core.h with IEEE-exact operations only. Enqueued on
- * `stream` (a cudaStream_t, NULL = legacy default); scratch comes from the
- * stream-ordered allocator. Returns PSTEREO_OK, PSTEREO_ECONFIG (bad spec)
+ * `stream` (a cudaStream_t, NULL = legacy default) after the blur taps are
+ * uploaded (which waits for the stream's earlier work); scratch comes from
+ * the stream-ordered allocator. Returns PSTEREO_OK, PSTEREO_ECONFIG (bad spec)
  * or PSTEREO_EINTERNAL; the message is in pstereo_synth_last_error(). */
 int pstereo_gpu_synth(int device, const pstereo_synth_spec* s, int n_pairs,
                       uint64_t seed0, uint8_t* left, uint8_t* right,
@@ -319,7 +320,8 @@ int pstereo_load_scene_spec(const char* path, pstereo_scene_spec* out, char* msg
 /* render_scene (src/synth.cpp:209-284) for n_scenes scenes of one size on
  * the device: DEVICE buffers left/right fp32 [n][h][w] (GrayImage, all
  * valid) and, when non-NULL, the reference disparity / depth fields as
- * doubles [n][h][w] (all valid). Enqueued on `stream`. */
+ * doubles [n][h][w] (all valid). Enqueued on `stream` after the specs are
+ * uploaded (which waits for the stream's earlier work). */
 int pstereo_gpu_render(int device, const pstereo_scene_spec* specs, int n_scenes,
                        float* left, float* right, double* ref_disparity,
                        double* ref_depth, void* stream);

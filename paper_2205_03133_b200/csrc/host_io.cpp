@@ -303,7 +303,8 @@ uint8_t paeth(int a, int b, int c) {
   return uint8_t(c);
 }
 
-Raster decode_png(const std::string& path, const std::vector<uint8_t>& b) {
+Raster decode_png(const std::string& path, const std::vector<uint8_t>& b,
+                  bool header_only = false) {
   auto fail = [&](const std::string& why) { io_error(path + ": " + why); };
   size_t pos = 8;
   uint32_t W = 0, H = 0;
@@ -359,6 +360,16 @@ Raster decode_png(const std::string& path, const std::vector<uint8_t>& b) {
                         ((ctype == 2 || ctype == 4 || ctype == 6) && (depth == 8 || depth == 16));
   if (!depth_ok) fail("PNG decode failed (bit depth)");
   if (ctype == 3 && (plte.empty() || plte.size() % 3)) fail("PNG decode failed (PLTE)");
+  if (header_only) {  // dimensions and output channels without inflating the data
+    Raster r;
+    r.w = int(W);
+    r.h = int(H);
+    r.c = ctype == 3 ? (trns.empty() ? 3 : 4)
+          : ctype == 0 ? (trns.size() >= 2 ? 4 : 1)
+          : ctype == 2 ? (trns.size() >= 6 ? 4 : 3)
+          : 4;
+    return r;
+  }
   const int bpp_bits = spp * depth;
   const size_t filt_bpp = size_t(std::max(1, bpp_bits / 8));
   // inflate
@@ -506,11 +517,12 @@ Raster decode_png(const std::string& path, const std::vector<uint8_t>& b) {
   return r;
 }
 
-// load_image, src/io.cpp:253-263
-Raster load_image(const std::string& path) {
+// load_image, src/io.cpp:253-263 (header_only: dimensions and channels)
+Raster load_image(const std::string& path, bool header_only = false) {
   const std::vector<uint8_t> b = read_bytes(path);
   static const uint8_t sig[8] = {0x89, 'P', 'N', 'G', '\r', '\n', 0x1A, '\n'};
-  if (b.size() >= 8 && std::memcmp(b.data(), sig, 8) == 0) return decode_png(path, b);
+  if (b.size() >= 8 && std::memcmp(b.data(), sig, 8) == 0)
+    return decode_png(path, b, header_only);
   if (b.size() >= 2 && b[0] == 'P' && (b[1] == '5' || b[1] == '6')) return decode_pnm(path, b);
   io_error(path + ": unrecognized image format (PNG/PGM/PPM supported)");
 }
@@ -653,7 +665,7 @@ int pstereo_load_calibration(const char* path, double* focal_px, double* baselin
 int pstereo_load_image(const char* path, int* width, int* height, int* channels,
                        uint8_t* pixels, size_t cap, char* msg, size_t msg_cap) {
   return guarded(msg, msg_cap, [&] {
-    const Raster r = load_image(path);
+    const Raster r = load_image(path, pixels == nullptr);
     *width = r.w;
     *height = r.h;
     *channels = r.c;
