@@ -111,3 +111,34 @@ def test_benchmark_flow_matches_reference(gpu, ref, variance):
         for v in ms:
             acc += v
         assert agg["mean_err"] == acc / len(ms)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_randomized_scenes(gpu, ref, seed):
+    """Random valid SceneSpecs (every surface / texture / shading, noise, camera,
+    sizes): fields bit-identical, views within the libm ulp rule."""
+    rng = np.random.default_rng(1000 + seed)
+    specs = []
+    w, h = int(rng.integers(24, 200)), int(rng.integers(16, 150))
+    for _ in range(6):
+        surface = ["plane", "slanted_plane", "sphere"][int(rng.integers(3))]
+        kw = dict(width=w, height=h, surface=surface,
+                  texture=["perlin", "checker", "constant"][int(rng.integers(3))],
+                  shading=["diffuse", "nonlambertian"][int(rng.integers(2))],
+                  noise_std=float(rng.choice([0.0, rng.uniform(0, 0.05)])),
+                  seed=int(rng.integers(0, 2**40)), focal_px=float(rng.uniform(200, 900)),
+                  baseline=float(rng.uniform(1, 10)), texture_scale=float(rng.uniform(4, 64)),
+                  texture_octaves=int(rng.integers(1, 9)), ambient=float(rng.uniform(0, 1)),
+                  highlight_strength=float(rng.uniform(0, 1)),
+                  highlight_falloff=float(rng.uniform(1, 12)))
+        if surface == "plane":
+            kw["disparity"] = float(rng.uniform(0.5, 30))
+        elif surface == "slanted_plane":
+            kw["disparity0"] = float(rng.uniform(2, 20))
+            kw["disparity_gradient"] = float(rng.uniform(-0.4, 0.4)) * min(1.0, kw["disparity0"] / w)
+        else:
+            kw["sphere_depth"] = float(rng.uniform(20, 80))
+            kw["sphere_radius"] = float(rng.uniform(2, 30))
+            kw["background_depth"] = kw["sphere_depth"] + float(rng.uniform(5, 80))
+        specs.append(gpu.scene_spec(**kw))
+    _compare(gpu, specs, ref)

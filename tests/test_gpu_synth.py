@@ -50,3 +50,18 @@ def test_chunk_boundary_and_empty(gpu):
 def test_bad_spec_is_config_error(gpu):
     with pytest.raises(gpu.ConfigError):
         gpu.synth_batch_gpu(0, 1, channels=2)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_randomized_specs(gpu, seed):
+    """Random generator specs (sizes, channels, octaves, wavelengths, blur,
+    disparity range, noise, stress): byte-identical to the host."""
+    rng = np.random.default_rng(2000 + seed)
+    for _ in range(3):
+        kw = dict(width=int(rng.integers(8, 300)), height=int(rng.integers(8, 200)),
+                  channels=int(rng.choice([1, 3])), octaves=int(rng.integers(1, 7)),
+                  base_wavelength=float(rng.uniform(2, 80)),
+                  d_min=float(rng.uniform(0, 10)), d_range=float(rng.uniform(0, 40)),
+                  blur_sigma=float(rng.uniform(0.5, 30)), noise_sigma=float(rng.uniform(0, 5)),
+                  stress=int(rng.integers(0, 2)))
+        _check(gpu, 0, int(rng.integers(1, 4)), int(rng.integers(0, 2**40)), **kw)

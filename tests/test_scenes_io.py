@@ -272,3 +272,31 @@ def test_calibration(built, tmp_path):
     f.write_text("focal_px = 500\nwidth = 640\nheight = 480\n")
     with pytest.raises(P.ConfigError, match="missing key"):
         P.load_calibration(f)
+
+
+def test_cli_usage_and_file_errors_without_gpu(built, tmp_path):
+    """pstereo_gpu_cli exit codes (inc/pstereo/runner.hpp:16-19) for errors that
+    happen before any device work: usage / config 2, unreadable files 3."""
+    import subprocess
+
+    import paper_2205_03133_b200 as P
+
+    cli = str(Path(P.__file__).resolve().parent / "pstereo_gpu_cli")
+
+    def run(*a):
+        return subprocess.run([cli, *map(str, a)], capture_output=True, text=True).returncode
+
+    assert run() == 2
+    assert run("frobnicate") == 2
+    assert run("match", "only_one.png") == 2
+    assert run("match", "a.png", "b.png") == 2                      # --calib missing
+    assert run("match", "a.png", "b.png", "--calib", "c.txt", "--patch-size", "x") == 2
+    assert run("match", "a.png", "b.png", "--calib", "c.txt", "--bogus", "1") == 2
+    assert run("match", "a.png", "b.png", "--calib", "c.txt", "--patch-size", "1") == 2
+    assert run("match", tmp_path / "no.png", tmp_path / "no2.png", "--calib", "c.txt") == 3
+    assert run("bench") == 2
+    assert run("bench", tmp_path / "missing_scene.txt") == 3
+    (tmp_path / "bad.txt").write_text("surface = cube\n")
+    assert run("bench", tmp_path / "bad.txt") == 2
+    (tmp_path / "cfg.ini").write_text("[bench]\nreps = zero\n")
+    assert run("--config", tmp_path / "cfg.ini", "bench", tmp_path / "bad.txt") == 2
