@@ -25,6 +25,7 @@
 
 #include <cstdint>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -54,26 +55,62 @@ struct SynthDev {
   float* disparity;      // [pair][h][w] or null
 };
 
+// Horizontal pass, four consecutive outputs per thread: the row's line is read
+// as float4 (one 16-byte load feeds four taps of four outputs) and the tap
+// weights rotate through registers. Output o of a thread takes tap jj - o at
+// input jj, in ascending order; out-of-range taps use zero weights, and since
+// every weight and every noise value is >= +0, adding +0 * v = +0 to a sum
+// that is >= +0 leaves it bit-identical -- the host's sums exactly.
+constexpr int kHPad = 4;   // zero weights before tap 0
+constexpr int kHTail = 8;  // zero weights after the last tap (the last block overruns by <= 5)
+
 __global__ void k_syn_hblur(SynthDev S) {
-  extern __shared__ float sm_h[];
+  extern __shared__ __align__(16) float sm_h[];
   const int y = blockIdx.x, p = blockIdx.y;
   const int w = S.w, r = S.r, taps = 2 * r + 1;
-  float* kw = sm_h;
-  float* line = sm_h + taps;
+  const int nline = ((w + 2 * r + 3) & ~3) + 8;           // float4-padded line
+  float* line = sm_h;
+  float* kw = sm_h + nline;                                // [kHPad zeros][taps][kHTail zeros]
   const uint64_t key = syn_pair_key(S.seed0 + (uint64_t)p);
-  for (int i = threadIdx.x; i < taps; i += blockDim.x) kw[i] = S.weights[i];
-  for (int i = threadIdx.x; i < w + 2 * r; i += blockDim.x) {
+  for (int i = threadIdx.x; i < taps + kHPad + kHTail; i += blockDim.x) {
+    const int t = i - kHPad;
+    kw[i] = (t >= 0 && t < taps) ? S.weights[t] : 0.0f;
+  }
+  for (int i = threadIdx.x; i < nline; i += blockDim.x) {
     int xs = i - r;
     xs = xs < 0 ? 0 : (xs >= w ? w - 1 : xs);
     line[i] = syn_white(key, xs, y);
   }
   __syncthreads();
   float* out = S.tmp + ((size_t)p * S.h + y) * w;
-  for (int x = threadIdx.x; x < w; x += blockDim.x) {
-    float acc = 0.0f;
-    const float* src = line + x;
-    for (int i = 0; i < taps; ++i) acc = __fadd_rn(acc, __fmul_rn(kw[i], src[i]));
-    out[x] = acc;
+  const float4* line4 = (const float4*)line;
+  const int nq = (w + 3) >> 2;
+  const int nblk = (taps + 3 + 3) >> 2;  // input steps jj = 0 .. taps + 2
+  for (int q = threadIdx.x; q < nq; q += blockDim.x) {
+    float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;
+    // k1..k3 = weights of taps jj-1, jj-2, jj-3 (zero before tap 0)
+    float k1 = 0.0f, k2 = 0.0f, k3 = 0.0f;
+    for (int b = 0; b < nblk; ++b) {
+      const float4 v4 = line4[q + b];
+      const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float k0 = kw[kHPad + 4 * b + u];  // tap jj = 4b + u
+        const float v = vv[u];
+        a0 = __fadd_rn(a0, __fmul_rn(k0, v));
+        a1 = __fadd_rn(a1, __fmul_rn(k1, v));
+        a2 = __fadd_rn(a2, __fmul_rn(k2, v));
+        a3 = __fadd_rn(a3, __fmul_rn(k3, v));
+        k3 = k2;
+        k2 = k1;
+        k1 = k0;
+      }
+    }
+    const int x = 4 * q;
+    out[x] = a0;
+    if (x + 1 < w) out[x + 1] = a1;
+    if (x + 2 < w) out[x + 2] = a2;
+    if (x + 3 < w) out[x + 3] = a3;
   }
 }
 
@@ -118,18 +155,24 @@ constexpr int kVR = 8;   // rows per thread
 constexpr int kVW = 8;   // warps per CTA -> 64 rows per CTA
 
 __global__ void __launch_bounds__(32 * kVW) k_syn_vblur_tile(SynthDev S) {
-  extern __shared__ float sm_t[];
+  extern __shared__ __align__(16) float sm_t[];
   const int p = blockIdx.z;
   const int lane = threadIdx.x, warp = threadIdx.y;
   const int w = S.w, h = S.h, r = S.r, taps = 2 * r + 1;
-  const int tpad = (taps + 31) & ~31;
-  float* kw = sm_t;
-  float* tile = sm_t + tpad;  // [(kVR * kVW + 2r) rows][32]
+  // weights with kVR-1 zeros before tap 0 and kVR+1 after: output o at input jj
+  // reads kwp[jj - o + kVR - 1]; the extra terms are +0 * v on sums >= +0
+  // (weights and field values are non-negative), i.e. bit-identities
+  const int nkw = (taps + 2 * kVR + 3) & ~3;
+  float* kwp = sm_t;
+  float* tile = sm_t + nkw;  // [(kVR * kVW + 2r) rows][32]
   const int tid = warp * 32 + lane, nt = 32 * kVW;
   const int x0 = blockIdx.x * 32, y_cta = blockIdx.y * (kVR * kVW);
   const int rows = kVR * kVW + 2 * r;
   const float* src = S.tmp + (size_t)p * h * w;
-  for (int i = tid; i < taps; i += nt) kw[i] = S.weights[i];
+  for (int i = tid; i < nkw; i += nt) {
+    const int t = i - (kVR - 1);
+    kwp[i] = (t >= 0 && t < taps) ? S.weights[t] : 0.0f;
+  }
   for (int q = tid; q < rows * 32; q += nt) {
     const int rr = q >> 5, c = q & 31;
     int ys = y_cta - r + rr;
@@ -138,18 +181,22 @@ __global__ void __launch_bounds__(32 * kVW) k_syn_vblur_tile(SynthDev S) {
     tile[q] = src[(size_t)ys * w + xs];
   }
   __syncthreads();
-  float acc[kVR];
+  float acc[kVR], kr[kVR];
 #pragma unroll
-  for (int o = 0; o < kVR; ++o) acc[o] = 0.0f;
+  for (int o = 0; o < kVR; ++o) {
+    acc[o] = 0.0f;
+    kr[o] = kwp[kVR - 1 - o];  // weights of input jj = 0
+  }
   const float* col = tile + warp * kVR * 32 + lane;
-  // input row jj (tile-relative to this warp) feeds output o with tap jj - o
-  for (int jj = 0; jj < kVR - 1 + taps; ++jj) {
+  const int steps = kVR - 1 + taps;
+#pragma unroll 8
+  for (int jj = 0; jj < steps; ++jj) {
     const float v = col[jj * 32];
 #pragma unroll
-    for (int o = 0; o < kVR; ++o) {
-      const int i = jj - o;
-      if (i >= 0 && i < taps) acc[o] = __fadd_rn(acc[o], __fmul_rn(kw[i], v));
-    }
+    for (int o = 0; o < kVR; ++o) acc[o] = __fadd_rn(acc[o], __fmul_rn(kr[o], v));
+#pragma unroll
+    for (int o = kVR - 1; o > 0; --o) kr[o] = kr[o - 1];
+    kr[0] = kwp[jj + kVR];  // weight of tap jj + 1 for output 0
   }
   const int x = x0 + lane;
   unsigned mn_inv = 0u, mx = 0u;
@@ -373,6 +420,31 @@ int fail(int code, const std::string& msg) {
   return code;
 }
 
+// Stream-ordered scratch from a per-device pool that keeps its memory between
+// calls (release threshold: never), so repeated calls do not remap hundreds of
+// megabytes of scratch each time.
+cudaError_t scratch_alloc(int device, void** p, size_t bytes, cudaStream_t st) {
+  static std::mutex mu;
+  static std::vector<cudaMemPool_t> pools;
+  cudaMemPool_t pool = nullptr;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if ((int)pools.size() <= device) pools.resize(device + 1, nullptr);
+    if (!pools[device]) {
+      cudaMemPoolProps props = {};
+      props.allocType = cudaMemAllocationTypePinned;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = device;
+      cudaError_t e = cudaMemPoolCreate(&pools[device], &props);
+      if (e != cudaSuccess) return e;
+      uint64_t keep = ~0ull;
+      cudaMemPoolSetAttribute(pools[device], cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    pool = pools[device];
+  }
+  return cudaMallocFromPoolAsync(p, bytes, pool, st);
+}
+
 }  // namespace
 
 extern "C" int pstereo_synth_check(const pstereo_synth_spec* s);
@@ -397,10 +469,11 @@ extern "C" int pstereo_gpu_synth(int device, const pstereo_synth_spec* s, int n_
   const int r = pstereo_synth_blur_weights(s->blur_sigma, nullptr, 0);
   std::vector<float> kw((size_t)(2 * r + 1));
   pstereo_synth_blur_weights(s->blur_sigma, kw.data(), 2 * r + 1);
-  const size_t smem_h = sizeof(float) * ((size_t)(2 * r + 1) + (size_t)(w + 2 * r));
+  const size_t smem_h =
+      sizeof(float) * ((size_t)(((w + 2 * r + 3) & ~3) + 8) + (size_t)(2 * r + 1 + kHPad + kHTail));
   const size_t smem_v = sizeof(float) * (size_t)(2 * r + 1);
   const size_t smem_vt =
-      sizeof(float) * ((size_t)((2 * r + 1 + 31) & ~31) + (size_t)(kVR * kVW + 2 * r) * 32);
+      sizeof(float) * ((size_t)((2 * r + 1 + 2 * kVR + 3) & ~3) + (size_t)(kVR * kVW + 2 * r) * 32);
   const size_t smem_views =
       sizeof(double) * ((size_t)w * C + 4 * SYN_MAX_DISCS + 2 * 3 * SYN_BLOBS);
   const size_t smem_views_c =
@@ -445,7 +518,7 @@ extern "C" int pstereo_gpu_synth(int device, const pstereo_synth_spec* s, int n_
   const size_t b_nd = sizeof(int) * chunk;
   auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
   const size_t total = al(b_w) + 2 * al(b_field) + al(b_mm) + al(b_cov) + al(b_disc) + al(b_nd);
-  e = cudaMallocAsync(&base, total, st);
+  e = scratch_alloc(device, &base, total, st);
   if (e != cudaSuccess) return fail(PSTEREO_EINTERNAL, cudaGetErrorString(e));
   char* q = (char*)base;
   S.weights = (const float*)q;
