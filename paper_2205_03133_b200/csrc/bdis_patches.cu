@@ -29,6 +29,9 @@
 //     (inc/image.hpp:53-71) with no per-sample double<->int conversions.
 #include <cuda_runtime.h>
 
+#include <cstdio>
+#include <cstring>
+
 #include <algorithm>
 #include <type_traits>
 #include <cstdlib>
@@ -666,7 +669,20 @@ BandPlan plan_bands(const Level& L, const PatchParams& pp, int max_smem_per_cta)
   // wide levels; 128-slot CTAs, three per SM, for medium ones; 256-slot CTAs
   // for the narrowest (whole-level bands, one CTA carries all of a pair)
   const bool medium = g.nx >= 30 && g.nx < 60;
-  const int threads = env("PSTEREO_TUNE_THREADS", g.nx < 30 ? 256 : medium ? 128 : 192);
+  int threads = env("PSTEREO_TUNE_THREADS", g.nx < 30 ? 256 : medium ? 128 : 192);
+  int ctas = env("PSTEREO_TUNE_CTAS", medium ? 3 : 2);
+  // tuning runs only: PSTEREO_TUNE_SPEC="e1=192x2,e2=128x3" per level exponent
+  if (const char* spec = getenv("PSTEREO_TUNE_SPEC")) {
+    char key[16];
+    snprintf(key, sizeof key, "e%d=", L.e);
+    if (const char* q = strstr(spec, key)) {
+      int t = 0, c = 0;
+      if (sscanf(q + strlen(key), "%dx%d", &t, &c) == 2 && t >= 32 && t <= 256 && c >= 1) {
+        threads = t;
+        ctas = c;
+      }
+    }
+  }
   auto bytes_for = [&](int rb) {
     const int rows = (rb - 1) * g.stride + g.size;
     return band_layout(rows, bp.rpitch, bp.fpitch, bp.bpitch, rb * g.nx, pp.nwin, valid,
@@ -676,10 +692,35 @@ BandPlan plan_bands(const Level& L, const PatchParams& pp, int max_smem_per_cta)
   // (measured best of a T x ppl x CTAs sweep at the bench workload;
   // PSTEREO_TUNE_THREADS / _PPL10 / _CTAS override, for tuning runs only)
   const int ppl10 = env("PSTEREO_TUNE_PPL10", 20);
-  const int ctas = env("PSTEREO_TUNE_CTAS", medium ? 3 : 2);
-  const size_t per_sm = size_t(max_smem_per_cta) / ctas - 1024;
-  int rb = std::max(1, std::min(g.ny, (ppl10 * threads / 10 + g.nx / 2) / g.nx));
-  while (rb > 1 && bytes_for(rb) > per_sm) --rb;
+  auto fit = [&](int t, int c) {
+    const size_t per_sm = size_t(max_smem_per_cta) / c - 1024;
+    int r = std::max(1, std::min(g.ny, (ppl10 * t / 10 + g.nx / 2) / g.nx));
+    while (r > 1 && band_layout((r - 1) * g.stride + g.size, bp.rpitch, bp.fpitch, bp.bpitch,
+                                r * g.nx, pp.nwin, valid, t).total > per_sm)
+      --r;
+    return r;
+  };
+  int rb = fit(threads, ctas);
+  // Large patches and dense grids make band rows expensive in shared memory:
+  // when the default shape's band starves (<= 2 patch rows for s >= 12, <= 3
+  // for s >= 16) or the grid is dense and wide (stride <= s/4, >= 60 patch
+  // columns), one 256-thread CTA per SM with the whole shared memory and a
+  // taller band wins (measured per level over the config-4 patch-size x
+  // stride grid, scripts/gpu_shape_sweep.py: s=16 stride 4 finest level
+  // 10.2 -> 4.5 ms; s=8 stride 4, the bench shape, is unaffected)
+  if (!getenv("PSTEREO_TUNE_SPEC") && !getenv("PSTEREO_TUNE_THREADS") &&
+      !getenv("PSTEREO_TUNE_CTAS")) {
+    const bool starving = (rb <= 2 && g.size >= 12) || (rb <= 3 && g.size >= 16);
+    const bool dense = 4 * g.stride <= g.size && g.nx >= 60;
+    if (starving || dense) {
+      const int r1 = fit(256, 1);
+      if (r1 >= rb + 1) {
+        threads = 256;
+        ctas = 1;
+        rb = r1;
+      }
+    }
+  }
   // small batches: a CTA's rounds are a latency chain, so spread the level
   // over more, smaller bands until every SM has a CTA (single-frame latency)
   const int sms = env("PSTEREO_SMS", 148);
