@@ -701,16 +701,18 @@ BandPlan plan_bands(const Level& L, const PatchParams& pp, int max_smem_per_cta)
     return r;
   };
   int rb = fit(threads, ctas);
-  // Large patches and dense grids make band rows expensive in shared memory:
-  // when the default shape's band starves (<= 2 patch rows for s >= 12, <= 3
-  // for s >= 16) or the grid is dense and wide (stride <= s/4, >= 60 patch
-  // columns), one 256-thread CTA per SM with the whole shared memory and a
-  // taller band wins (measured per level over the config-4 patch-size x
-  // stride grid, scripts/gpu_shape_sweep.py: s=16 stride 4 finest level
-  // 10.2 -> 4.5 ms; s=8 stride 4, the bench shape, is unaffected)
+  // Large patches, wide levels and dense grids make band rows expensive in
+  // shared memory: when the default shape's band starves (<= 2 patch rows for
+  // s >= 12 or >= 100 patch columns, <= 3 for s >= 16) or the grid is dense
+  // and wide (stride <= s/4, >= 60 patch columns), one 256-thread CTA per SM
+  // with the whole shared memory and a taller band wins (measured per level,
+  // scripts/gpu_shape_sweep.py: s=16 stride 4 finest level 10.2 -> 4.5 ms,
+  // 1920x1080 s=8 finest level 2.2 -> 1.3 ms; the bench shape, 640x480 s=8
+  // stride 4, is unaffected)
   if (!getenv("PSTEREO_TUNE_SPEC") && !getenv("PSTEREO_TUNE_THREADS") &&
       !getenv("PSTEREO_TUNE_CTAS")) {
-    const bool starving = (rb <= 2 && g.size >= 12) || (rb <= 3 && g.size >= 16);
+    const bool starving =
+        (rb <= 2 && (g.size >= 12 || g.nx >= 100)) || (rb <= 3 && g.size >= 16);
     const bool dense = 4 * g.stride <= g.size && g.nx >= 60;
     if (starving || dense) {
       const int r1 = fit(256, 1);

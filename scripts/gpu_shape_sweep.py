@@ -11,7 +11,10 @@ import torch
 sys.path.insert(0, ".")
 import paper_2205_03133_b200 as P  # noqa: E402
 
-W, H, B = 640, 480, 256
+# usage: gpu_shape_sweep.py [W H B "s:stride,s:stride,..."]
+W, H, B = (int(a) for a in sys.argv[1:4]) if len(sys.argv) > 3 else (640, 480, 256)
+GRID = ([tuple(int(v) for v in c.split(":")) for c in sys.argv[4].split(",")]
+        if len(sys.argv) > 4 else [(s, st) for s in (8, 12, 16) for st in (2, 4, 6)])
 dl, dr = P.synth_batch_gpu(0, B, seed0=0, width=W, height=H)
 disp = torch.empty((B, H, W), dtype=torch.float32, device="cuda")
 SHAPES = ["96x4", "128x2", "128x3", "128x4", "192x1", "192x2", "256x1", "256x2"]
@@ -42,9 +45,9 @@ def stages(cfg, spec):
     return {k: v / calls for k, v in t.items() if k.startswith("patches_")}
 
 
-for s in (8, 12, 16):
-    for stride in (2, 4, 6):
-        ce = 4 if s <= 12 else 3
+for s, stride in GRID:
+    if True:
+        ce = 4 if (s <= 12 or W > 640) else 3
         cfg = P.PipelineConfig(coarsest_exp=ce, finest_exp=1, patch_size=s, overlap=1 - stride / s)
         base = stages(cfg, None)
         best = {}
@@ -61,4 +64,5 @@ for s in (8, 12, 16):
             best[lvl] = {"default_ms": round(base[lvl], 4), "best": cand[0][1],
                          "best_ms": round(cand[0][0], 4),
                          "all": {sh: round(t, 4) for t, sh in sorted(cand, key=lambda x: x[1])}}
-        print(json.dumps({"s": s, "stride": stride, "levels": best}), flush=True)
+        print(json.dumps({"size": f"{W}x{H}", "s": s, "stride": stride, "levels": best}),
+              flush=True)
