@@ -713,7 +713,7 @@ int run_device(pstereo_ctx* ctx, Scratch& sc, const std::vector<LevelGeom>& geo,
   if (fused) {
     pa.u8l = src_u8[0];
     pa.u8r = src_u8[1];
-    pa.vec8 = left_u8 && channels == 1 && W % 8 == 0 && H % 2 == 0 &&
+    pa.vec8 = left_u8 && (channels == 1 || channels == 3) && W % 8 == 0 && H % 2 == 0 &&
               (uintptr_t)src_u8[0] % 8 == 0 && (uintptr_t)src_u8[1] % 8 == 0;
     pa.f0l = left_u8 ? nullptr : fsrc[0];
     pa.f0r = left_u8 ? nullptr : fsrc[1];

@@ -145,7 +145,9 @@ __device__ __forceinline__ float down4(float a, float b, float c, float d) {
   return __fmul_rn(0.25f, __fadd_rn(__fadd_rn(__fadd_rn(a, b), c), d));
 }
 
-template <bool kU8>
+// kRGB: the vectorised RGB level-1 path (its own instantiation, so the gray
+// path keeps its register budget)
+template <bool kU8, bool kRGB = false>
 __global__ void __launch_bounds__(256) k_pyramid(PyrArgs a) {
   extern __shared__ __align__(16) float sbuf[];
   const long long pair = blockIdx.y;
@@ -254,7 +256,42 @@ __global__ void __launch_bounds__(256) k_pyramid(PyrArgs a) {
       const int y0 = band << (ce - 1), rows = min(1 << (ce - 1), h - y0);
       float* Lb = buf[0];
       float* Rb = buf[0] + a.buf_floats;
-      if (kU8 && a.vec8) {
+      if (kRGB) {
+        // RGB rasters, W % 8 == 0, even H: 24 source bytes (8 pixels) of two
+        // rows per view, three 8-byte loads each, give 4 level-1 pixels; the
+        // luma of every pixel is src_px's (the same table sums, the same order)
+        const int qw = w >> 2;
+        for (int q = tid; q < rows * qw; q += nt) {
+          const int r = q / qw, xq = q - r * qw;
+          const long long base =
+              3 * (pair * (long long)a.W * a.H + (long long)(2 * (y0 + r)) * a.W + 8 * xq);
+  #pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            const uint8_t* src = (v ? a.u8r : a.u8l) + base;
+            unsigned tw[6], bw[6];
+  #pragma unroll
+            for (int k = 0; k < 3; ++k) {
+              const uint2 t = __ldg((const uint2*)src + k);
+              const uint2 b = __ldg((const uint2*)(src + 3 * a.W) + k);
+              tw[2 * k] = t.x;
+              tw[2 * k + 1] = t.y;
+              bw[2 * k] = b.x;
+              bw[2 * k + 1] = b.y;
+            }
+            auto byte = [](const unsigned* wd, int n) { return (wd[n >> 2] >> (8 * (n & 3))) & 255u; };
+            auto luma = [&](const unsigned* wd, int px) {
+              const double sum = __dadd_rn(__dadd_rn(c3[byte(wd, 3 * px)], c3[256 + byte(wd, 3 * px + 1)]),
+                                           c3[512 + byte(wd, 3 * px + 2)]);
+              return __double2float_rn(__dmul_rn(sum, 1.0 / 255.0));
+            };
+            float o[4];
+  #pragma unroll
+            for (int k = 0; k < 4; ++k)
+              o[k] = down4(luma(tw, 2 * k), luma(tw, 2 * k + 1), luma(bw, 2 * k), luma(bw, 2 * k + 1));
+            *(float4*)((v ? Rb : Lb) + r * w + 4 * xq) = make_float4(o[0], o[1], o[2], o[3]);
+          }
+        }
+      } else if (kU8 && a.vec8) {  // C == 1 here: the launcher routes vec8 RGB to kRGB
         // gray rasters, W % 8 == 0, even H: 8 source bytes of two rows per view
         // give 4 level-1 pixels (down4 of the grayscale values, as below)
         const int qw = w >> 2;
@@ -320,7 +357,11 @@ size_t pyramid_smem_bytes(const PyrArgs& a) {
 cudaError_t launch_pyramid(const PyrArgs& a, bool u8, cudaStream_t s) {
   const size_t smem = pyramid_smem_bytes(a);
   dim3 grid((a.hs[a.ce] + 1) / 2, a.n_pairs);  // two bands per CTA
-  if (u8) {
+  if (u8 && a.vec8 && a.C == 3) {
+    cudaFuncSetAttribute(k_pyramid<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    k_pyramid<true, true><<<grid, 256, smem, s>>>(a);
+  } else if (u8) {
     cudaFuncSetAttribute(k_pyramid<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_pyramid<true><<<grid, 256, smem, s>>>(a);
   } else {

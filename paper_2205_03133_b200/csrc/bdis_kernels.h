@@ -100,7 +100,7 @@ struct PyrArgs {
   float* G[kMaxLevels];
   float* Rp[kMaxLevels];
   int buf_floats;  // floats per view in one shared buffer: 2^(ce-1) * ws[1]
-  int vec8;        // gray u8, W % 8 == 0, even H, 8-byte aligned rasters
+  int vec8;        // gray or RGB u8, W % 8 == 0, even H, 8-byte aligned rasters
 };
 size_t pyramid_smem_bytes(const PyrArgs& a);
 cudaError_t launch_pyramid(const PyrArgs& a, bool u8, cudaStream_t s);
