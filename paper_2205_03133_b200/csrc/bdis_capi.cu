@@ -648,6 +648,8 @@ int run_device(pstereo_ctx* ctx, Scratch& sc, const std::vector<LevelGeom>& geo,
     pa.hs[e] = hs[e];
   }
   pa.buf_floats = ce >= 1 ? (1 << (ce - 1)) * ws[1] : 0;
+  // levels 2 and 4 alternate into a second, smaller buffer
+  pa.buf1_floats = ce >= 2 ? (((1 << (ce - 2)) * ws[2] + 3) & ~3) : 0;
   const bool fused = all_valid && pyramid_smem_bytes(pa) <= size_t(ctx->max_smem);
 
   // ---- inputs (already on the device)

@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(256) k_pyramid(PyrArgs a) {
   // level-1 rows of this band live in buf0 (L then R), level e >= 2 alternate
   float* buf[2] = {sbuf, sbuf + 2 * a.buf_floats};
   // grayscale lookup tables after the level buffers (8-byte aligned)
-  double* c3 = (double*)(sbuf + ((4 * a.buf_floats + 1) & ~1));
+  double* c3 = (double*)(sbuf + ((2 * a.buf_floats + 2 * a.buf1_floats + 1) & ~1));
   float* g1 = (float*)(c3 + 768);
   if (kU8) {
     for (int q = tid; q < 256; q += nt) {
@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(256) k_pyramid(PyrArgs a) {
     const int w = a.ws[e];
     const long long pl = pair * (long long)w * a.hs[e];
     const long long pr = pair * (long long)(w + 1) * a.hs[e];
-    if ((w & 3) == 0 && w >= 8 && (a.buf_floats & 3) == 0) {
+    if ((w & 3) == 0 && w >= 8 && ((Rb - Lb) & 3) == 0 && ((Lb - sbuf) & 3) == 0) {
       // four pixels per thread: 16-byte stores of L and G (rows of 4k floats)
       const int qw = w >> 2;
       for (int q = tid; q < rows * qw; q += nt) {
@@ -331,11 +331,11 @@ __global__ void __launch_bounds__(256) k_pyramid(PyrArgs a) {
       const int pw = a.ws[e - 1], ph = a.hs[e - 1];
       const int py0 = band << (ce - e + 1);
       const float* PL = buf[(e - 2) & 1];
-      const float* PR = PL + a.buf_floats;
+      const float* PR = PL + (((e - 2) & 1) ? a.buf1_floats : a.buf_floats);
       const int w = a.ws[e], h = a.hs[e];
       const int y0 = band << (ce - e), rows = min(1 << (ce - e), h - y0);
       float* Lb = buf[(e - 1) & 1];
-      float* Rb = Lb + a.buf_floats;
+      float* Rb = Lb + (((e - 1) & 1) ? a.buf1_floats : a.buf_floats);
       for (int q = tid; q < rows * w; q += nt) {
         const int y = y0 + q / w, x = q % w;
         const int x0 = 2 * x, x1 = min(2 * x + 1, pw - 1);
@@ -350,7 +350,8 @@ __global__ void __launch_bounds__(256) k_pyramid(PyrArgs a) {
 }
 
 size_t pyramid_smem_bytes(const PyrArgs& a) {
-  const size_t bufs = a.ce >= 1 ? size_t((4 * a.buf_floats + 1) & ~1) * sizeof(float) : 0;
+  const size_t bufs =
+      a.ce >= 1 ? size_t((2 * a.buf_floats + 2 * a.buf1_floats + 1) & ~1) * sizeof(float) : 0;
   return bufs + 768 * sizeof(double) + 256 * sizeof(float);  // + grayscale tables
 }
 

@@ -99,7 +99,8 @@ struct PyrArgs {
   float* L[kMaxLevels];
   float* G[kMaxLevels];
   float* Rp[kMaxLevels];
-  int buf_floats;  // floats per view in one shared buffer: 2^(ce-1) * ws[1]
+  int buf_floats;  // floats per view in shared buffer 0 (levels 1, 3): 2^(ce-1) * ws[1]
+  int buf1_floats; // floats per view in shared buffer 1 (levels 2, 4), rounded to 4
   int vec8;        // gray or RGB u8, W % 8 == 0, even H, 8-byte aligned rasters
 };
 size_t pyramid_smem_bytes(const PyrArgs& a);
