@@ -504,7 +504,7 @@ __device__ __forceinline__ Fused gather_tile(const Grid& g, const TileRecords& r
 // computed once). The records of the covering patches are staged in shared
 // memory and each pixel gathers them in ascending patch index.
 template <bool kVar, typename T, int K>
-__global__ void __launch_bounds__(kFuseThreads) k_fuse_ccl_local(
+__global__ void __launch_bounds__(kFuseThreads, (!kVar && K <= 3) ? 5 : 4) k_fuse_ccl_local(
     Level L, FinestBufs fb, const double* __restrict__ mask, CclBufs cb) {
   __shared__ int sl[kTilePx];
   __shared__ int s_area[kTilePx];
