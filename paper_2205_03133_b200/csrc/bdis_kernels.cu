@@ -148,7 +148,7 @@ __device__ __forceinline__ float down4(float a, float b, float c, float d) {
 // kRGB: the vectorised RGB level-1 path (its own instantiation, so the gray
 // path keeps its register budget)
 template <bool kU8, bool kRGB = false>
-__global__ void __launch_bounds__(256) k_pyramid(PyrArgs a) {
+__global__ void __launch_bounds__(256, kRGB ? 4 : 8) k_pyramid(PyrArgs a) {
   extern __shared__ __align__(16) float sbuf[];
   const long long pair = blockIdx.y;
   const int tid = threadIdx.x, nt = blockDim.x;
