@@ -47,7 +47,7 @@ def stages(cfg, spec):
 
 for s, stride in GRID:
     if True:
-        ce = 4 if (s <= 12 or W > 640) else 3
+        ce = int(os.environ.get("SWEEP_CE", 4 if (s <= 12 or W > 640) else 3))
         cfg = P.PipelineConfig(coarsest_exp=ce, finest_exp=1, patch_size=s, overlap=1 - stride / s)
         base = stages(cfg, None)
         best = {}

@@ -154,6 +154,22 @@ def test_config4_sweep(gpu, port, w, h, ch, size, stride):
     _check(P, port, cfg, l[None], r[None])
 
 
+@pytest.mark.parametrize("w,h,ch,size,stride,n", [
+    (640, 480, 1, 16, 4, 16),    # starving bands -> one 256-thread CTA per SM
+    (640, 480, 3, 8, 2, 12),     # dense wide grid
+    (1280, 1024, 3, 8, 4, 6),    # wide s=8 levels, vectorised RGB pyramid
+])
+def test_planner_shapes_batches(gpu, port, w, h, ch, size, stride, n):
+    """Batches large enough that the band planner keeps its tall-band shapes
+    (s >= 12 starving bands, dense or wide grids) and the RGB pyramid path:
+    every pair bit-identical to the oracle."""
+    P = gpu
+    left, right = P.synth_batch(4, n, seed0=50 + size, width=w, height=h, channels=ch)
+    cfg = P.PipelineConfig(coarsest_exp=4, finest_exp=1, patch_size=size,
+                           overlap=1.0 - stride / size)
+    _check(P, port, cfg, left, right)
+
+
 def test_empty_batch_and_limits(gpu):
     """n = 0 is a no-op; frames larger than the context's maximum are refused."""
     P = gpu
