@@ -133,16 +133,26 @@ __global__ void __launch_bounds__(kMetThreads) k_metrics(MetricsArgs a) {
       const unsigned dmask = (1u << bits) - 1u;
       for (int q = tid; q < kBins; q += kMetThreads) s_hist[q] = 0;
       __syncthreads();
-      for (long long i0 = 0; i0 < m; i0 += kMetThreads) {
-        const long long i = i0 + tid;
-        unsigned d = kBins;  // no bin
-        if (i < m) {
-          const unsigned long long key = keys[i];
-          if ((key & pmask) == prefix) d = (unsigned)(key >> sh) & dmask;
+      // kKeyIlp keys per thread in flight: the pass is bound by the global
+      // load latency, not by the histogram updates
+      constexpr int kKeyIlp = 8;
+      for (long long i0 = 0; i0 < m; i0 += (long long)kMetThreads * kKeyIlp) {
+        unsigned long long kv[kKeyIlp];
+#pragma unroll
+        for (int u = 0; u < kKeyIlp; ++u) {
+          const long long i = i0 + (long long)u * kMetThreads + tid;
+          kv[u] = i < m ? __ldcg(keys + i) : ~0ull;
         }
-        // one atomic per distinct digit in the warp (hot bins are common)
-        const unsigned peers = __match_any_sync(0xffffffffu, d);
-        if (d != kBins && lane == __ffs(peers) - 1) atomicAdd(&s_hist[d], (unsigned)__popc(peers));
+#pragma unroll
+        for (int u = 0; u < kKeyIlp; ++u) {
+          const long long i = i0 + (long long)u * kMetThreads + tid;
+          unsigned d = kBins;  // no bin
+          if (i < m && (kv[u] & pmask) == prefix) d = (unsigned)(kv[u] >> sh) & dmask;
+          // one atomic per distinct digit in the warp (hot bins are common)
+          const unsigned peers = __match_any_sync(0xffffffffu, d);
+          if (d != kBins && lane == __ffs(peers) - 1)
+            atomicAdd(&s_hist[d], (unsigned)__popc(peers));
+        }
       }
       __syncthreads();
       if (tid == 0) {
@@ -177,7 +187,7 @@ __global__ void __launch_bounds__(kMetThreads) k_metrics(MetricsArgs a) {
         // rank mid-1 is below the value at rank mid: the largest smaller key
         unsigned long long best = 0;
         for (long long i = tid; i < m; i += kMetThreads) {
-          const unsigned long long key = keys[i];
+          const unsigned long long key = __ldcg(keys + i);
           if (key < prefix && key > best) best = key;
         }
         for (int o = 16; o > 0; o >>= 1) {
