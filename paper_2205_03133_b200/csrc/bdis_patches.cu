@@ -671,15 +671,18 @@ BandPlan plan_bands(const Level& L, const PatchParams& pp, int max_smem_per_cta)
   const bool medium = g.nx >= 30 && g.nx < 60;
   int threads = env("PSTEREO_TUNE_THREADS", g.nx < 30 ? 256 : medium ? 128 : 192);
   int ctas = env("PSTEREO_TUNE_CTAS", medium ? 3 : 2);
+  int ppl10 = env("PSTEREO_TUNE_PPL10", 20);
   // tuning runs only: PSTEREO_TUNE_SPEC="e1=192x2,e2=128x3" per level exponent
   if (const char* spec = getenv("PSTEREO_TUNE_SPEC")) {
     char key[16];
     snprintf(key, sizeof key, "e%d=", L.e);
     if (const char* q = strstr(spec, key)) {
-      int t = 0, c = 0;
-      if (sscanf(q + strlen(key), "%dx%d", &t, &c) == 2 && t >= 32 && t <= 256 && c >= 1) {
+      int t = 0, c = 0, pp10 = 0;
+      const int got = sscanf(q + strlen(key), "%dx%dx%d", &t, &c, &pp10);
+      if (got >= 2 && t >= 32 && t <= 256 && c >= 1) {
         threads = t;
         ctas = c;
+        if (got == 3 && pp10 > 0) ppl10 = pp10;
       }
     }
   }
@@ -691,7 +694,6 @@ BandPlan plan_bands(const Level& L, const PatchParams& pp, int max_smem_per_cta)
   // up to ~2 patches per slot of a 192-thread CTA, while two CTAs fit an SM
   // (measured best of a T x ppl x CTAs sweep at the bench workload;
   // PSTEREO_TUNE_THREADS / _PPL10 / _CTAS override, for tuning runs only)
-  const int ppl10 = env("PSTEREO_TUNE_PPL10", 20);
   auto fit = [&](int t, int c) {
     const size_t per_sm = size_t(max_smem_per_cta) / c - 1024;
     int r = std::max(1, std::min(g.ny, (ppl10 * t / 10 + g.nx / 2) / g.nx));
