@@ -388,7 +388,7 @@ cudaError_t launch_pyramid(const PyrArgs& a, bool u8, cudaStream_t s) {
 //                   compressed to point at it (no per-pixel pass, no memset).
 // Links always point to the smaller index (atomicMin), so the partition --
 // and therefore the kept mask -- does not depend on scheduling.
-constexpr int kTileW = 32, kTileH = 32, kTilePx = kTileW * kTileH;
+constexpr int kTileW = 32, kTileH = 64, kTilePx = kTileW * kTileH;
 constexpr int kFuseThreads = 256, kFuseWarps = kFuseThreads / 32, kFuseRows = kTileH / kFuseWarps;
 
 template <typename Ptr>
