@@ -160,6 +160,70 @@ __device__ __forceinline__ Fused gather(const Level& P, long long pair, int x, i
   return gather_with<kProb, kVar>(P.g, rec, x, y, mask);
 }
 
+// The Gauss-Newton loop of variance_fit below for the symmetric five-point
+// window (points ordered -a, -b, 0, b, a): same arithmetic, same order of the
+// sums, with g and d r / d sigma shared between +-o.
+__device__ inline double variance_fit5(const double* delta, const double* p, double fallback) {
+  const double d2a = __dmul_rn(delta[0], delta[0]);
+  const double d2b = __dmul_rn(delta[1], delta[1]);
+  const double d2c = __dmul_rn(delta[2], delta[2]);
+  double c = 1.0;
+  double sigma = sqrt(0.1);
+  for (int iter = 0; iter < 10; ++iter) {  // kVarianceFitIterations
+    const double den = __dmul_rn(__dmul_rn(2.0, sigma), sigma);
+    const double s3 = __dmul_rn(__dmul_rn(sigma, sigma), sigma);
+    const double ga = exp(__ddiv_rn(-d2a, den));
+    const double gb = exp(__ddiv_rn(-d2b, den));
+    // delta = 0: -0 / den = -0 and exp(-0) = 1 exactly whenever den > 0
+    const double gc = den > 0.0 ? 1.0 : exp(__ddiv_rn(-d2c, den));
+    const double ja = __ddiv_rn(__dmul_rn(__dmul_rn(c, ga), d2a), s3);
+    const double jb = __ddiv_rn(__dmul_rn(__dmul_rn(c, gb), d2b), s3);
+    const double jc = __ddiv_rn(__dmul_rn(__dmul_rn(c, gc), d2c), s3);
+    const double gs[5] = {ga, gb, gc, gb, ga};
+    const double js5[5] = {ja, jb, jc, jb, ja};
+    double a00 = 0.0, a01 = 0.0, a11 = 0.0, b0 = 0.0, b1 = 0.0;
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+      const double g = gs[i], js = js5[i];
+      const double r = __dsub_rn(__dmul_rn(c, g), p[i]);
+      a00 = __dadd_rn(a00, __dmul_rn(g, g));
+      a01 = __dadd_rn(a01, __dmul_rn(g, js));
+      a11 = __dadd_rn(a11, __dmul_rn(js, js));
+      b0 = __dsub_rn(b0, __dmul_rn(g, r));
+      b1 = __dsub_rn(b1, __dmul_rn(js, r));
+    }
+    if (!(a00 > 0.0)) return fallback;
+    const double l00 = __dsqrt_rn(a00);
+    const double l01 = __ddiv_rn(a01, l00);
+    const double d11 = __dsub_rn(a11, __dmul_rn(l01, l01));
+    if (!(d11 > 1e-300)) return fallback;
+    const double l11 = __dsqrt_rn(d11);
+    const double y0 = __ddiv_rn(b0, l00);
+    const double y1 = __ddiv_rn(__dsub_rn(b1, __dmul_rn(l01, y0)), l11);
+    const double xs = __ddiv_rn(y1, l11);
+    const double xc = __ddiv_rn(__dsub_rn(y0, __dmul_rn(l01, xs)), l00);
+    c = __dadd_rn(c, xc);
+    sigma = __dadd_rn(sigma, xs);
+    if (!isfinite(c) || !isfinite(sigma) || sigma <= 0.0) return fallback;
+  }
+  const double den = __dmul_rn(__dmul_rn(2.0, sigma), sigma);
+  // (-delta) * delta == -(delta * delta) exactly
+  const double ga = exp(__ddiv_rn(-d2a, den));
+  const double gb = exp(__ddiv_rn(-d2b, den));
+  const double gc = den > 0.0 ? 1.0 : exp(__ddiv_rn(-d2c, den));
+  const double gs[5] = {ga, gb, gc, gb, ga};
+  double ssr = 0.0;
+#pragma unroll
+  for (int i = 0; i < 5; ++i) {
+    const double r = __dsub_rn(__dmul_rn(c, gs[i]), p[i]);
+    ssr = __dadd_rn(ssr, __dmul_rn(r, r));
+  }
+  const double fit = __dsqrt_rn(__ddiv_rn(ssr, 5.0));
+  if (!isfinite(fit)) return fallback;
+  if (fit > 0.1) return fallback;  // kVarianceFitMaxResidual
+  return sigma;
+}
+
 // estimate_patch_variance (src/depth_variance.cpp:94-170) on the window
 // priors. CUDA exp() may differ from glibc's by an ulp: sigma_k agrees to
 // ~1e-15 relative, which is why var_disp is held to 1e-3 rel, not bits.
@@ -182,6 +246,13 @@ __device__ inline double variance_fit(const double* woff, int nwin, int wcenter,
     if (delta[i] == 0.0) continue;
     if (!(center_prior > p[i])) return fallback;
   }
+  // The common window -- five valid samples at {-a, -b, 0, b, a} (the
+  // symmetric closure of two offsets) -- has three distinct d2 = delta^2, and
+  // g and d r / d sigma depend on the offset only through d2: evaluate them
+  // once per distinct d2 (the same operations on the same operands, hence the
+  // same bits as per point), in registers.
+  if (n == 5 && delta[2] == 0.0 && delta[0] == -delta[4] && delta[1] == -delta[3])
+    return variance_fit5(delta, p, fallback);
   double c = 1.0;
   double sigma = sqrt(0.1);
   for (int iter = 0; iter < 10; ++iter) {  // kVarianceFitIterations
