@@ -178,7 +178,9 @@ __device__ inline double variance_fit5(const double* delta, const double* p, dou
     const double gc = den > 0.0 ? 1.0 : exp(__ddiv_rn(-d2c, den));
     const double ja = __ddiv_rn(__dmul_rn(__dmul_rn(c, ga), d2a), s3);
     const double jb = __ddiv_rn(__dmul_rn(__dmul_rn(c, gb), d2b), s3);
-    const double jc = __ddiv_rn(__dmul_rn(__dmul_rn(c, gc), d2c), s3);
+    // (c * 1) * 0 / s3 = +-0 with the sign of c, for finite c and s3 > 0
+    const double jc = (gc == 1.0 && s3 > 0.0) ? copysign(0.0, c)
+                                              : __ddiv_rn(__dmul_rn(__dmul_rn(c, gc), d2c), s3);
     const double gs[5] = {ga, gb, gc, gb, ga};
     const double js5[5] = {ja, jb, jc, jb, ja};
     double a00 = 0.0, a01 = 0.0, a11 = 0.0, b0 = 0.0, b1 = 0.0;
