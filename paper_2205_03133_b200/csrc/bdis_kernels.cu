@@ -943,6 +943,44 @@ __global__ void __launch_bounds__(256) k_output_x4(OutputArgs a) {
   }
 }
 
+// The same for the common request of the filtered disparity alone (plus its
+// validity): no other planes in registers, so more CTAs stay resident.
+template <typename T>
+__global__ void __launch_bounds__(256) k_output_disp_x4(OutputArgs a) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  const int qw = a.fw >> 2;
+  if (q >= qw * a.fh) return;
+  const long long pair = blockIdx.y;
+  const int fy = q / qw, fx = (q - fy * qw) << 2;
+  const long long f = pair * a.fplane + (long long)fy * a.fw + fx;
+  const uchar4 fl = *(const uchar4*)(a.fb.flags + f);
+  const uint8_t fls[4] = {fl.x, fl.y, fl.z, fl.w};
+  T d[4];
+  load4<T>(a.fb.disp, f, d);
+  unsigned keep = 0;
+  const int* lab = a.label + pair * a.fplane;
+  const int* area = a.area + pair * a.fplane;
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (fls[k] & kFlagKeep)  // local root -> global root -> component area
+      keep |= (unsigned)((fls[k] & kFlagSure) ||
+                         area[lab[lab[fy * a.fw + fx + k]]] >= a.min_px) << k;
+  if (a.fill_invalid) {
+    const T iv = (T)a.invalid_value;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (!((keep >> k) & 1u)) d[k] = iv;
+  }
+  const long long pbase = pair * (long long)a.W * a.H;
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int y = 2 * fy + r;
+    const long long o = pbase + (long long)(a.flip_rows ? a.H - 1 - y : y) * a.W + 2 * fx;
+    put_row8<T>(a.out_disp, o, d[0], d[1], d[2], d[3]);
+    if (a.out_dvalid) put_row8_u8(a.out_dvalid, o, keep);
+  }
+}
+
 // MatchStats per pair and level (src/coarse_to_fine.cpp:302-314).
 __global__ void k_stats(StatsArgs a) {
   const int pair = blockIdx.x, lvl = blockIdx.y;
@@ -1056,6 +1094,14 @@ void launch_output(const OutputArgs& a, int f64, int n_pairs, cudaStream_t s) {
     x4 = x4 && aligned(p, 8);
   if (x4) {
     dim3 grid(blocks_for((long long)(a.fw / 4) * a.fh, 256), n_pairs);
+    const bool disp_only = a.out_disp && !a.out_prob && !a.out_mdisp && !a.out_mvalid &&
+                           !a.out_depth && !a.out_depth_valid && !a.out_var && !a.out_sigma &&
+                           !a.out_sigma_valid;
+    if (disp_only) {
+      if (f64) k_output_disp_x4<double><<<grid, 256, 0, s>>>(a);
+      else k_output_disp_x4<float><<<grid, 256, 0, s>>>(a);
+      return;
+    }
     if (f64) k_output_x4<double><<<grid, 256, 0, s>>>(a);
     else k_output_x4<float><<<grid, 256, 0, s>>>(a);
     return;

@@ -314,6 +314,26 @@ def test_device_sub_batches_are_invisible(gpu):
             assert np.array_equal(a.view(np.uint8), b.view(np.uint8)), (chunks, k)
 
 
+def test_disparity_only_output_path(gpu, port):
+    """Requests of the disparity plane alone (+ validity) take a dedicated
+    output kernel: same values as the full-plane request and the oracle."""
+    P = gpu
+    left, right = P.synth_batch(0, 3, seed0=70, width=320, height=240)
+    cfg = P.PipelineConfig(coarsest_exp=3, finest_exp=1, patch_size=8, overlap=0.5)
+    full = ["disparity", "disparity_valid", "probability", "depth", "depth_valid"]
+    with P.Matcher(cfg, 320, 240, 3) as m:
+        for dt in (P.F32, P.F64):
+            a = m.run_batch(left, right, 500.0, 5.0, dtype=dt, want=full)
+            b = m.run_batch(left, right, 500.0, 5.0, dtype=dt, want=("disparity", "disparity_valid"))
+            c = m.run_batch(left, right, 500.0, 5.0, dtype=dt, want=("disparity",),
+                            invalid_value=-1.0, flip_rows=True)
+            assert np.array_equal(a["disparity"], b["disparity"])
+            assert np.array_equal(a["disparity_valid"], b["disparity_valid"])
+            want_c = np.where(a["disparity_valid"] != 0, a["disparity"], -1.0)[:, ::-1]
+            assert np.array_equal(c["disparity"], want_c.astype(c["disparity"].dtype))
+    _check(P, port, cfg, left, right)
+
+
 def test_invalid_value_fill(gpu):
     """fill_invalid writes the PFM-style sentinel (src/io.cpp:297-310) into
     invalid disparity/depth pixels and leaves valid ones untouched."""
