@@ -744,6 +744,10 @@ __global__ void k_ccl_border(int w, int h, long long plane, const uint8_t* __res
   volatile int* vl = l;
   const int j = left ? i - 1 : i - w;
   if (!(mask[base + j] & kFlagKeep)) return;
+  // both tile-local components already meet the area rule on their own: the
+  // union cannot change any keep decision (a smaller component joined to
+  // either one still reaches that one's area), so it is skipped
+  if ((mask[base + i] & kFlagSure) && (mask[base + j] & kFlagSure)) return;
   // start from the tile-local roots; neighbouring border threads mostly join
   // the same pair of components, so one lane per distinct pair does the union
   const int a = l[i], b = l[j];
