@@ -1,32 +1,44 @@
 #!/usr/bin/env python
 """BDIS matching-core throughput on B200 (BASELINE.json metric: 640x480 stereo
-pairs/sec, fraction of the memory roofline).
+pairs/sec at 1/2/4/8 B200, fraction of the memory roofline).
 
 A "step" = one batched run_pipeline (pyramid -> per-level patch solves ->
-finest fusion -> confidence filter -> depth) over BATCH pairs of the config-2
-workload (seeded config-0 generator pairs, 640x480 uint8 gray, exps 3..1, 8x8
-patches at stride 4, variance off). Pairs are independent, so under torchrun
-each rank processes its own BATCH pairs (seeds rank*BATCH...), no collective on
-the data path ("scaling": "weak"); the only NCCL call is the max-over-ranks
-reduction of the timings.
+finest fusion -> confidence filter -> output) over the workload's batch. The
+default workload is BASELINE config 2: 256 seeded config-0 generator pairs,
+640x480 uint8 gray, exps 3..1, 8x8 patches at stride 4, variance off. Under
+N ranks the batch is split into contiguous pair blocks (strong scaling, the
+BASELINE definition: 256 pairs total, 32 per GPU at N=8); pairs are
+independent, so there is no collective on the data path -- the only
+collective is the max-over-ranks reduction of the timings. A weak-scaling
+number (256 pairs per GPU) is reported beside it when N > 1.
 
-  value   device-resident inputs/outputs, CUDA events on the launch stream
-  e2e     the same through the public C ABI with pinned HOST buffers: H2D of
-          both views and D2H of the disparity map (NaN = invalid, i.e. the
-          validity mask folded in) inside every timed step
-  roofline  dominant kernel (the finest-level k_patches launch) from live CUDA
-          events; traffic from the committed ncu capture (profiles/)
-  cpu_baseline  the reference (oracle/_ref, the unmodified reference sources)
-          on this host's cores, bounded sample (rank 0, N=1 only)
+  value     device-resident inputs/outputs, CUDA events on the launch stream
+  e2e       the same through the public C ABI with pinned HOST buffers: H2D of
+            both views and D2H of the output inside every timed step
+  roofline  dominant kernel (the finest-level k_patches launch) from live
+            CUDA events; DRAM traffic from the committed ncu capture
+  cpu_baseline  the reference (oracle/_ref: the unmodified reference sources)
+            on this host's cores over the same batch (rank 0, N=1 only)
+  parity    the GPU step's outputs against those reference outputs
 
---impl reference times the reference CPU implementation itself, all host cores,
-same metric/config.
+The timed step's output is the filtered disparity map as fp32 with NaN at
+invalid pixels (the validity mask folded in: the BASELINE bytes-per-pair);
+`full_outputs` times the same batch writing every plane run_pipeline returns
+(disparity + mask, probability, depth + mask).
+
+--impl reference times the reference CPU implementation itself (run_pipeline
+from oracle/_ref, all host cores) on the same workload; that process never
+loads the product library (its inputs come from oracle/libbdis_synth.so).
+
+`python bench.py --gpus N` with no torchrun environment launches the N ranks
+itself (torch.distributed.run, 127.0.0.1).
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import tempfile
@@ -39,8 +51,48 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-W, H = 640, 480
 HBM_FALLBACK_GBS = 6650.0
+FOCAL, BASELINE_MM = 500.0, 5.0
+
+
+# ---------------------------------------------------------------------------
+# workloads (BASELINE.json configs): generator config + overrides, the
+# PipelineConfig fields (SURVEY.md 8a mapping), the batch
+
+def _c4_levels(w, h, s):
+    ce, ws, hs = 1, (w + 1) // 2, (h + 1) // 2
+    while ce < 4 and (ws + 1) // 2 >= s and (hs + 1) // 2 >= s:
+        ws, hs, ce = (ws + 1) // 2, (hs + 1) // 2, ce + 1
+    return ce
+
+
+def workload(name: str) -> dict:
+    c0 = dict(coarsest_exp=3, finest_exp=1, patch_size=8, overlap=0.5)
+    if name == "c2":
+        return dict(name=name, gen=0, over={}, W=640, H=480, C=1, batch=256, params=c0,
+                    desc="config2: 640x480 u8 gray, exps 3..1, 8x8 patches stride 4, "
+                         "variance off, seeds 0..255")
+    if name == "c1":
+        return dict(name=name, gen=1, over={}, W=640, H=480, C=1, batch=256,
+                    params=dict(c0, estimate_variance=True),
+                    desc="config1 generator (photometric stress), 640x480 u8 gray, exps 3..1, "
+                         "8x8 patches stride 4, variance on")
+    if name == "c3":
+        return dict(name=name, gen=3, over={}, W=1280, H=1024, C=1, batch=128,
+                    params=dict(coarsest_exp=4, finest_exp=1, patch_size=12,
+                                overlap=1.0 - 4.0 / 12.0, estimate_variance=True),
+                    desc="config3: 1280x1024 u8 gray, exps 4..1, 12x12 patches stride 4, "
+                         "variance on")
+    if name.startswith("c4:"):
+        # c4:WxH:size:stride:channels:batch
+        dims, s, st, ch, b = name[3:].split(":")
+        w, h = (int(v) for v in dims.split("x"))
+        s, st, ch, b = int(s), int(st), int(ch), int(b)
+        return dict(name=name, gen=4, over=dict(width=w, height=h, channels=ch), W=w, H=h, C=ch,
+                    batch=b, params=dict(coarsest_exp=_c4_levels(w, h, s), finest_exp=1,
+                                         patch_size=s, overlap=1.0 - st / s),
+                    desc=f"config4 sweep: {w}x{h} u8 x{ch}, {s}x{s} patches stride {st}")
+    raise SystemExit(f"unknown workload {name!r} (c2, c1, c3, c4:WxH:s:stride:ch:batch)")
 
 
 def peaks():
@@ -58,8 +110,18 @@ def host_cores():
         return os.cpu_count() or 1
 
 
+def metric_name(wl) -> str:
+    return f"{wl['W']}x{wl['H']} stereo pairs/sec"
+
+
+def bytes_per_pair(wl) -> int:
+    # u8 input views + fp32 disparity + u8 mask (+ fp32 var)
+    var = 4 if wl["params"].get("estimate_variance") else 0
+    return wl["W"] * wl["H"] * (2 * wl["C"] + 4 + 1 + var)
+
+
 # ---------------------------------------------------------------------------
-# CPU reference (oracle/_ref = the reference's own sources, or the C port)
+# CPU reference (oracle/_ref = the reference's own sources, else the C port)
 
 def _cpu_oracle():
     from oracle import pyoracle
@@ -68,16 +130,20 @@ def _cpu_oracle():
     return pyoracle.load(kind), kind
 
 
-def cpu_throughput(left, right, cfg, threads, focal=500.0, baseline=5.0):
-    """Runs run_pipeline on every pair with `threads` workers (threads=1 each,
+def cpu_run(left, right, params, threads, keep=False):
+    """run_pipeline on every pair with `threads` workers (threads=1 each:
     pair-level parallelism, the fair CPU throughput per SURVEY.md 8d).
-    Returns (pairs/s over the wall time, per-pair runtime_ms list)."""
+    Returns (pairs/s over the wall time, per-pair runtime_ms, outputs|None)."""
+    from oracle import pyoracle
+
     orc, _ = _cpu_oracle()
-    grays = [(orc.to_grayscale(left[k])[0], orc.to_grayscale(right[k])[0])
+    cfg = pyoracle.Config(**params)
+    grays = [(orc.to_grayscale(left[k]), orc.to_grayscale(right[k]))
              for k in range(left.shape[0])]
     idx = [0]
     lock = threading.Lock()
-    times = []
+    times = [0.0] * len(grays)
+    outs = [None] * len(grays) if keep else None
 
     def worker():
         while True:
@@ -86,9 +152,12 @@ def cpu_throughput(left, right, cfg, threads, focal=500.0, baseline=5.0):
                 idx[0] += 1
             if k >= len(grays):
                 return
-            r = orc.run_pipeline(grays[k][0], grays[k][1], cfg, focal, baseline)
-            with lock:
-                times.append(r["runtime_ms"])
+            (lf, lv), (rf, rv) = grays[k]
+            r = orc.run_pipeline(lf, rf, cfg, FOCAL, BASELINE_MM, lv, rv)
+            times[k] = r["runtime_ms"]
+            if keep:
+                outs[k] = {n: r[n] for n in ("disparity", "disparity_valid", "probability",
+                                             "depth", "depth_valid")}
 
     ths = [threading.Thread(target=worker) for _ in range(threads)]
     t0 = time.perf_counter()
@@ -97,43 +166,39 @@ def cpu_throughput(left, right, cfg, threads, focal=500.0, baseline=5.0):
     for t in ths:
         t.join()
     wall = time.perf_counter() - t0
-    return len(grays) / wall, times
+    return len(grays) / wall, times, outs
 
 
-def oracle_cfg():
+def run_reference_arm(args, wl):
+    """The reference's own CPU implementation (run_pipeline, oracle/_ref) on the
+    same workload: every step is the whole batch on all host cores. Never
+    imports the product (inputs from the test-side generator library)."""
     from oracle import pyoracle
-
-    return pyoracle.Config(coarsest_exp=3, finest_exp=1, patch_size=8, overlap=0.5)
-
-
-def run_reference_arm(args):
-    import paper_2205_03133_b200 as P
 
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     cores = host_cores()
-    orc, kind = _cpu_oracle()
-    n = max(cores, 1)
-    left, right = P.synth_batch(0, n * (args.steps + args.warmup), seed0=0, threads=cores)
-    cfg = oracle_cfg()
-    total_pairs, total_t = 0, 0.0
+    _, kind = _cpu_oracle()
+    B = wl["batch"]
+    left, right = pyoracle.synth_batch(wl["gen"], B, seed0=0, threads=cores, **wl["over"])
+    step_s = []
     for step in range(args.warmup + args.steps):
-        sl = slice(step * n, (step + 1) * n)
-        rate, _ = cpu_throughput(left[sl], right[sl], cfg, cores)
+        rate, _, _ = cpu_run(left, right, wl["params"], cores)
         if step >= args.warmup:
-            total_pairs += n
-            total_t += n / rate
-    value = total_pairs / total_t
-    sample = (f"{args.steps} steps x {n} config-2 pairs (640x480, seeds 0..), one pair per core "
-              f"per step, run_pipeline threads=1")
+            step_s.append(B / rate)
+    total_t = sum(step_s)
+    value = B * args.steps / total_t
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    sample = (f"{args.steps} timed steps x {B} pairs ({wl['name']}, seeds 0..{B - 1}), "
+              f"{cores} workers, one pair per worker at a time, run_pipeline threads=1")
     line = {
-        "impl": "reference", "metric": "640x480 stereo pairs/sec", "value": value,
-        "unit": "pairs/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * total_t / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "config2: 640x480 u8 gray, exps 3..1, s=8 stride 4, var off",
-                   "global_batch": n, "parallelism": f"{cores} host threads"},
+        "impl": "reference", "metric": metric_name(wl), "value": value, "unit": "pairs/s",
+        "n_gpus": max(args.gpus, world), "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total_t / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": wl["desc"], "global_batch": B,
+                   "parallelism": f"{cores} host threads (pair-parallel)"},
         "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": cores, "kind": kind,
                          "sample": sample},
         "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0,
@@ -197,80 +262,162 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # our arm
 
-def run_ours(args):
+def _axis(L, s, stride):
+    c0 = (s - 1) * 0.5
+    cmax = (L - 1) - c0
+    out = []
+    k = 0
+    while True:
+        c = c0 + k * stride
+        if c >= cmax - 1e-9:
+            out.append(cmax)
+            return out
+        out.append(c)
+        k += 1
+
+
+def parity_report(ref_outs, gpu, k0):
+    """Pairs k0.. of the GPU's F64 planes (device tensors) against the
+    reference's run_pipeline outputs for the same pairs."""
+    import torch
+
+    n = len(ref_outs)
+    bitexact = 0
+    mask_diff = 0
+    max_dd = 0.0
+    planes = ("disparity", "probability", "depth")
+    for k in range(n):
+        ro = ref_outs[k]
+        g = {name: gpu[name][k0 + k].cpu().numpy() for name in gpu}
+        same = True
+        for vname in ("disparity_valid", "depth_valid"):
+            d = int((g[vname] != ro[vname]).sum())
+            same = same and d == 0
+            if vname == "disparity_valid":
+                mask_diff += d
+        for name in planes:
+            a = np.ascontiguousarray(g[name]).view(np.uint64)
+            b = np.ascontiguousarray(ro[name]).view(np.uint64)
+            same = same and bool(np.array_equal(a, b))
+        both = (g["disparity_valid"] != 0) & (ro["disparity_valid"] != 0)
+        if both.any():
+            max_dd = max(max_dd, float(np.abs(g["disparity"][both] - ro["disparity"][both]).max()))
+        bitexact += int(same)
+        del g
+    torch.cuda.synchronize()
+    return {"pairs": n, "bitexact": bitexact, "mask_diff_px": mask_diff, "max_abs_dd": max_dd,
+            "planes": "disparity, disparity_valid, probability, depth, depth_valid (f64 bits)",
+            "against": "oracle/_ref run_pipeline (the unmodified reference)"}
+
+
+def run_ours(args, wl):
     import torch
     import torch.distributed as dist
 
     import paper_2205_03133_b200 as P
+    from paper_2205_03133_b200.shard import max_over_ranks, strong_shard, weak_shard
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    # functional check of the multi-rank logic on a one-GPU box (not a
-    # measurement): PSTEREO_BENCH_BACKEND=gloo and ranks folded onto the GPUs
-    backend = os.environ.get("PSTEREO_BENCH_BACKEND", "nccl")
-    if backend != "nccl":
-        local %= max(torch.cuda.device_count(), 1)
+    ndev = torch.cuda.device_count()
+    # more ranks than GPUs (a one-GPU box): a functional run of the multi-rank
+    # logic, not a measurement -- ranks share the GPU, timings reduce over gloo
+    folded = world > ndev
+    backend = os.environ.get("PSTEREO_BENCH_BACKEND", "gloo" if folded else "nccl")
+    local %= max(ndev, 1)
     torch.cuda.set_device(local)
     if world > 1:
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
-    B = args.batch
-    cfg = P.PipelineConfig.baseline(0)
-    from paper_2205_03133_b200.shard import max_over_ranks, weak_shard
-
-    shard = weak_shard(B, rank, world)  # pairs are independent: no exchange
+    W, H, CH, B = wl["W"], wl["H"], wl["C"], wl["batch"]
+    cfg = P.PipelineConfig(**wl["params"])
     dev = torch.device("cuda", local)
+    # pairs are independent: contiguous blocks, no exchange (SURVEY.md 8e)
+    shard = strong_shard(B, rank, world)
+    nb = shard.count
+    shape = (nb, H, W) if CH == 1 else (nb, H, W, CH)
     # inputs generated in HBM by the device generator (SURVEY.md 8f row 1):
     # the same bytes as the host generator, without host work or PCIe per rank
-    dl, dr = P.synth_batch_gpu(0, shard.count, seed0=shard.start, device=local)
+    dl, dr = P.synth_batch_gpu(wl["gen"], nb, seed0=shard.start, device=local, **wl["over"])
     torch.cuda.synchronize(dev)
-    left, right = dl.cpu().numpy(), dr.cpu().numpy()  # host copies: e2e leg, CPU baseline
-    # output: the filtered disparity map with NaN at invalid pixels (the
-    # reference persists maps the same way with a -1 sentinel, src/io.cpp:297-310);
-    # the validity mask is exactly isfinite(disparity)
-    disp = torch.empty((B, H, W), dtype=torch.float32, device=dev)
-    m = P.Matcher(cfg, W, H, B, device=local)
-    # a dedicated stream: our kernels and the timing events must share it
-    # (NULL would select the context's own stream, not torch's legacy stream)
+    disp = torch.empty((max(nb, 1), H, W), dtype=torch.float32, device=dev)
+    m = P.Matcher(cfg, W, H, max(B, 1), device=local)
+    # a dedicated stream: our kernels and the timing events share it (NULL
+    # would select the context's own stream, not torch's legacy stream)
     stream = torch.cuda.Stream(dev)
     torch.cuda.set_stream(stream)
     sh = stream.cuda_stream
-    outs = {"disparity": disp.data_ptr()}
     NAN = float("nan")
 
-    def step():
-        m.run_device_u8(B, W, H, 1, dl.data_ptr(), dr.data_ptr(), outs, stream=sh,
-                        invalid_value=NAN)
+    def step(n=nb, l=dl, r=dr, outs=None):
+        m.run_device_u8(n, W, H, CH, l.data_ptr(), r.data_ptr(),
+                        outs or {"disparity": disp.data_ptr()}, stream=sh, invalid_value=NAN)
+
+    def timed(fn, steps, warmup):
+        for _ in range(warmup):
+            fn()
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        return max_over_ranks(e0.elapsed_time(e1), device=None if backend != "nccl" else dev)
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize(dev)
     launches_per_step = m.launch_count()
-
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        step()
-    e1.record(stream)
-    torch.cuda.synchronize(dev)
-    if world > 1:
-        dist.barrier()
+    ms_max = timed(step, args.steps, 0)
     clk = clocks.stop()
-    ms = e0.elapsed_time(e1)
-    # per-stage device times from a separate, instrumented pass (the stage
-    # events serialise the launches, so they stay out of the timed region)
+    value = B * args.steps / (ms_max / 1e3)
+    step_ms = ms_max / args.steps
+
+    # every plane run_pipeline returns (PipelineOutput: disparity, probability,
+    # depth; validity planes) for the same batch
+    full = {"disparity": torch.empty((max(nb, 1), H, W), dtype=torch.float32, device=dev),
+            "disparity_valid": torch.empty((max(nb, 1), H, W), dtype=torch.uint8, device=dev),
+            "probability": torch.empty((max(nb, 1), H, W), dtype=torch.float32, device=dev),
+            "depth": torch.empty((max(nb, 1), H, W), dtype=torch.float32, device=dev),
+            "depth_valid": torch.empty((max(nb, 1), H, W), dtype=torch.uint8, device=dev)}
+    full_ptrs = {k: v.data_ptr() for k, v in full.items()}
+
+    def step_full():
+        m.run_device_u8(nb, W, H, CH, dl.data_ptr(), dr.data_ptr(), full_ptrs, stream=sh,
+                        focal=FOCAL, baseline=BASELINE_MM)
+
+    full_ms = timed(step_full, max(3, min(args.steps, 10)), 2) / max(3, min(args.steps, 10))
+    del full
+
+    # weak scaling beside it (N > 1): every rank matches B pairs
+    weak = None
+    if world > 1 and not args.no_weak:
+        ws = weak_shard(B, rank, world)
+        wl_, wr_ = P.synth_batch_gpu(wl["gen"], B, seed0=ws.start, device=local, **wl["over"])
+        wdisp = torch.empty((B, H, W), dtype=torch.float32, device=dev)
+        wsteps = max(3, min(args.steps, 10))
+        wms = timed(lambda: step(B, wl_, wr_, {"disparity": wdisp.data_ptr()}), wsteps, 2)
+        weak = {"value": world * B * wsteps / (wms / 1e3), "unit": "pairs/s",
+                "per_gpu_batch": B, "global_batch": world * B, "ms_per_step": wms / wsteps}
+        del wl_, wr_, wdisp
+
+    # per-stage device times from a separate, instrumented pass (stage events
+    # serialise the launches, so they stay out of the timed region)
     m.set_device_chunks(1)  # one launch per stage: per-launch durations for the roofline
-    step()  # (re)sizes the working set for the unsplit batch outside the profile
+    step()
     torch.cuda.synchronize(dev)
     m.set_profiling(True)
     prof_steps = min(args.steps, 10)
@@ -279,21 +426,19 @@ def run_ours(args):
     torch.cuda.synchronize(dev)
     stages, calls = m.stage_times()
     m.set_profiling(False)
-    # a step may run as several sub-batch calls (PSTEREO_DEVICE_CHUNKS)
-    pairs_per_call = B * prof_steps / max(calls, 1)
-    ms_max = max_over_ranks(ms, device=dev)
-    value = world * B * args.steps / (ms_max / 1e3)
+    m.set_device_chunks(2)
+    pairs_per_call = nb * prof_steps / max(calls, 1)
 
     # ---- e2e through the public ABI with pinned host buffers
-    hl = torch.from_numpy(left).pin_memory()
-    hr = torch.from_numpy(right).pin_memory()
-    hd = torch.empty((B, H, W), dtype=torch.float32).pin_memory()
+    hl = dl.cpu().pin_memory()
+    hr = dr.cpu().pin_memory()
+    hd = torch.empty((max(nb, 1), H, W), dtype=torch.float32).pin_memory()
     houts = {"disparity": hd.data_ptr()}
 
     def step_e2e():
         # async host outputs: step k+1's uploads and kernels run under step k's
         # downloads; every step still moves its own inputs and result
-        m.run_host_u8(B, W, H, 1, hl.data_ptr(), hr.data_ptr(), houts, stream=sh,
+        m.run_host_u8(nb, W, H, CH, hl.data_ptr(), hr.data_ptr(), houts, stream=sh,
                       invalid_value=NAN, async_host=True)
 
     e2e_steps = 0 if args.no_e2e else max(3, min(args.steps, 20))
@@ -309,19 +454,19 @@ def run_ours(args):
     m.wait(sh)  # every step's download has landed in host memory
     torch.cuda.synchronize(dev)
     e2e_s = time.perf_counter() - t0
-    e2e_s = max_over_ranks(e2e_s, device=dev)
-    e2e_value = world * B * e2e_steps / e2e_s if e2e_steps else None
-    # parity spot check of the e2e output against the device-resident run
-    if e2e_steps:
-        dc = disp.cpu()
-        assert torch.equal(torch.isnan(hd), torch.isnan(dc)), "e2e validity differs"
-        assert torch.equal(torch.nan_to_num(hd), torch.nan_to_num(dc)), "e2e output differs"
+    e2e_s = max_over_ranks(e2e_s, device=None if backend != "nccl" else dev)
+    e2e_value = B * e2e_steps / e2e_s if e2e_steps else None
+    if e2e_steps:  # the e2e output equals the device-resident run
+        dc = disp[:nb].cpu()
+        assert torch.equal(torch.isnan(hd[:nb]), torch.isnan(dc)), "e2e validity differs"
+        assert torch.equal(torch.nan_to_num(hd[:nb]), torch.nan_to_num(dc)), "e2e output differs"
 
     # ---- roofline of the dominant kernel: the finest-level k_patches launch
     hbm, peak_kind = peaks()
     dims = P.level_dims(cfg, W, H)
     e_f, w_f, h_f = dims[-1]
-    s_, st_ = cfg.patch_size, max(1, int(round(cfg.patch_size * (1 - cfg.overlap))))
+    s_ = cfg.patch_size
+    st_ = max(1, int(round(cfg.patch_size * (1 - cfg.overlap))))
     npatch_f = len(_axis(w_f, s_, st_)) * len(_axis(h_f, s_, st_))
     # read the left/right/gradient fp32 planes (12 B/px)
     # and the coarser records (16 B/patch), write the records (32 B/patch)
@@ -329,45 +474,47 @@ def run_ours(args):
     patch_ms = stages.get(f"patches_e{e_f}", 0.0) / max(calls, 1)
     achieved = alg_bytes / (patch_ms / 1e3) / 1e9 if patch_ms > 0 else 0.0
     traffic = None
-    fp64 = None
+    pipes = None
     tj = ROOT / "profiles" / "ncu_traffic.json"
-    if tj.exists():
+    if tj.exists() and wl["name"] == "c2":
         t = json.loads(tj.read_text())["k_patches_finest"]
         traffic = t["dram_bytes_per_launch"] / t["pairs_in_launch"] * pairs_per_call
         if "fp64_inst_per_launch" in t and patch_ms > 0:
             # the pipes this kernel actually runs on: FP64 (DADD/DMUL/DFMA) and
-            # XU (float<->double/int conversions); counts from ncu for the same
-            # launch scaled to this batch, time from the live CUDA events; peaks
-            # are this box's measured per-SM rates (scripts/microbench.cu:
-            # DADD 62.6, F2F 15.5 thread-ops/clk/SM) x 148 SMs x max clock
+            # XU (conversions); counts from ncu for the same launch scaled to
+            # this batch, time from the live CUDA events; peaks are this box's
+            # measured per-SM rates (scripts/microbench.cu: DADD 62.6, F2F 15.5
+            # thread-ops/clk/SM) x 148 SMs x max clock
             sm_hz = 148 * 1965e6
-            f_ops = (t["fp64_inst_per_launch"] / t["pairs_in_launch"] * pairs_per_call
-                     / (patch_ms / 1e3))
-            x_ops = (t["conversion_inst_per_launch"] / t["pairs_in_launch"] * pairs_per_call
-                     / (patch_ms / 1e3))
-            fp64 = {"unit": "T thread-inst/s",
-                    "fp64_achieved": f_ops / 1e12, "fp64_peak": 62.6 * sm_hz / 1e12,
-                    "fp64_frac": f_ops / (62.6 * sm_hz),
-                    "xu_achieved": x_ops / 1e12, "xu_peak": 15.5 * sm_hz / 1e12,
-                    "xu_frac": x_ops / (15.5 * sm_hz)}
-    step_ms = ms_max / args.steps
-    b_pair = W * H * (2 * 1 + 4 + 1)  # inputs + fp32 disparity + u8 mask
+            scale = pairs_per_call / t["pairs_in_launch"] / (patch_ms / 1e3)
+            f_ops = t["fp64_inst_per_launch"] * scale
+            x_ops = t["conversion_inst_per_launch"] * scale
+            pipes = {"unit": "T thread-inst/s",
+                     "fp64_achieved": f_ops / 1e12, "fp64_peak": 62.6 * sm_hz / 1e12,
+                     "fp64_frac": f_ops / (62.6 * sm_hz),
+                     "xu_achieved": x_ops / 1e12, "xu_peak": 15.5 * sm_hz / 1e12,
+                     "xu_frac": x_ops / (15.5 * sm_hz)}
+            if "warp_inst_per_launch" in t:
+                i_ops = t["warp_inst_per_launch"] * scale
+                pipes["issue_frac"] = i_ops / (4 * sm_hz)
+    b_pair = bytes_per_pair(wl)
     line = {
-        "metric": "640x480 stereo pairs/sec", "value": value, "unit": "pairs/s",
+        "metric": metric_name(wl), "value": value, "unit": "pairs/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded config-0 generator, see DESIGN.md)",
-        "config": {"workload": "config2: batch of 640x480 u8 gray pairs, exps 3..1, 8x8 patches "
-                               "stride 4, variance off",
-                   "global_batch": world * B, "per_gpu_batch": B,
-                   "parallelism": f"pair-sharded x{world} (no collective)",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded BASELINE generator, see DESIGN.md)",
+        "config": {"workload": wl["desc"], "global_batch": B, "per_gpu_batch": nb,
+                   "parallelism": f"pair-sharded x{world}, contiguous blocks, no collective",
                    "inputs": "generated on device (pstereo_gpu_synth, byte-identical to the "
                              "host generator)",
-                   "l2": (f"inputs {2 * B * W * H / 1e6:.0f} MB/step per GPU "
-                          + ("> 126 MB L2 (no flush needed)" if 2 * B * W * H > 126e6
-                             else "< 126 MB L2: reduced batch, not a bench number"))},
+                   "output": "fp32 filtered disparity, NaN = invalid (mask folded in)",
+                   "l2": (f"inputs {2 * nb * W * H * CH / 1e6:.0f} MB/step per GPU "
+                          + ("> 126 MB L2 (no flush needed)" if 2 * nb * W * H * CH > 126e6
+                             else "< 126 MB L2: consecutive steps may hit L2 for inputs"))},
         "gpu_launches": launches_per_step * args.steps,
-        "e2e": {"value": e2e_value, "unit": "pairs/s", "h2d_bytes_per_step": 2 * B * W * H,
+        "full_outputs": {"value": B / (full_ms / 1e3), "unit": "pairs/s", "ms_per_step": full_ms,
+                         "planes": "disparity f32 + mask, probability f32, depth f32 + mask"},
+        "e2e": {"value": e2e_value, "unit": "pairs/s", "h2d_bytes_per_step": 2 * B * W * H * CH,
                 "d2h_bytes_per_step": B * W * H * 4, "steps": e2e_steps,
                 "output": "fp32 filtered disparity, NaN at invalid pixels"},
         "roofline": {"bound": "hbm", "kernel": f"k_patches, finest level (exp {e_f})",
@@ -376,26 +523,49 @@ def run_ours(args):
                      "alg_bytes_per_launch": alg_bytes, "launch_ms": patch_ms,
                      "pairs_per_launch": pairs_per_call,
                      "kernel_share_of_step": patch_ms * calls / prof_steps / step_ms,
-                     "pipes": fp64,
-                     "note": "not HBM-bound: a latency/issue-bound FP64 mirror of the "
-                             "reference's double arithmetic (ncu: issue 47%, FP64 34%, XU 42%; "
-                             "DESIGN.md section 4, profiles/r01)"},
-        "path_roofline": {"bytes_per_pair": b_pair, "roofline_pairs_s": hbm * 1e9 / b_pair,
+                     "pipes": pipes,
+                     "note": "not HBM-bound: an issue/FP64-bound mirror of the reference's "
+                             "double arithmetic (DESIGN.md section 4, profiles/)"},
+        "path_roofline": {"bytes_per_pair": b_pair, "roofline_pairs_s": world * hbm * 1e9 / b_pair,
                           "frac": value / (world * hbm * 1e9 / b_pair)},
         "stage_ms_per_step": {k: v / prof_steps for k, v in stages.items()},
         "stage_note": "instrumented pass (stage events serialise launches), outside the timed "
                       "region",
         "clocks": clk,
     }
+    if weak:
+        line["weak_scaling"] = weak
+    if folded:
+        line["functional_only"] = (f"{world} ranks on {ndev} GPU(s): the multi-rank path ran, "
+                                   "the number is not a measurement")
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cores = host_cores()
-        n_cpu = min(B, max(16, 16 * cores))
-        rate, times = cpu_throughput(left[:n_cpu], right[:n_cpu], oracle_cfg(), cores)
+        left, right = dl.cpu().numpy(), dr.cpu().numpy()
+        rate, times, ref_outs = cpu_run(left, right, wl["params"], cores, keep=True)
         _, kind = _cpu_oracle()
         line["cpu_baseline"] = {
             "value": rate, "unit": "pairs/s", "cores": cores, "kind": kind,
-            "sample": f"first {n_cpu} pairs of this batch, {cores} workers x run_pipeline "
-                      f"threads=1; median single-pair runtime_ms {float(np.median(times)):.1f}"}
+            "sample": f"all {nb} pairs of this batch, {cores} workers x run_pipeline threads=1; "
+                      f"median single-pair runtime_ms {float(np.median(times)):.1f}"}
+        # parity of this batch: the GPU's f64 planes against the reference's
+        f64 = {"disparity": torch.empty((nb, H, W), dtype=torch.float64, device=dev),
+               "disparity_valid": torch.empty((nb, H, W), dtype=torch.uint8, device=dev),
+               "probability": torch.empty((nb, H, W), dtype=torch.float64, device=dev),
+               "depth": torch.empty((nb, H, W), dtype=torch.float64, device=dev),
+               "depth_valid": torch.empty((nb, H, W), dtype=torch.uint8, device=dev)}
+        m.run_device_u8(nb, W, H, CH, dl.data_ptr(), dr.data_ptr(),
+                        {k: v.data_ptr() for k, v in f64.items()}, dtype=P.F64, stream=sh,
+                        focal=FOCAL, baseline=BASELINE_MM)
+        torch.cuda.synchronize(dev)
+        line["parity"] = parity_report(ref_outs, f64, 0)
+        # the timed step's own output (fp32, NaN = invalid) for the same pairs
+        dd = disp[:nb].cpu().numpy()
+        ok = all(np.array_equal(~np.isnan(dd[k]), ref_outs[k]["disparity_valid"] != 0) and
+                 np.array_equal(dd[k][~np.isnan(dd[k])],
+                                ref_outs[k]["disparity"].astype(np.float32)[~np.isnan(dd[k])])
+                 for k in range(nb))
+        line["parity"]["timed_output_matches"] = bool(ok)
+        del f64, ref_outs
     if rank == 0:
         print(json.dumps(line), flush=True)
     m.close()
@@ -403,18 +573,10 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def _axis(L, s, stride):
-    c0 = (s - 1) * 0.5
-    cmax = (L - 1) - c0
-    out = []
-    k = 0
-    while True:
-        c = c0 + k * stride
-        if c >= cmax - 1e-9:
-            out.append(cmax)
-            return out
-        out.append(c)
-        k += 1
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
 
 
 def main():
@@ -422,15 +584,27 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--batch", type=int, default=256)
+    ap.add_argument("--workload", default="c2",
+                    help="c2 (default, BASELINE config 2), c1, c3, or c4:WxH:size:stride:ch:batch")
+    ap.add_argument("--batch", type=int, default=0, help="override the workload's global batch")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer leg (profiling)")
+    ap.add_argument("--no-weak", action="store_true", help="skip the weak-scaling leg (N > 1)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # launch the ranks ourselves: one process per GPU (torchrun semantics)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+               "--master-port", str(_free_port()), str(Path(__file__).resolve()), *sys.argv[1:]]
+        raise SystemExit(subprocess.call(cmd))
+    wl = workload(args.workload)
+    if args.batch:
+        wl["batch"] = args.batch
     if args.impl == "reference":
-        run_reference_arm(args)
+        run_reference_arm(args, wl)
     else:
-        run_ours(args)
+        run_ours(args, wl)
 
 
 if __name__ == "__main__":

@@ -543,3 +543,49 @@ def load(kind: str = "port") -> Oracle:
 
 def available(kind: str) -> bool:
     return LIBS[kind].exists()
+
+
+# ---- BASELINE.json input generator, test side (oracle/libbdis_synth.so) ----
+# The same plain-C generator the product ships (csrc/synth.c), compiled into a
+# separate library so the reference arm of bench.py never loads the product.
+
+class SynthSpec(C.Structure):
+    _fields_ = [("width", C.c_int), ("height", C.c_int), ("channels", C.c_int),
+                ("seed", C.c_uint64), ("octaves", C.c_int), ("base_wavelength", C.c_double),
+                ("d_min", C.c_double), ("d_range", C.c_double), ("blur_sigma", C.c_double),
+                ("noise_sigma", C.c_double), ("stress", C.c_int)]
+
+
+_SYNTH = None
+
+
+def _synth_lib():
+    global _SYNTH
+    if _SYNTH is None:
+        path = HERE / "libbdis_synth.so"
+        if not path.exists():
+            raise FileNotFoundError(f"{path} not built (make -C oracle)")
+        L = C.CDLL(str(path))
+        L.pstereo_synth_default.argtypes = [C.POINTER(SynthSpec), C.c_int]
+        L.pstereo_synth_batch.argtypes = [C.POINTER(SynthSpec), C.c_int, C.c_uint64, u8p, u8p,
+                                          C.c_int]
+        _SYNTH = L
+    return _SYNTH
+
+
+def synth_batch(config: int, n: int, seed0: int = 0, threads: int = 8, **overrides):
+    """Pairs seed0..seed0+n-1 of BASELINE.json configs[config]: (left, right)
+    uint8 arrays [n, H, W(, C)], byte-identical to the product's generator."""
+    L = _synth_lib()
+    s = SynthSpec()
+    L.pstereo_synth_default(C.byref(s), config)
+    for k, v in overrides.items():
+        setattr(s, k, v)
+    shape = (n, s.height, s.width) if s.channels == 1 else (n, s.height, s.width, s.channels)
+    left = np.zeros(shape, np.uint8)
+    right = np.zeros(shape, np.uint8)
+    rc = L.pstereo_synth_batch(C.byref(s), n, seed0, left.ctypes.data_as(u8p),
+                               right.ctypes.data_as(u8p), threads)
+    if rc:
+        raise OracleError(rc, "synth_batch")
+    return left, right

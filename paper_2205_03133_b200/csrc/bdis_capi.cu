@@ -228,6 +228,10 @@ struct pstereo_ctx {
   bool timeline = false;
   std::vector<std::pair<std::string, cudaEvent_t>> tl;
   int out_parity = 0;
+  // per staging set: recorded on s_out after that set's downloads; a later call
+  // writing the same set waits for it (async_host calls N and N+2 share a set)
+  cudaEvent_t stage_free[2] = {nullptr, nullptr};
+  bool stage_pending[2] = {false, false};
   // host-buffer pipeline (chunked H2D / compute / D2H)
   int chunk_pairs = 0;
   int device_chunks = 2;  // sub-batches of a device call (PSTEREO_DEVICE_CHUNKS)
@@ -432,6 +436,8 @@ void pstereo_gpu_destroy(pstereo_ctx* ctx) {
   for (auto& set : ctx->out_stage)
     for (auto& b : set) b.release();
   for (auto e : ctx->chunk_events) cudaEventDestroy(e);
+  for (auto e : ctx->stage_free)
+    if (e) cudaEventDestroy(e);
   if (ctx->s_in) cudaStreamDestroy(ctx->s_in);
   if (ctx->s_out) cudaStreamDestroy(ctx->s_out);
   if (ctx->s_comp) cudaStreamDestroy(ctx->s_comp);
@@ -1004,6 +1010,12 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
     cudaEventRecord(e, t);
     ctx->tl.emplace_back(what, e);
   };
+  const int parity = ctx->out_parity;
+  if (host_out && ctx->stage_pending[parity]) {
+    // the staging set this call writes may still be downloading for the call
+    // before last (async_host): the kernels start only after those copies
+    CK(cudaStreamWaitEvent(s, ctx->stage_free[parity], 0));
+  }
   if (pipelined || split) {
     // the helper streams start behind the work already queued on the caller's stream
     CK(cudaEventRecord(ev_start, s));
@@ -1088,6 +1100,10 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
   if (host_out) {
     ctx->out_parity ^= 1;
     CK(cudaEventRecord(ev_out, ctx->s_out));
+    if (!ctx->stage_free[parity])
+      CK(cudaEventCreateWithFlags(&ctx->stage_free[parity], cudaEventDisableTiming));
+    CK(cudaEventRecord(ctx->stage_free[parity], ctx->s_out));
+    ctx->stage_pending[parity] = true;
     if (!async) CK(cudaStreamWaitEvent(s, ev_out, 0));
   }
   const bool need_sync = !async && (host_out || !hstats.empty() || want_finest);

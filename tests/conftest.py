@@ -48,6 +48,15 @@ def ref(built):
 
 
 @pytest.fixture(scope="session")
+def checker(built):
+    """The parity checker for GPU tests: the reference itself (oracle/_ref)
+    wherever it was built, else the plain-C restatement pinned to it."""
+    from oracle import pyoracle
+
+    return pyoracle.load("reference" if pyoracle.available("reference") else "port")
+
+
+@pytest.fixture(scope="session")
 def gpu(built):
     if not _gpu_available():
         pytest.skip("no CUDA device")

@@ -94,3 +94,61 @@ def compare_pair(gpu, k, pipe, match, cfg, report=None):
                                        bits(match["var_disp"][m])).mean()) if m.any() else 1.0
     stats["valid_fraction"] = float(pipe["disparity_valid"].mean())
     return stats
+
+
+def random_case(P, seed):
+    """A random valid PipelineConfig and pair (tests/test_gpu_parity.py's
+    randomized sweep; tests/test_port_vs_ref.py pins the port to the reference
+    on the same cases). Returns (cfg, left, right) uint8 rasters."""
+    rng = np.random.default_rng(1000 + seed)
+    size = int(rng.integers(2, 21))
+    stride = int(rng.integers(1, size + 1))
+    fe = int(rng.integers(0, 2))
+    ce = fe + int(rng.integers(0, 4))
+    minw = size << ce
+    w = int(rng.integers(minw, minw + 120))
+    h = int(rng.integers(minw, minw + 90))
+    offs = sorted(set(float(x) for x in rng.choice([0.25, 0.5, 0.75, 1.0, 1.5, 2.0],
+                                                   size=int(rng.integers(1, 4)), replace=False)))
+    cfg = P.PipelineConfig(coarsest_exp=ce, finest_exp=fe, patch_size=size,
+                           overlap=1.0 - stride / size,
+                           min_iterations=int(rng.integers(1, 6)), max_iterations=12,
+                           window_offsets=offs,
+                           pixel_threshold=float(rng.uniform(0.05, 0.4)),
+                           gamma=float(rng.uniform(0.1, 1.0)),
+                           valid_patch_ratio=float(rng.uniform(0.5, 1.0)),
+                           estimate_variance=bool(rng.integers(0, 2)))
+    ch = int(rng.choice([1, 3, 4]))
+    l, r = P.synth_pair(0, seed=seed, width=w, height=h, channels=min(ch, 3),
+                        d_range=float(rng.uniform(2, 12)), d_min=float(rng.uniform(0, 3)))
+    if ch == 4:  # RGBA: alpha == 0 marks invalid pixels (src/image.cpp:32-34)
+        alpha = [np.full((h, w, 1), 255, np.uint8) for _ in range(2)]
+        for a in alpha:
+            a[rng.random((h, w)) < rng.uniform(0, 0.05)] = 0
+            y0, x0 = int(rng.integers(0, h)), int(rng.integers(0, w))
+            a[y0:y0 + int(rng.integers(1, h // 2 + 2)), x0:x0 + int(rng.integers(1, w // 2 + 2))] = 0
+        l, r = np.concatenate([l, alpha[0]], axis=2), np.concatenate([r, alpha[1]], axis=2)
+    return cfg, l, r
+
+
+def compare_oracles(a, b, cfg, left, right, focal=500.0, baseline=5.0):
+    """Runs run_pipeline + match_stereo of two checker libraries on the same
+    raster pair and asserts every output identical (f64 bits; MatchStats and
+    the finest records included)."""
+    la, lva = a.to_grayscale(left)
+    ra, rva = a.to_grayscale(right)
+    lb, lvb = b.to_grayscale(left)
+    rb, rvb = b.to_grayscale(right)
+    for x, y in ((la, lb), (lva, lvb), (ra, rb), (rva, rvb)):
+        assert np.array_equal(bits(x) if x.dtype == np.float64 else x, y)
+    pa, ma = run_oracle(a, la, ra, cfg, focal, baseline, lva, rva)
+    pb, mb = run_oracle(b, lb, rb, cfg, focal, baseline, lvb, rvb)
+    for res_a, res_b in ((pa, pb), (ma, mb)):
+        for k in res_a:
+            if k == "runtime_ms":
+                continue
+            va, vb = res_a[k], res_b[k]
+            if isinstance(va, np.ndarray):
+                assert np.array_equal(bits(va), bits(vb)), k
+            else:
+                assert va == vb, k

@@ -1,5 +1,6 @@
-"""GPU parity: the sm_100a path through the C ABI against the CPU oracle
-(oracle/bdis_oracle.c, itself pinned bit-exact to the reference build) on the
+"""GPU parity: the sm_100a path through the C ABI against the reference itself
+(oracle/_ref, the unmodified reference sources; the plain-C restatement
+oracle/bdis_oracle.c, pinned bit-exact to it, where _ref was not built) on the
 same seeded inputs. Bit-exact except var_disp / depth sigma (1e-3 rel, see
 tests/parity.py)."""
 import os
@@ -7,109 +8,109 @@ import os
 import numpy as np
 import pytest
 
-from tests.parity import compare_pair, run_gpu_batch, run_oracle
+from tests.parity import compare_pair, random_case, run_gpu_batch, run_oracle
 
 pytestmark = pytest.mark.gpu
 
 FOCAL, BASELINE = 500.0, 5.0
 
 
-def _check(P, port, cfg, left_u8, right_u8, lv=None, rv=None):
+def _check(P, checker, cfg, left_u8, right_u8, lv=None, rv=None):
     """left_u8/right_u8: [n,h,w(,c)] uint8 rasters."""
     gpu = run_gpu_batch(P, cfg, left_u8, right_u8, FOCAL, BASELINE)
     out = []
     for k in range(left_u8.shape[0]):
-        lf, lvk = port.to_grayscale(left_u8[k])
-        rf, rvk = port.to_grayscale(right_u8[k])
-        pipe, match = run_oracle(port, lf, rf, cfg, FOCAL, BASELINE, lvk, rvk)
+        lf, lvk = checker.to_grayscale(left_u8[k])
+        rf, rvk = checker.to_grayscale(right_u8[k])
+        pipe, match = run_oracle(checker, lf, rf, cfg, FOCAL, BASELINE, lvk, rvk)
         out.append(compare_pair(gpu, k, pipe, match, cfg))
     return out
 
 
-def test_config0_pair_bitexact(gpu, port):
+def test_config0_pair_bitexact(gpu, checker):
     P = gpu
     l, r = P.synth_pair(0)
-    _check(P, port, P.PipelineConfig.baseline(0), l[None], r[None])
+    _check(P, checker, P.PipelineConfig.baseline(0), l[None], r[None])
 
 
-def test_config1_stress_variance(gpu, port):
+def test_config1_stress_variance(gpu, checker):
     P = gpu
     l, r = P.synth_pair(1)
-    st = _check(P, port, P.PipelineConfig.baseline(1), l[None], r[None])
+    st = _check(P, checker, P.PipelineConfig.baseline(1), l[None], r[None])
     print("config1 agreement", st)
 
 
-def test_reference_defaults(gpu, port):
+def test_reference_defaults(gpu, checker):
     P = gpu
     l, r = P.synth_pair(0, seed=7)
-    _check(P, port, P.PipelineConfig(), l[None], r[None])
+    _check(P, checker, P.PipelineConfig(), l[None], r[None])
 
 
-def test_batch_of_seeds(gpu, port):
+def test_batch_of_seeds(gpu, checker):
     P = gpu
     left, right = P.synth_batch(0, 4, seed0=10, width=320, height=240)
-    _check(P, port, P.PipelineConfig.baseline(0), left, right)
+    _check(P, checker, P.PipelineConfig.baseline(0), left, right)
 
 
 @pytest.mark.parametrize("size,stride", [(8, 2), (12, 4), (16, 6), (10, 5), (9, 3)])
-def test_patch_size_stride_sweep(gpu, port, size, stride):
+def test_patch_size_stride_sweep(gpu, checker, size, stride):
     P = gpu
     l, r = P.synth_pair(0, seed=3, width=200, height=150)
     cfg = P.PipelineConfig(coarsest_exp=2, finest_exp=1, patch_size=size,
                            overlap=1.0 - stride / size, estimate_variance=True)
-    _check(P, port, cfg, l[None], r[None])
+    _check(P, checker, cfg, l[None], r[None])
 
 
 @pytest.mark.parametrize("w,h", [(97, 75), (64, 48), (33, 17)])
-def test_odd_dimensions(gpu, port, w, h):
+def test_odd_dimensions(gpu, checker, w, h):
     P = gpu
     l, r = P.synth_pair(0, seed=5, width=w, height=h, blur_sigma=8.0, d_range=6.0, d_min=1.0)
     cfg = P.PipelineConfig(coarsest_exp=1, finest_exp=0, patch_size=6, overlap=0.5,
                            estimate_variance=True)
-    _check(P, port, cfg, l[None], r[None])
+    _check(P, checker, cfg, l[None], r[None])
 
 
 @pytest.mark.parametrize("w,h", [(97, 75), (131, 67)])
-def test_odd_dimensions_upsampled(gpu, port, w, h):
+def test_odd_dimensions_upsampled(gpu, checker, w, h):
     """Odd full-resolution sizes with finest_exp 1: the last finest column/row
     covers one full-resolution pixel, which the component areas must weigh."""
     P = gpu
     l, r = P.synth_pair(0, seed=6, width=w, height=h, blur_sigma=8.0, d_range=6.0, d_min=1.0)
     cfg = P.PipelineConfig(coarsest_exp=2, finest_exp=1, patch_size=6, overlap=0.5,
                            estimate_variance=True, gamma=0.05)
-    _check(P, port, cfg, l[None], r[None])
+    _check(P, checker, cfg, l[None], r[None])
 
 
-def test_rgb_and_rgba_validity(gpu, port):
+def test_rgb_and_rgba_validity(gpu, checker):
     P = gpu
     l, r = P.synth_pair(0, seed=11, width=160, height=120, channels=3)
     cfg = P.PipelineConfig(coarsest_exp=2, finest_exp=1, patch_size=8, overlap=0.5)
-    _check(P, port, cfg, l[None], r[None])
+    _check(P, checker, cfg, l[None], r[None])
     # RGBA: alpha == 0 marks invalid pixels (src/image.cpp:32-34)
     rng = np.random.default_rng(0)
     la = np.concatenate([l, np.full(l.shape[:2] + (1,), 255, np.uint8)], axis=2)
     ra = np.concatenate([r, np.full(r.shape[:2] + (1,), 255, np.uint8)], axis=2)
     la[30:60, 40:80, 3] = 0
     ra[rng.random(ra.shape[:2]) < 0.01, 3] = 0
-    _check(P, port, cfg, la[None], ra[None])
+    _check(P, checker, cfg, la[None], ra[None])
 
 
-def test_float_api_with_mask(gpu, port):
+def test_float_api_with_mask(gpu, checker):
     """GrayImage entry point with an explicit validity mask."""
     P = gpu
     l, r = P.synth_pair(0, seed=2, width=128, height=96)
-    lf, _ = port.to_grayscale(l)
-    rf, _ = port.to_grayscale(r)
+    lf, _ = checker.to_grayscale(l)
+    rf, _ = checker.to_grayscale(r)
     lv = np.ones_like(l, np.uint8)
     lv[:, 100:] = 0
     cfg = P.PipelineConfig(coarsest_exp=2, finest_exp=1, patch_size=8, overlap=0.5,
                            estimate_variance=True)
     gpu_out = run_gpu_batch(P, cfg, lf[None], rf[None], FOCAL, BASELINE, left_valid=lv[None])
-    pipe, match = run_oracle(port, lf, rf, cfg, FOCAL, BASELINE, lv, None)
+    pipe, match = run_oracle(checker, lf, rf, cfg, FOCAL, BASELINE, lv, None)
     compare_pair(gpu_out, 0, pipe, match, cfg)
 
 
-def test_shifted_analytic_pair(gpu, port):
+def test_shifted_analytic_pair(gpu, checker):
     """The reference's own end-to-end case (tests/test_coarse_to_fine.cpp:253-287):
     64x48 sinusoid pair shifted by 2 px, exps 2..1, recovered within 0.2 px."""
     P = gpu
@@ -128,30 +129,30 @@ def test_shifted_analytic_pair(gpu, port):
     valid = res["disparity_valid"].astype(bool)
     assert valid.sum() > 64 * 48 / 2
     assert np.abs(res["disparity"][valid] - 2.0).max() < 0.2
-    pipe, match = run_oracle(port, left, right, cfg, 1.0, 1.0)
+    pipe, match = run_oracle(checker, left, right, cfg, 1.0, 1.0)
     np.testing.assert_array_equal(res["disparity"], match["disparity"])
 
 
-def test_config3_full_size(gpu, port):
+def test_config3_full_size(gpu, checker):
     """BASELINE config 3: 1280x1024, exps 4..1, 12x12 patches stride 4,
     variance on -- the largest single-pair configuration."""
     P = gpu
     l, r = P.synth_pair(3)
-    _check(P, port, P.PipelineConfig.baseline(3), l[None], r[None])
+    _check(P, checker, P.PipelineConfig.baseline(3), l[None], r[None])
 
 
 @pytest.mark.parametrize("w,h,ch,size,stride", [
     (320, 240, 3, 8, 2), (320, 240, 3, 12, 6), (320, 240, 1, 16, 4), (640, 480, 3, 12, 2),
     pytest.param(1920, 1080, 3, 16, 6, marks=pytest.mark.slow),
 ])
-def test_config4_sweep(gpu, port, w, h, ch, size, stride):
+def test_config4_sweep(gpu, checker, w, h, ch, size, stride):
     """BASELINE config 4: sizes x patch sizes x strides, RGB through the
     Rec.601 conversion (src/image.cpp:36)."""
     P = gpu
     l, r = P.synth_pair(4, seed=size * 10 + stride, width=w, height=h, channels=ch)
     cfg = P.PipelineConfig(coarsest_exp=3, finest_exp=1, patch_size=size,
                            overlap=1.0 - stride / size)
-    _check(P, port, cfg, l[None], r[None])
+    _check(P, checker, cfg, l[None], r[None])
 
 
 @pytest.mark.parametrize("w,h,ch,size,stride,n", [
@@ -159,7 +160,7 @@ def test_config4_sweep(gpu, port, w, h, ch, size, stride):
     (640, 480, 3, 8, 2, 12),     # dense wide grid
     (1280, 1024, 3, 8, 4, 6),    # wide s=8 levels, vectorised RGB pyramid
 ])
-def test_planner_shapes_batches(gpu, port, w, h, ch, size, stride, n):
+def test_planner_shapes_batches(gpu, checker, w, h, ch, size, stride, n):
     """Batches large enough that the band planner keeps its tall-band shapes
     (s >= 12 starving bands, dense or wide grids) and the RGB pyramid path:
     every pair bit-identical to the oracle."""
@@ -167,7 +168,7 @@ def test_planner_shapes_batches(gpu, port, w, h, ch, size, stride, n):
     left, right = P.synth_batch(4, n, seed0=50 + size, width=w, height=h, channels=ch)
     cfg = P.PipelineConfig(coarsest_exp=4, finest_exp=1, patch_size=size,
                            overlap=1.0 - stride / size)
-    _check(P, port, cfg, left, right)
+    _check(P, checker, cfg, left, right)
 
 
 def test_empty_batch_and_limits(gpu):
@@ -191,7 +192,7 @@ def test_determinism(gpu):
         assert np.array_equal(a[k], b[k]), k
 
 
-def test_large_batch_determinism(gpu, port):
+def test_large_batch_determinism(gpu, checker):
     """Many CTAs per SM over several waves (stale shared memory from earlier
     CTAs, every SM busy): device-resident runs repeat bit-for-bit, the chunked
     host path agrees with them, and sampled pairs match the oracle."""
@@ -219,9 +220,9 @@ def test_large_batch_determinism(gpu, port):
         assert np.array_equal(np.isnan(runs[0]), np.isnan(other))
         assert np.array_equal(np.nan_to_num(runs[0]), np.nan_to_num(other))
     for k in (0, n - 1):
-        lf, lv = port.to_grayscale(left[k])
-        rf, rv = port.to_grayscale(right[k])
-        pipe, _ = run_oracle(port, lf, rf, cfg, 1.0, 1.0, lv, rv)
+        lf, lv = checker.to_grayscale(left[k])
+        rf, rv = checker.to_grayscale(right[k])
+        pipe, _ = run_oracle(checker, lf, rf, cfg, 1.0, 1.0, lv, rv)
         ov = np.asarray(pipe["disparity_valid"]).astype(bool)
         assert np.array_equal(~np.isnan(runs[0][k]), ov)
         od = np.asarray(pipe["disparity"]).astype(np.float32)
@@ -285,6 +286,40 @@ def test_async_host_calls_overlap_safely(gpu):
         assert np.array_equal(np.nan_to_num(a), np.nan_to_num(b))
 
 
+def test_async_host_many_large_calls(gpu):
+    """Eight back-to-back async_host calls on distinct 32-pair 640x480 batches,
+    each with its own pinned outputs, one wait() at the end. The outputs are
+    three f64 planes + a mask (26 B/px down against 2 B/px up), so each call's
+    downloads take several times its uploads and kernels: call k+2 reuses the
+    staging set call k is still downloading -- every host plane
+    must still equal the synchronous result of its own batch."""
+    import torch
+
+    P = gpu
+    n, w, h, calls = 32, 640, 480, 8
+    cfg = P.PipelineConfig.baseline(0)
+    planes = ("disparity", "disparity_valid", "probability", "depth")
+    with P.Matcher(cfg, w, h, n) as m:
+        batches = [P.synth_batch(0, n, seed0=1000 + k * n) for k in range(calls)]
+        want = [m.run_batch(l, r, focal=500.0, baseline=5.0, dtype=P.F64, want=planes)
+                for l, r in batches]
+        pinned = [(torch.from_numpy(l).pin_memory(), torch.from_numpy(r).pin_memory())
+                  for l, r in batches]
+        outs = [{k: torch.full((n, h, w), 7, dtype=torch.uint8 if "valid" in k
+                               else torch.float64).pin_memory() for k in planes}
+                for _ in range(calls)]
+        for (hl, hr), o in zip(pinned, outs):
+            m.run_host_u8(n, w, h, 1, hl.data_ptr(), hr.data_ptr(),
+                          {k: v.data_ptr() for k, v in o.items()}, dtype=P.F64, focal=500.0,
+                          baseline=5.0, async_host=True)
+        m.wait()
+    for k in range(calls):
+        for name in planes:
+            a = want[k][name]
+            b = outs[k][name].numpy()
+            assert np.array_equal(a.view(np.uint8), b.view(np.uint8)), (k, name)
+
+
 def test_device_sub_batches_are_invisible(gpu):
     """A device call split into sub-batches over two compute streams
     (pstereo_gpu_set_device_chunks, default 2 for >= 32 pairs) writes exactly
@@ -314,7 +349,7 @@ def test_device_sub_batches_are_invisible(gpu):
             assert np.array_equal(a.view(np.uint8), b.view(np.uint8)), (chunks, k)
 
 
-def test_disparity_only_output_path(gpu, port):
+def test_disparity_only_output_path(gpu, checker):
     """Requests of the disparity plane alone (+ validity) take a dedicated
     output kernel: same values as the full-plane request and the oracle."""
     P = gpu
@@ -331,7 +366,7 @@ def test_disparity_only_output_path(gpu, port):
             assert np.array_equal(a["disparity_valid"], b["disparity_valid"])
             want_c = np.where(a["disparity_valid"] != 0, a["disparity"], -1.0)[:, ::-1]
             assert np.array_equal(c["disparity"], want_c.astype(c["disparity"].dtype))
-    _check(P, port, cfg, left, right)
+    _check(P, checker, cfg, left, right)
 
 
 def test_invalid_value_fill(gpu):
@@ -355,37 +390,10 @@ def test_invalid_value_fill(gpu):
 
 
 @pytest.mark.parametrize("seed", range(int(os.environ.get("PSTEREO_RANDOM_CASES", "16"))))
-def test_randomized_configs(gpu, port, seed):
+def test_randomized_configs(gpu, checker, seed):
     """Random valid PipelineConfigs and frame sizes (patch sizes 2..20, any
-    stride, 1..4 levels, window offsets, thresholds, variance on/off, gray or
-    RGB): bit-exact against the oracle every time."""
+    stride, 1..4 levels, window offsets, thresholds, variance on/off, gray,
+    RGB or RGBA with holes): bit-exact against the reference every time."""
     P = gpu
-    rng = np.random.default_rng(1000 + seed)
-    size = int(rng.integers(2, 21))
-    stride = int(rng.integers(1, size + 1))
-    fe = int(rng.integers(0, 2))
-    ce = fe + int(rng.integers(0, 4))
-    minw = size << ce
-    w = int(rng.integers(minw, minw + 120))
-    h = int(rng.integers(minw, minw + 90))
-    offs = sorted(set(float(x) for x in rng.choice([0.25, 0.5, 0.75, 1.0, 1.5, 2.0],
-                                                   size=int(rng.integers(1, 4)), replace=False)))
-    cfg = P.PipelineConfig(coarsest_exp=ce, finest_exp=fe, patch_size=size,
-                           overlap=1.0 - stride / size,
-                           min_iterations=int(rng.integers(1, 6)), max_iterations=12,
-                           window_offsets=offs,
-                           pixel_threshold=float(rng.uniform(0.05, 0.4)),
-                           gamma=float(rng.uniform(0.1, 1.0)),
-                           valid_patch_ratio=float(rng.uniform(0.5, 1.0)),
-                           estimate_variance=bool(rng.integers(0, 2)))
-    ch = int(rng.choice([1, 3, 4]))
-    l, r = P.synth_pair(0, seed=seed, width=w, height=h, channels=min(ch, 3),
-                        d_range=float(rng.uniform(2, 12)), d_min=float(rng.uniform(0, 3)))
-    if ch == 4:  # RGBA: alpha == 0 marks invalid pixels (src/image.cpp:32-34)
-        alpha = [np.full((h, w, 1), 255, np.uint8) for _ in range(2)]
-        for a in alpha:
-            a[rng.random((h, w)) < rng.uniform(0, 0.05)] = 0
-            y0, x0 = int(rng.integers(0, h)), int(rng.integers(0, w))
-            a[y0:y0 + int(rng.integers(1, h // 2 + 2)), x0:x0 + int(rng.integers(1, w // 2 + 2))] = 0
-        l, r = np.concatenate([l, alpha[0]], axis=2), np.concatenate([r, alpha[1]], axis=2)
-    _check(P, port, cfg, l[None], r[None])
+    cfg, l, r = random_case(P, seed)
+    _check(P, checker, cfg, l[None], r[None])
