@@ -376,6 +376,54 @@ int pstereo_write_metrics_csv(const char* path, const pstereo_metrics_row* rows,
 int pstereo_read_metrics_csv(const char* path, pstereo_metrics_row* rows, int cap,
                              int* n_rows, char* msg, size_t msg_cap);
 
+/* IoErrorKind (inc/errors.hpp:14-19) of the last PSTEREO_EIO returned on the
+ * calling thread by one of the functions above, -1 if none. */
+#define PSTEREO_IO_MISSING_FILE 0
+#define PSTEREO_IO_DECODE_FAILURE 1
+#define PSTEREO_IO_DIMENSION_MISMATCH 2
+#define PSTEREO_IO_WRITE_FAILURE 3
+int pstereo_last_io_kind(void);
+
+/* ---- helpers of the C++ drop-in headers (include/pstereo/ headers) ---- */
+/* The calling host thread's current CUDA device (cudaGetDevice). */
+int pstereo_gpu_current_device(int* device);
+/* cudaSetDevice for the calling host thread. */
+int pstereo_gpu_set_current_device(int device);
+/* to_grayscale (src/image.cpp:16-43) of one HOST raster [height][width]
+ * [channels] on `device` (the k_gray_u8 kernel of the match path): fp32 gray
+ * and u8 validity (alpha == 0 invalid) into host buffers. Channels other
+ * than 1, 3, 4 return PSTEREO_ECONFIG (the reference throws
+ * std::invalid_argument). Blocking. */
+int pstereo_gpu_to_grayscale(int device, int width, int height, int channels,
+                             const uint8_t* pixels, float* gray, uint8_t* valid);
+
+/* ---- pair sharding over several devices ----
+ * The reference's only parallelism is parallel_patches
+ * (src/coarse_to_fine.cpp:184-205): worker threads over the patches of one
+ * pair. Here whole pairs are the unit: a pstereo_multi owns one context and
+ * one persistent host thread per entry of `devices` (entries may repeat: two
+ * contexts on one GPU). A match call splits n_pairs into contiguous blocks,
+ * block d = pairs [d*n/N, (d+1)*n/N), and every worker runs its block through
+ * its own context from HOST buffers (its own uploads, kernels and downloads;
+ * no collective, no peer traffic), writing the block's slice of every output
+ * plane, stats and finest records. The call returns when every block is
+ * done; results are identical to one context running all pairs. max_pairs is
+ * the largest n_pairs a call may pass. */
+typedef struct pstereo_multi pstereo_multi;
+int pstereo_multi_create(const int* devices, int n_devices, const pstereo_params* p,
+                         int max_width, int max_height, int max_pairs,
+                         pstereo_multi** out);
+void pstereo_multi_destroy(pstereo_multi* m);
+const char* pstereo_multi_last_error(const pstereo_multi* m);
+int pstereo_multi_n_devices(const pstereo_multi* m);
+/* pstereo_gpu_match_u8 semantics with host inputs and host outputs
+ * (out->on_device must be 0; async_host is ignored). When `ms_per_device` is
+ * non-NULL it receives each worker's wall time of its block (ms). */
+int pstereo_multi_match_u8(pstereo_multi* m, int n_pairs, int width, int height,
+                           int channels, const uint8_t* left, const uint8_t* right,
+                           double focal_px, double baseline,
+                           const pstereo_outputs* out, double* ms_per_device);
+
 #ifdef __cplusplus
 }
 #endif

@@ -18,13 +18,15 @@ and every compute call needs an sm_100 device.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 from pathlib import Path
 
 import numpy as np
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "libpstereo_gpu.so"
+# PSTEREO_GPU_LIB: an alternative build of the same library (A/B timing runs)
+LIB_PATH = Path(os.environ.get("PSTEREO_GPU_LIB", PKG / "libpstereo_gpu.so"))
 
 PSTEREO_OK, PSTEREO_EINTERNAL, PSTEREO_ECONFIG, PSTEREO_EDEGENERATE = 0, 1, 2, 4
 MAX_OFF = 16
@@ -147,6 +149,14 @@ def lib() -> C.CDLL:
         L.pstereo_gpu_create.argtypes = [C.c_int, C.POINTER(_Params), C.c_int, C.c_int, C.c_int,
                                          C.POINTER(C.c_void_p)]
         L.pstereo_gpu_destroy.argtypes = [C.c_void_p]
+        L.pstereo_multi_create.argtypes = [C.POINTER(C.c_int), C.c_int, C.POINTER(_Params),
+                                           C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]
+        L.pstereo_multi_destroy.argtypes = [C.c_void_p]
+        L.pstereo_multi_last_error.restype = C.c_char_p
+        L.pstereo_multi_last_error.argtypes = [C.c_void_p]
+        L.pstereo_multi_match_u8.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
+                                             C.c_void_p, C.c_void_p, C.c_double, C.c_double,
+                                             C.POINTER(_Outputs), C.c_void_p]
         L.pstereo_gpu_last_launch_count.argtypes = [C.c_void_p]
         L.pstereo_gpu_set_profiling.argtypes = [C.c_void_p, C.c_int]
         L.pstereo_gpu_set_device_chunks.argtypes = [C.c_void_p, C.c_int]
@@ -615,32 +625,8 @@ class Matcher:
             left = np.ascontiguousarray(left, np.float32)
             right = np.ascontiguousarray(right, np.float32)
             n, h, w = left.shape
-        vt = np.float64 if dtype == F64 else np.float32
-        res = {}
-        o = _Outputs()
-        o.dtype = dtype
-        o.on_device = 0
-        o.flip_rows = int(bool(flip_rows))
-        if invalid_value is not None:
-            o.fill_invalid, o.invalid_value = 1, float(invalid_value)
-        planes = {"disparity": vt, "disparity_valid": np.uint8, "probability": vt, "depth": vt,
-                  "depth_valid": np.uint8, "depth_sigma": vt, "sigma_valid": np.uint8,
-                  "match_disparity": vt, "match_valid": np.uint8, "var_disp": vt}
-        for k in want:
-            a = np.zeros((n, h, w), planes[k])
-            res[k] = a
-            setattr(o, k, a.ctypes.data)
-        st = None
-        if stats:
-            st = (LevelStats * (n * self.n_levels))()
-            o.stats = st
-        fin = cnt = None
-        if finest_cap:
-            fin = (PatchEstimate * (n * finest_cap))()
-            cnt = np.zeros(n, np.int32)
-            o.finest = fin
-            o.finest_count = cnt.ctypes.data_as(i32p)
-            o.finest_cap = finest_cap
+        o, res, st, fin, cnt = _host_outputs(n, h, w, want, dtype, stats, self.n_levels,
+                                             finest_cap, invalid_value, flip_rows)
         if is_u8:
             rc = lib().pstereo_gpu_match_u8(self._h, n, w, h, ch, left.ctypes.data,
                                             right.ctypes.data, 0, focal, baseline, C.byref(o),
@@ -655,19 +641,7 @@ class Matcher:
                                              baseline, C.byref(o), None)
         if rc:
             _raise(rc, self.last_error())
-        if stats:
-            res["stats"] = np.array([s.as_tuple() for s in st], np.int64).reshape(
-                n, self.n_levels, 5)
-        if finest_cap:
-            res["finest"] = []
-            for p in range(n):
-                rows = [(fin[p * finest_cap + k].cx, fin[p * finest_cap + k].cy,
-                         fin[p * finest_cap + k].u, fin[p * finest_cap + k].prob,
-                         fin[p * finest_cap + k].posterior, fin[p * finest_cap + k].sigma_k)
-                        for k in range(min(int(cnt[p]), finest_cap))]
-                res["finest"].append(np.array(rows, np.float64).reshape(-1, 6))
-            res["finest_count"] = cnt
-        return res
+        return _finish_outputs(res, n, self.n_levels, st, fin, cnt, finest_cap)
 
     # ---- device-pointer batched API (the zero-copy path used by bench.py)
     def wait(self, stream=None):
@@ -926,3 +900,112 @@ def run_benchmark_gpu(scenes, cfg: "PipelineConfig", repetitions: int = 10, devi
     agg["valid_px"] = int(px / len(frames) + 0.5)
     agg["runtime_ms"] = ms_ / len(frames)
     return frames, agg
+
+
+def _host_outputs(n, h, w, want, dtype, stats, n_levels, finest_cap, invalid_value, flip_rows):
+    """pstereo_outputs over freshly allocated host planes (numpy)."""
+    vt = np.float64 if dtype == F64 else np.float32
+    res = {}
+    o = _Outputs()
+    o.dtype = dtype
+    o.on_device = 0
+    o.flip_rows = int(bool(flip_rows))
+    if invalid_value is not None:
+        o.fill_invalid, o.invalid_value = 1, float(invalid_value)
+    planes = {"disparity": vt, "disparity_valid": np.uint8, "probability": vt, "depth": vt,
+              "depth_valid": np.uint8, "depth_sigma": vt, "sigma_valid": np.uint8,
+              "match_disparity": vt, "match_valid": np.uint8, "var_disp": vt}
+    for k in want:
+        a = np.zeros((n, h, w), planes[k])
+        res[k] = a
+        setattr(o, k, a.ctypes.data)
+    st = None
+    if stats:
+        st = (LevelStats * max(n * n_levels, 1))()
+        o.stats = st
+    fin = cnt = None
+    if finest_cap:
+        fin = (PatchEstimate * max(n * finest_cap, 1))()
+        cnt = np.zeros(max(n, 1), np.int32)
+        o.finest = fin
+        o.finest_count = cnt.ctypes.data_as(i32p)
+        o.finest_cap = finest_cap
+    return o, res, st, fin, cnt
+
+
+def _finish_outputs(res, n, n_levels, st, fin, cnt, finest_cap):
+    if st is not None:
+        res["stats"] = np.array([st[i].as_tuple() for i in range(n * n_levels)],
+                                np.int64).reshape(n, n_levels, 5)
+    if finest_cap:
+        res["finest"] = []
+        for p in range(n):
+            rows = [(fin[p * finest_cap + k].cx, fin[p * finest_cap + k].cy,
+                     fin[p * finest_cap + k].u, fin[p * finest_cap + k].prob,
+                     fin[p * finest_cap + k].posterior, fin[p * finest_cap + k].sigma_k)
+                    for k in range(min(int(cnt[p]), finest_cap))]
+            res["finest"].append(np.array(rows, np.float64).reshape(-1, 6))
+        res["finest_count"] = cnt[:n]
+    return res
+
+
+class MultiMatcher:
+    """pstereo_multi: one context and one host thread per entry of `devices`
+    (entries may repeat); a batch is split into contiguous pair blocks, one
+    per device, each matched from host memory with no exchange between
+    devices."""
+
+    def __init__(self, cfg: PipelineConfig, max_width: int, max_height: int, max_pairs: int,
+                 devices=(0,)):
+        validate(cfg)
+        self.cfg = cfg
+        self._p = cfg.to_c()
+        devs = (C.c_int * len(devices))(*devices)
+        h = C.c_void_p()
+        rc = lib().pstereo_multi_create(devs, len(devices), C.byref(self._p), max_width,
+                                        max_height, max_pairs, C.byref(h))
+        if rc:
+            _raise(rc, f"pstereo_multi_create failed (devices {list(devices)})")
+        self._h = h
+        self.n_devices = len(devices)
+        self.n_levels = cfg.coarsest_exp - cfg.finest_exp + 1
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().pstereo_multi_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def run_batch(self, left, right, focal=1.0, baseline=1.0, dtype=F32,
+                  want=("disparity", "disparity_valid"), stats=False, finest_cap=0,
+                  invalid_value=None, flip_rows=False):
+        """uint8 pairs [n,h,w] / [n,h,w,c] from host memory; returns the same
+        dict as Matcher.run_batch plus "ms_per_device"."""
+        left = np.ascontiguousarray(left, np.uint8)
+        right = np.ascontiguousarray(right, np.uint8)
+        if left.ndim == 3:
+            (n, h, w), ch = left.shape, 1
+        else:
+            n, h, w, ch = left.shape
+        o, res, st, fin, cnt = _host_outputs(n, h, w, want, dtype, stats, self.n_levels,
+                                             finest_cap, invalid_value, flip_rows)
+        ms = (C.c_double * self.n_devices)()
+        rc = lib().pstereo_multi_match_u8(self._h, n, w, h, ch, left.ctypes.data,
+                                          right.ctypes.data, focal, baseline, C.byref(o),
+                                          C.cast(ms, C.c_void_p))
+        if rc:
+            _raise(rc, lib().pstereo_multi_last_error(self._h).decode())
+        res = _finish_outputs(res, n, self.n_levels, st, fin, cnt, finest_cap)
+        res["ms_per_device"] = list(ms)
+        return res

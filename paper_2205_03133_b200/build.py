@@ -22,7 +22,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 CUDA_SOURCES = ["bdis_kernels.cu", "bdis_patches.cu", "bdis_metrics.cu", "bdis_capi.cu",
                 "bdis_synth.cu", "bdis_render.cu"]
-CXX_SOURCES = ["host_io.cpp"]
+CXX_SOURCES = ["host_io.cpp", "bdis_multi.cpp"]
 TOOLS = ["cli.cpp"]
 C_SOURCES = ["synth.c"]
 HEADERS = ["bdis_device.cuh", "bdis_kernels.h", "synth_core.h"]

@@ -1247,3 +1247,44 @@ extern "C" int pstereo_debug_eval_residual(int device, int width, int height, co
   for (auto* b : {&dqx, &dqy, &d_n}) b->release();
   return rc;
 }
+
+// ---------------------------------------------------------------------------
+// drop-in helpers for the C++ headers (include/pstereo/*.hpp)
+
+extern "C" int pstereo_gpu_current_device(int* device) {
+  if (!device) return PSTEREO_EINTERNAL;
+  return cudaGetDevice(device) == cudaSuccess ? PSTEREO_OK : PSTEREO_EINTERNAL;
+}
+
+extern "C" int pstereo_gpu_set_current_device(int device) {
+  return cudaSetDevice(device) == cudaSuccess ? PSTEREO_OK : PSTEREO_EINTERNAL;
+}
+
+// to_grayscale (src/image.cpp:16-43) of one host raster on `device`, through
+// the k_gray_u8 kernel the match path uses.
+extern "C" int pstereo_gpu_to_grayscale(int device, int width, int height, int channels,
+                                        const uint8_t* pixels, float* gray, uint8_t* valid) {
+  if (width < 0 || height < 0 || (channels != 1 && channels != 3 && channels != 4))
+    return PSTEREO_ECONFIG;
+  const size_t px = size_t(width) * height;
+  if (px == 0) return PSTEREO_OK;
+  if (!pixels || !gray || !valid) return PSTEREO_EINTERNAL;
+  if (cudaSetDevice(device) != cudaSuccess) return PSTEREO_EINTERNAL;
+  DevBuf<uint8_t> src, ok;
+  DevBuf<float> out;
+  int rc = src.ensure(px * channels) == cudaSuccess && ok.ensure(px) == cudaSuccess &&
+                   out.ensure(px) == cudaSuccess
+               ? PSTEREO_OK
+               : PSTEREO_EINTERNAL;
+  if (rc == PSTEREO_OK) {
+    cudaMemcpy(src.p, pixels, px * channels, cudaMemcpyHostToDevice);
+    launch_gray_u8(src.p, channels, (long long)px, out.p, ok.p, nullptr);
+    if (cudaMemcpy(gray, out.p, px * 4, cudaMemcpyDeviceToHost) != cudaSuccess ||
+        cudaMemcpy(valid, ok.p, px, cudaMemcpyDeviceToHost) != cudaSuccess)
+      rc = PSTEREO_EINTERNAL;
+  }
+  src.release();
+  ok.release();
+  out.release();
+  return rc;
+}

@@ -20,6 +20,10 @@
 // values it needs (init_next_level / inherited probability, :257-283) at its
 // patch centres straight from the coarse patch records (bdis::gather).
 #include <cuda_runtime.h>
+
+#include <map>
+#include <mutex>
+#include <utility>
 #include <math.h>
 #include <stdint.h>
 
@@ -355,18 +359,31 @@ size_t pyramid_smem_bytes(const PyrArgs& a) {
   return bufs + 768 * sizeof(double) + 256 * sizeof(float);  // + grayscale tables
 }
 
+cudaError_t ensure_smem_cap(const void* kernel, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> cap;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& c = cap[{dev, kernel}];
+  if (bytes <= c) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) c = bytes;
+  return e;
+}
+
 cudaError_t launch_pyramid(const PyrArgs& a, bool u8, cudaStream_t s) {
   const size_t smem = pyramid_smem_bytes(a);
   dim3 grid((a.hs[a.ce] + 1) / 2, a.n_pairs);  // two bands per CTA
   if (u8 && a.vec8 && a.C == 3) {
-    cudaFuncSetAttribute(k_pyramid<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
+    ensure_smem_cap((const void*)k_pyramid<true, true>, smem);
     k_pyramid<true, true><<<grid, 256, smem, s>>>(a);
   } else if (u8) {
-    cudaFuncSetAttribute(k_pyramid<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    ensure_smem_cap((const void*)k_pyramid<true>, smem);
     k_pyramid<true><<<grid, 256, smem, s>>>(a);
   } else {
-    cudaFuncSetAttribute(k_pyramid<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    ensure_smem_cap((const void*)k_pyramid<false>, smem);
     k_pyramid<false><<<grid, 256, smem, s>>>(a);
   }
   return cudaGetLastError();

@@ -106,6 +106,13 @@ struct PyrArgs {
 size_t pyramid_smem_bytes(const PyrArgs& a);
 cudaError_t launch_pyramid(const PyrArgs& a, bool u8, cudaStream_t s);
 
+// Raises a kernel's dynamic shared-memory cap (cudaFuncAttributeMax-
+// DynamicSharedMemorySize) on the current device to at least `bytes`. The
+// attribute is per function and process-wide, so contexts on other host
+// threads launching the same kernel with other sizes would race on a plain
+// set; this only ever grows it, under a lock.
+cudaError_t ensure_smem_cap(const void* kernel, size_t bytes);
+
 // Finest-level fields written by the fusion kernel, already upsampled values
 // in the output element type (disparity scaled by 2^fe, depth and sigma from
 // the full-resolution disparity, src/coarse_to_fine.cpp:328-337,

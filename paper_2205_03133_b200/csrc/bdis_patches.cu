@@ -745,8 +745,7 @@ template <int S, bool kSmem, bool kValid>
 static cudaError_t launch_t(const Level& L, const Level& P, const PatchParams& pp,
                             const BandPlan& bp, cudaStream_t s) {
   auto kern = k_patches<S, kSmem, kValid>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)bp.smem_bytes);
+  cudaError_t e = ensure_smem_cap((const void*)kern, bp.smem_bytes);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(bp.n_bands, pp.n_pairs);

@@ -32,6 +32,11 @@
 #include "../../include/pstereo_gpu.h"
 #include "synth_core.h"
 
+namespace bdis {
+// bdis_kernels.cu: grow-only, thread-safe dynamic shared-memory cap
+cudaError_t ensure_smem_cap(const void* kernel, size_t bytes);
+}  // namespace bdis
+
 namespace {
 
 thread_local std::string g_synth_error;
@@ -483,17 +488,14 @@ extern "C" int pstereo_gpu_synth(int device, const pstereo_synth_spec* s, int n_
   const size_t smem_cap = 227 * 1024;
   if (smem_h > smem_cap || smem_views > smem_cap)
     return fail(PSTEREO_ECONFIG, "pstereo_gpu_synth: width or blur radius too large");
-  cudaFuncSetAttribute(k_syn_hblur, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_h);
-  cudaFuncSetAttribute(k_syn_vblur, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_v);
+  bdis::ensure_smem_cap((const void*)k_syn_hblur, smem_h);
+  bdis::ensure_smem_cap((const void*)k_syn_vblur, smem_v);
   const bool vtile = smem_vt <= smem_cap;
   if (vtile)
-    cudaFuncSetAttribute(k_syn_vblur_tile, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem_vt);
-  cudaFuncSetAttribute(k_syn_views<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)smem_views);
+    bdis::ensure_smem_cap((const void*)k_syn_vblur_tile, smem_vt);
+  bdis::ensure_smem_cap((const void*)k_syn_views<false>, smem_views);
   if (vcache)
-    cudaFuncSetAttribute(k_syn_views<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem_views_c);
+    bdis::ensure_smem_cap((const void*)k_syn_views<true>, smem_views_c);
 
   // chunked so the scratch stays bounded (~8.1 B per pixel per pair in flight)
   const int chunk = n_pairs < 64 ? n_pairs : 64;

@@ -193,11 +193,11 @@ int run_match(const Args& a, std::ostream& out) {
   const Raster L = load_image(lp), R = load_image(rp);
   // load_stereo_pair (src/io.cpp:265-280): sizes must agree
   if (L.width != R.width || L.height != R.height)
-    throw IoError(lp + " is " + std::to_string(L.width) + "x" + std::to_string(L.height) +
+    throw IoError(IoErrorKind::dimension_mismatch, lp + " is " + std::to_string(L.width) + "x" + std::to_string(L.height) +
                   " but " + rp + " is " + std::to_string(R.width) + "x" +
                   std::to_string(R.height));
   if (L.channels != R.channels)
-    throw IoError(lp + " and " + rp + " differ in channel count");
+    throw IoError(IoErrorKind::dimension_mismatch, lp + " and " + rp + " differ in channel count");
   const CalibrationFile cal = load_calibration(calib);
   if (cal.width != L.width || cal.height != L.height)
     throw ConfigError("calibration is for " + std::to_string(cal.width) + "x" +
@@ -225,7 +225,7 @@ int run_match(const Args& a, std::ostream& out) {
   if (rc) detail::raise(rc, pstereo_gpu_last_error(ctx));
   std::error_code ec;
   std::filesystem::create_directories(out_dir, ec);
-  if (ec) throw IoError("cannot create " + out_dir + ": " + ec.message());
+  if (ec) throw IoError(IoErrorKind::write_failure, "cannot create " + out_dir + ": " + ec.message());
   const std::string dir = out_dir + "/";
   char msg[512];
   auto put = [&](const std::vector<float>& v, const std::string& name) {

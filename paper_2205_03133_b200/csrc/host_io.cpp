@@ -28,11 +28,14 @@ namespace {
 
 struct Error : std::runtime_error {
   int code;
-  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+  int kind;  // IoErrorKind for PSTEREO_EIO (inc/errors.hpp:14-19)
+  Error(int c, const std::string& m, int k = -1) : std::runtime_error(m), code(c), kind(k) {}
 };
 
+thread_local int t_io_kind = -1;
+
 [[noreturn]] void config_error(const std::string& m) { throw Error(PSTEREO_ECONFIG, m); }
-[[noreturn]] void io_error(const std::string& m) { throw Error(PSTEREO_EIO, m); }
+[[noreturn]] void io_error(int kind, const std::string& m) { throw Error(PSTEREO_EIO, m, kind); }
 
 template <class F>
 int guarded(char* msg, size_t cap, F&& body) {
@@ -41,12 +44,14 @@ int guarded(char* msg, size_t cap, F&& body) {
       std::snprintf(msg, cap, "%s", m);
     }
   };
+  t_io_kind = -1;
   try {
     body();
     put("");
     return PSTEREO_OK;
   } catch (const Error& e) {
     put(e.what());
+    t_io_kind = e.kind;
     return e.code;
   } catch (const std::exception& e) {
     put(e.what());
@@ -100,7 +105,7 @@ Kv parse_kv_text(const std::string& text, const std::string& origin) {
 
 std::string read_text(const std::string& path) {
   std::ifstream in(path);
-  if (!in) io_error("cannot open " + path);
+  if (!in) io_error(PSTEREO_IO_MISSING_FILE, "cannot open " + path);
   std::ostringstream buf;
   buf << in.rdbuf();
   return buf.str();
@@ -235,7 +240,7 @@ void load_scene(const std::string& path, pstereo_scene_spec* out) {
 
 std::vector<uint8_t> read_bytes(const std::string& path) {
   std::ifstream in(path, std::ios::binary);
-  if (!in) io_error("cannot open " + path);
+  if (!in) io_error(PSTEREO_IO_MISSING_FILE, "cannot open " + path);
   return std::vector<uint8_t>((std::istreambuf_iterator<char>(in)),
                               std::istreambuf_iterator<char>());
 }
@@ -247,7 +252,7 @@ struct Raster {
 
 // decode_pnm, src/io.cpp:151-198
 Raster decode_pnm(const std::string& path, const std::vector<uint8_t>& b) {
-  auto fail = [&](const std::string& why) { io_error(path + ": " + why); };
+  auto fail = [&](const std::string& why) { io_error(PSTEREO_IO_DECODE_FAILURE, path + ": " + why); };
   size_t pos = 0;
   auto next_token = [&]() {
     while (pos < b.size()) {
@@ -305,7 +310,7 @@ uint8_t paeth(int a, int b, int c) {
 
 Raster decode_png(const std::string& path, const std::vector<uint8_t>& b,
                   bool header_only = false) {
-  auto fail = [&](const std::string& why) { io_error(path + ": " + why); };
+  auto fail = [&](const std::string& why) { io_error(PSTEREO_IO_DECODE_FAILURE, path + ": " + why); };
   size_t pos = 8;
   uint32_t W = 0, H = 0;
   int depth = 0, ctype = -1, interlace = 0;
@@ -524,7 +529,7 @@ Raster load_image(const std::string& path, bool header_only = false) {
   if (b.size() >= 8 && std::memcmp(b.data(), sig, 8) == 0)
     return decode_png(path, b, header_only);
   if (b.size() >= 2 && b[0] == 'P' && (b[1] == '5' || b[1] == '6')) return decode_pnm(path, b);
-  io_error(path + ": unrecognized image format (PNG/PGM/PPM supported)");
+  io_error(PSTEREO_IO_DECODE_FAILURE, path + ": unrecognized image format (PNG/PGM/PPM supported)");
 }
 
 // ---- metrics CSV (src/io.cpp:346-439) -------------------------------------
@@ -560,16 +565,16 @@ double parse_csv_double(const std::string& cell, const std::string& path) {
     if (used != cell.size()) throw std::invalid_argument(cell);
     return v;
   } catch (const std::exception&) {
-    io_error(path + ": bad numeric cell '" + cell + "'");
+    io_error(PSTEREO_IO_DECODE_FAILURE, path + ": bad numeric cell '" + cell + "'");
   }
 }
 
 std::vector<pstereo_metrics_row> read_csv(const std::string& path) {
   std::ifstream in(path, std::ios::binary);
-  if (!in) io_error("cannot open " + path);
+  if (!in) io_error(PSTEREO_IO_MISSING_FILE, "cannot open " + path);
   std::string line;
   if (!std::getline(in, line) || trim(line) != kCsvHeader)
-    io_error(path + ": missing metrics header");
+    io_error(PSTEREO_IO_DECODE_FAILURE, path + ": missing metrics header");
   std::vector<pstereo_metrics_row> rows;
   while (std::getline(in, line)) {
     line = trim(line);
@@ -582,7 +587,7 @@ std::vector<pstereo_metrics_row> read_csv(const std::string& path) {
         start = i + 1;
       }
     if (cells.size() != 6)
-      io_error(path + ": expected 6 cells, got " + std::to_string(cells.size()));
+      io_error(PSTEREO_IO_DECODE_FAILURE, path + ": expected 6 cells, got " + std::to_string(cells.size()));
     pstereo_metrics_row m;
     std::memset(&m, 0, sizeof m);
     std::snprintf(m.frame, sizeof m.frame, "%s", cells[0].c_str());
@@ -591,7 +596,7 @@ std::vector<pstereo_metrics_row> read_csv(const std::string& path) {
     try {
       m.valid_px = parse_int("valid_px", cells[3]);
     } catch (const Error& e) {
-      io_error(path + ": " + e.what());
+      io_error(PSTEREO_IO_DECODE_FAILURE, path + ": " + e.what());
     }
     m.runtime_ms = parse_csv_double(cells[4], path);
     m.coverage_rate = parse_csv_double(cells[5], path);
@@ -604,6 +609,8 @@ std::vector<pstereo_metrics_row> read_csv(const std::string& path) {
 }  // namespace
 
 extern "C" {
+
+int pstereo_last_io_kind(void) { return t_io_kind; }
 
 void pstereo_scene_default(pstereo_scene_spec* s) {
   std::memset(s, 0, sizeof *s);
@@ -683,7 +690,7 @@ int pstereo_write_pfm(const char* path, int w, int h, const float* values, const
     const std::string p = path;
     if (w < 0 || h < 0 || (!values && w * h > 0)) throw Error(PSTEREO_EINTERNAL, "bad PFM plane");
     std::ofstream out(p, std::ios::binary);
-    if (!out) io_error("cannot write " + p);
+    if (!out) io_error(PSTEREO_IO_WRITE_FAILURE, "cannot write " + p);
     out << "Pf\n" << w << " " << h << "\n-1.0\n";
     if (!valid && rows_bottom_up) {
       out.write(reinterpret_cast<const char*>(values), std::streamsize(sizeof(float)) * w * h);
@@ -698,7 +705,7 @@ int pstereo_write_pfm(const char* path, int w, int h, const float* values, const
                   std::streamsize(row.size() * sizeof(float)));
       }
     }
-    if (!out) io_error("write failed: " + p);
+    if (!out) io_error(PSTEREO_IO_WRITE_FAILURE, "write failed: " + p);
   });
 }
 
@@ -708,15 +715,15 @@ int pstereo_read_pfm(const char* path, int* width, int* height, float* values, s
   return guarded(msg, msg_cap, [&] {
     const std::string p = path;
     std::ifstream in(p, std::ios::binary);
-    if (!in) io_error("cannot open " + p);
+    if (!in) io_error(PSTEREO_IO_MISSING_FILE, "cannot open " + p);
     std::string magic;
     in >> magic;
-    if (magic != "Pf") io_error(p + ": not a grayscale PFM");
+    if (magic != "Pf") io_error(PSTEREO_IO_DECODE_FAILURE, p + ": not a grayscale PFM");
     int w = 0, h = 0;
     double scale = 0.0;
     in >> w >> h >> scale;
-    if (!in || w <= 0 || h <= 0) io_error(p + ": malformed header");
-    if (!(scale < 0.0)) io_error(p + ": big-endian PFM unsupported");
+    if (!in || w <= 0 || h <= 0) io_error(PSTEREO_IO_DECODE_FAILURE, p + ": malformed header");
+    if (!(scale < 0.0)) io_error(PSTEREO_IO_DECODE_FAILURE, p + ": big-endian PFM unsupported");
     in.get();
     *width = w;
     *height = h;
@@ -724,7 +731,7 @@ int pstereo_read_pfm(const char* path, int* width, int* height, float* values, s
     if (cap < size_t(w) * h) throw Error(PSTEREO_EINTERNAL, "value buffer too small");
     for (int y = h - 1; y >= 0; --y) {
       in.read(reinterpret_cast<char*>(values + size_t(y) * w), std::streamsize(w) * 4);
-      if (!in) io_error(p + ": truncated pixel data");
+      if (!in) io_error(PSTEREO_IO_DECODE_FAILURE, p + ": truncated pixel data");
     }
   });
 }
@@ -743,10 +750,10 @@ int pstereo_write_metrics_csv(const char* path, const pstereo_metrics_row* rows,
   return guarded(msg, cap, [&] {
     const std::string p = path;
     std::ofstream out(p, std::ios::binary);
-    if (!out) io_error("cannot write " + p);
+    if (!out) io_error(PSTEREO_IO_WRITE_FAILURE, "cannot write " + p);
     out << kCsvHeader << "\n";
     for (int i = 0; i < n_rows; ++i) out << format_row(rows[i]) << "\n";
-    if (!out) io_error("write failed: " + p);
+    if (!out) io_error(PSTEREO_IO_WRITE_FAILURE, "write failed: " + p);
   });
 }
 
