@@ -74,7 +74,7 @@ __host__ __device__ inline BandLayout band_layout(int rows, int rpitch, int fpit
   l.oCnt = take(size_t(npb) * 4, 4);
   l.oPool = take(size_t(npb) * 4, 4);
   l.oWlist = take(size_t(npb) * 4, 4);
-  l.oCounters = take(24 * 4, 4);
+  l.oCounters = take(32 * 4, 4);
   l.oSlotU = take(size_t(nslots) * 8, 8);
   l.oSlotPrev = take(size_t(nslots) * 8, 8);
   l.oSlotLastd = take(size_t(nslots) * 8, 8);

@@ -353,7 +353,7 @@ __global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams p
   }
   if (pp.have_prev) griddep_wait();
   griddep_launch();  // our predecessors are complete: the next level may start staging
-  if (tid < 24) counters[tid] = 0;
+  if (tid < 32) counters[tid] = 0;
   __syncthreads();
 
   // ---- phase 1: extract_patch + precompute_patch_system + u0 (:250-262)
