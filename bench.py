@@ -573,6 +573,68 @@ def run_ours(args, wl):
         dist.destroy_process_group()
 
 
+def run_sweep_c4(args):
+    """BASELINE config 4 on one GPU: every resolution at s=8 stride 4 and
+    every (patch size, stride) in {8,12,16} x {2,4,6} at 640x480, RGB inputs
+    from the device generator; batch 1 (latency, ms per call) and batch 1024
+    (throughput, pairs/s), device-resident, CUDA events. Beside it, the
+    reference's run_pipeline on one host core for pair 0, whose outputs the
+    GPU's batch-1 call must match bit for bit. One JSON line per case."""
+    import torch
+
+    import paper_2205_03133_b200 as P
+
+    cases = [(w, h, 8, 4) for w, h in ((320, 240), (640, 480), (1280, 1024), (1920, 1080))]
+    cases += [(640, 480, s, st) for s in (8, 12, 16) for st in (2, 4, 6) if (s, st) != (8, 4)]
+    if args.sweep_cases:
+        cases = [cases[int(i)] for i in args.sweep_cases.split(",")]
+    big = args.batch or 1024
+    for w, h, s, st in cases:
+        wl = workload(f"c4:{w}x{h}:{s}:{st}:3:{big}")
+        cfg = P.PipelineConfig(**wl["params"])
+        row = {"workload": wl["desc"], "exps": f"{cfg.coarsest_exp}..{cfg.finest_exp}",
+               "unit": "pairs/s"}
+        for B in (1, big):
+            dl, dr = P.synth_batch_gpu(4, B, seed0=0, **wl["over"])
+            disp = torch.empty((B, h, w), dtype=torch.float32, device="cuda")
+            stream = torch.cuda.Stream()
+            with P.Matcher(cfg, w, h, B) as m:
+                def step():
+                    m.run_device_u8(B, w, h, 3, dl.data_ptr(), dr.data_ptr(),
+                                    {"disparity": disp.data_ptr()}, stream=stream.cuda_stream,
+                                    invalid_value=float("nan"))
+                for _ in range(max(args.warmup, 3)):
+                    step()
+                torch.cuda.synchronize()
+                reps = 20 if B == 1 else max(3, min(args.steps, 5))
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                for _ in range(reps):
+                    step()
+                e1.record(stream)
+                torch.cuda.synchronize()
+                ms = e0.elapsed_time(e1) / reps
+            if B == 1:
+                row["latency_ms_b1"] = ms
+                left, right = dl.cpu().numpy(), dr.cpu().numpy()
+                d1 = disp[0].cpu().numpy()
+            else:
+                row[f"pairs_s_b{B}"] = B / (ms / 1e3)
+            del dl, dr, disp
+            torch.cuda.empty_cache()
+        _, kind = _cpu_oracle()
+        _, times, outs = cpu_run(left, right, wl["params"], 1, keep=True)
+        ref = outs[0]
+        ok = (np.array_equal(~np.isnan(d1), ref["disparity_valid"] != 0) and
+              np.array_equal(d1[~np.isnan(d1)],
+                             ref["disparity"].astype(np.float32)[~np.isnan(d1)]))
+        row["cpu_baseline"] = {"ms_per_pair": times[0], "cores": 1, "kind": kind,
+                               "sample": "pair 0 (seed 0), run_pipeline threads=1"}
+        row["parity_pair0"] = bool(ok)
+        print(json.dumps(row), flush=True)
+
+
 def _free_port() -> int:
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
@@ -591,6 +653,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer leg (profiling)")
     ap.add_argument("--no-weak", action="store_true", help="skip the weak-scaling leg (N > 1)")
+    ap.add_argument("--sweep", choices=["c4"], help="BASELINE config-4 sweep, one JSON line "
+                    "per case (1 GPU; --batch overrides the throughput batch of 1024)")
+    ap.add_argument("--sweep-cases", default="", help="comma-separated case indices (sweep)")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         # launch the ranks ourselves: one process per GPU (torchrun semantics)
@@ -598,6 +663,9 @@ def main():
                f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
                "--master-port", str(_free_port()), str(Path(__file__).resolve()), *sys.argv[1:]]
         raise SystemExit(subprocess.call(cmd))
+    if args.sweep:
+        run_sweep_c4(args)
+        return
     wl = workload(args.workload)
     if args.batch:
         wl["batch"] = args.batch
