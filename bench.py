@@ -483,7 +483,7 @@ def run_ours(args, wl):
             # the pipes this kernel actually runs on: FP64 (DADD/DMUL/DFMA) and
             # XU (conversions); counts from ncu for the same launch scaled to
             # this batch, time from the live CUDA events; peaks are this box's
-            # measured per-SM rates (scripts/microbench.cu: DADD 62.6, F2F 15.5
+            # measured per-SM rates (scripts/tools/microbench.cu: DADD 62.6, F2F 15.5
             # thread-ops/clk/SM) x 148 SMs x max clock
             sm_hz = 148 * 1965e6
             scale = pairs_per_call / t["pairs_in_launch"] / (patch_ms / 1e3)
