@@ -85,7 +85,8 @@ struct Rows {
 template <int S, bool kSmem, bool kValid, bool kJr = true>
 __device__ __forceinline__ Ev eval_patch(const Rows<kSmem>& rw, int w, int s_rt, int x0,
                                          int r0, int rpad, double mean, double u) {
-  constexpr int SA = S > 0 ? S : kMaxPatch;
+  // S > 0: the patch size; S < 0: a runtime size of at most -S; S == 0: up to kMaxPatch
+  constexpr int SA = S > 0 ? S : (S < 0 ? -S : kMaxPatch);
   const int s = S > 0 ? S : s_rt;
   const double wm1 = (double)(w - 1);
   const double xd0 = (double)x0;
@@ -95,7 +96,7 @@ __device__ __forceinline__ Ev eval_patch(const Rows<kSmem>& rw, int w, int s_rt,
   unsigned inb = 0, contig = 0;
 #pragma unroll
   for (int i = 0; i < SA; ++i) {
-    if (S == 0 && i >= s) break;
+    if (S <= 0 && i >= s) break;
     const double X = __dsub_rn(__dadd_rn(xd0, (double)i), u);  // (cx + offset(i)) - u
     const bool in = X >= 0.0 && X <= wm1;
     const int xi = in ? __double2int_rz(X) : 0;
@@ -198,7 +199,7 @@ __device__ __forceinline__ Ev eval_patch(const Rows<kSmem>& rw, int w, int s_rt,
     double b = 0.0;
 #pragma unroll
     for (int i = 0; i < SA; ++i) {
-      if (S == 0 && i >= s) break;
+      if (S <= 0 && i >= s) break;
       const double a = (double)rr[rw.s8(xo + cxi[i])];
       b = (double)rr[rw.s8(xo + cxi[i] + 1)];
       const double v = __dadd_rn(__dmul_rn(comf[i], a), __dmul_rn(cfx[i], b));
@@ -224,7 +225,7 @@ __device__ __forceinline__ Ev eval_patch(const Rows<kSmem>& rw, int w, int s_rt,
     double b = 0.0;
 #pragma unroll
     for (int i = 0; i < SA; ++i) {
-      if (S == 0 && i >= s) break;
+      if (S <= 0 && i >= s) break;
       const double a = (double)rr[rw.s8(xo + cxi[i])];
       b = (double)rr[rw.s8(xo + cxi[i] + 1)];
       bool use = (inb >> i) & 1u;
@@ -248,7 +249,7 @@ __device__ __forceinline__ Ev eval_patch(const Rows<kSmem>& rw, int w, int s_rt,
 
 
 template <int S, bool kSmem, bool kValid>
-__global__ void __launch_bounds__(256) k_patches(Level L, Level P, PatchParams pp, BandPlan bp) {
+__global__ void __launch_bounds__(256, S == -16 ? 2 : 0) k_patches(Level L, Level P, PatchParams pp, BandPlan bp) {
   extern __shared__ __align__(16) unsigned char smem[];
   const Grid& g = L.g;
   const int s = S > 0 ? S : g.size;
@@ -768,7 +769,12 @@ static cudaError_t launch_s(const Level& L, const Level& P, const PatchParams& p
     case 10: return launch_t<10, kSmem, kValid>(L, P, pp, bp, s);
     case 12: return launch_t<12, kSmem, kValid>(L, P, pp, bp, s);
     case 16: return launch_t<16, kSmem, kValid>(L, P, pp, bp, s);
-    default: return launch_t<0, kSmem, kValid>(L, P, pp, bp, s);
+    // other sizes: runtime-size instantiations whose column tables hold at
+    // most 8 / 16 entries (registers, not local memory), else 32
+    default:
+      if (L.g.size < 8) return launch_t<-8, kSmem, kValid>(L, P, pp, bp, s);
+      if (L.g.size < 16) return launch_t<-16, kSmem, kValid>(L, P, pp, bp, s);
+      return launch_t<0, kSmem, kValid>(L, P, pp, bp, s);
   }
 }
 
