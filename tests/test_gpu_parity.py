@@ -397,3 +397,25 @@ def test_randomized_configs(gpu, checker, seed):
     P = gpu
     cfg, l, r = random_case(P, seed)
     _check(P, checker, cfg, l[None], r[None])
+
+
+def test_ccl_sure_chains(gpu, checker):
+    """Components that cross 32x64 finest tiles as sure / not-sure / sure
+    pieces (k_ccl_border skips unions between two sure pieces): the
+    inputs hold such chains (tests/test_ccl_chains.py pins that on CPU) and
+    every output, the validity masks first, equals the reference's."""
+    from oracle import pyoracle
+    from tests.ccl_chains import CASES, chain_count
+
+    chains = 0
+    for thr, gamma, seed in CASES:
+        cfg = gpu.PipelineConfig(coarsest_exp=3, finest_exp=1, patch_size=8, overlap=0.5,
+                                 pixel_threshold=thr, gamma=gamma)
+        left, right = pyoracle.synth_batch(1, 1, seed0=seed)
+        out = run_gpu_batch(gpu, cfg, left, right, 500.0, 5.0)
+        lf, lv = checker.to_grayscale(left[0])
+        rf, rv = checker.to_grayscale(right[0])
+        pipe, match = run_oracle(checker, lf, rf, cfg, 500.0, 5.0, lv, rv)
+        compare_pair(out, 0, pipe, match, cfg)
+        chains += chain_count(match["probability"], match["disparity_valid"], thr, gamma, 8)
+    assert chains >= 4
