@@ -95,9 +95,11 @@ inline LevelDims level_dims(const pstereo_params& p, int width, int height) {
   return d;
 }
 
-// patches on one axis of a level (src/coarse_to_fine.cpp:51-88), an upper bound
+// patches on one axis of a level, an upper bound: make_patch_grid
+// (src/coarse_to_fine.cpp:51-88) places ceil((L - s) / stride) + 1 centres,
+// stride = max(1, lrint(s * (1 - overlap))) (ties to even)
 inline std::size_t grid_cap(int extent, const pstereo_params& p) {
-  long st = std::lround(p.patch_size * (1.0 - p.overlap));
+  long st = std::lrint(p.patch_size * (1.0 - p.overlap));
   if (st < 1) st = 1;
   return extent < p.patch_size ? 1 : std::size_t((extent - p.patch_size) / st + 2);
 }
@@ -189,6 +191,7 @@ inline MatchResult match_stereo(const GrayImage& left, const GrayImage& right,
         f.var_disp.valid[dst] = ok;
       }
     }
+  if (n_recs > int(cap)) throw gpu::GpuError("match_stereo: finest-level records truncated");
   f.patches.reserve(std::size_t(n_recs));
   for (int k = 0; k < n_recs; ++k) {
     const pstereo_patch_estimate& r = recs[std::size_t(k)];

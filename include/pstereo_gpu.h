@@ -408,7 +408,8 @@ int pstereo_gpu_to_grayscale(int device, int width, int height, int channels,
  * no collective, no peer traffic), writing the block's slice of every output
  * plane, stats and finest records. The call returns when every block is
  * done; results are identical to one context running all pairs. max_pairs is
- * the largest n_pairs a call may pass. */
+ * the largest n_pairs a call may pass. Like a context, a pstereo_multi is not
+ * re-entrant: one call at a time. */
 typedef struct pstereo_multi pstereo_multi;
 int pstereo_multi_create(const int* devices, int n_devices, const pstereo_params* p,
                          int max_width, int max_height, int max_pairs,

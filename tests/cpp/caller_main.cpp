@@ -10,7 +10,7 @@
 // tests/test_gpu_dropin.py runs both on the same inputs and compares the dumps
 // and the files run_match / run_bench write.
 //
-// Usage: caller WORKDIR LEFT.pgm RIGHT.pgm CALIB CONFIG(0..3)
+// Usage: caller WORKDIR LEFT.pgm RIGHT.pgm CALIB CONFIG(0..4)
 // Writes WORKDIR/dump.bin (records: name, kind, count, payload) plus the
 // run_match outputs under WORKDIR/match and WORKDIR/bench.csv.
 #include <cmath>
@@ -81,8 +81,10 @@ void rec_stats(const std::string& name, const MatchStats& s) {
 }
 
 PipelineConfig config_for(int c) {
-  // BASELINE.json configs -> PipelineConfig
+  // BASELINE.json configs -> PipelineConfig; 4 = the
+  // reference's own defaults (inc/config.hpp: 5..1, s = 10, overlap 0.55)
   PipelineConfig cfg;
+  if (c == 4) return cfg;
   cfg.coarsest_exp = c == 3 ? 4 : 3;
   cfg.finest_exp = 1;
   cfg.patch_size = c == 3 ? 12 : 8;
@@ -218,9 +220,12 @@ int main(int argc, char** argv) {
   scenes[2].disparity_gradient = 0.01;
   scenes[2].texture = TextureKind::checker;
   scenes[2].noise_std = 0.01;
+  // the reference's default 5-level pyramid needs >= 320 px at the coarsest
+  // level times 2^5 / patch: full-size scenes for config 4
+  const int sw = config == 4 ? 640 : 320, sh = config == 4 ? 480 : 240;
   for (auto& s : scenes) {
-    s.width = 320;
-    s.height = 240;
+    s.width = sw;
+    s.height = sh;
   }
   const BenchResult br = run_benchmark(scenes, cfg, 2);
   for (const FrameMetrics& m : br.frames) {
@@ -235,9 +240,9 @@ int main(int argc, char** argv) {
   rec_i("bench.avg_valid_px", br.aggregate.valid_px);
 
   // 4. the CLI's bench body (src/runner.cpp:164-183) on scene files
-  write_scene(dir + "/s1.txt", "name = s1\nsurface = plane\ndisparity = 5\nwidth = 256\nheight = 192\n");
-  write_scene(dir + "/s2.txt",
-              "name = s2\nsurface = sphere\nshading = nonlambertian\nwidth = 256\nheight = 192\n");
+  const std::string dims = config == 4 ? "width = 640\nheight = 480\n" : "width = 256\nheight = 192\n";
+  write_scene(dir + "/s1.txt", "name = s1\nsurface = plane\ndisparity = 5\n" + dims);
+  write_scene(dir + "/s2.txt", "name = s2\nsurface = sphere\nshading = nonlambertian\n" + dims);
   BenchArgs ba;
   ba.scene_paths = {dir + "/s1.txt", dir + "/s2.txt"};
   ba.out_csv = dir + "/bench.csv";

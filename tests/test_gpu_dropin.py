@@ -74,11 +74,14 @@ def _pfm(path):
     return np.frombuffer(head[3], "<f4").reshape(h, w)
 
 
-CASES = [  # (config, seed, width, height, channels)
+CASES = [  # (config, seed, width, height, channels); config 5 = generator 0
+    # with the reference's default PipelineConfig (5 levels, s = 10, overlap
+    # 0.55 -> stride lrint(4.5) = 4)
     (0, 0, 640, 480, 1),
     (1, 1, 640, 480, 1),
     (3, 0, 640, 512, 1),
     (0, 7, 320, 240, 3),
+    (5, 2, 640, 480, 1),
 ]
 
 
@@ -92,7 +95,8 @@ def test_reference_callers_against_dropin(gpu, tmp_path, config, seed, w, h, ch)
     over = dict(width=w, height=h)
     if ch != 1:
         over["channels"] = ch
-    left, right = pyoracle.synth_batch(config if ch == 1 else 4, 1, seed0=seed, **over)
+    gen = 4 if ch != 1 else (0 if config == 5 else config)
+    left, right = pyoracle.synth_batch(gen, 1, seed0=seed, **over)
     lp, rp, cp = tmp_path / "l.pnm", tmp_path / "r.pnm", tmp_path / "calib.txt"
     _write_pnm(lp, left[0])
     _write_pnm(rp, right[0])
@@ -101,7 +105,8 @@ def test_reference_callers_against_dropin(gpu, tmp_path, config, seed, w, h, ch)
     for tag, exe in (("ref", REF_EXE), ("gpu", GPU_EXE)):
         wd = tmp_path / tag
         r = subprocess.run([str(exe), str(wd), str(lp), str(rp), str(cp),
-                            str(min(config, 3))], capture_output=True, text=True, timeout=900)
+                            str(4 if config == 5 else min(config, 3))], capture_output=True,
+                           text=True, timeout=900)
         assert r.returncode == 0, f"{tag}: {r.stdout}{r.stderr}"
         runs[tag] = wd
     a = read_dump(runs["ref"] / "dump.bin")
