@@ -208,6 +208,24 @@ int main(int argc, char** argv) {
     rec("finest.has_sigma", 3, flags.data(), flags.size(), 8);
   }
 
+  // 2b. masked inputs (GrayImage validity, inc/image.hpp:21-26): an invalid
+  // block in each view, as an RGBA alpha of 0 would give
+  {
+    GrayImage ml = left, mr = right;
+    for (int y = left.height / 3; y < left.height / 2; ++y)
+      for (int x = left.width / 4; x < left.width / 3; ++x) {
+        ml.valid[std::size_t(y) * ml.width + x] = 0;
+        mr.valid[std::size_t(y) * mr.width + x + 7] = 0;
+      }
+    const PipelineOutput mo = run_pipeline(ml, mr, cfg, cam);
+    rec_field("masked.disparity", mo.disparity);
+    rec_field("masked.depth", mo.depth.depth);
+    rec_stats("masked.stats", mo.stats);
+    const MatchResult mm = match_stereo(ml, mr, cfg);
+    rec_field("masked.match", mm.disparity);
+    rec_i("masked.finest_patches", std::int64_t(mm.finest.patches.size()));
+  }
+
   // 3. run_benchmark (src/bench.cpp) over rendered scenes (src/synth.cpp)
   std::vector<SceneSpec> scenes(3);
   scenes[0].name = "plane";
