@@ -310,6 +310,30 @@ def parity_report(ref_outs, gpu, k0):
             "against": "oracle/_ref run_pipeline (the unmodified reference)"}
 
 
+def bind_to_gpu_numa_node(device: int):
+    """Pins this rank's host threads to the CPUs of its GPU's NUMA node (from
+    the PCI device's local_cpulist), so the pinned staging buffers of the e2e
+    leg are first-touched, and copied from, memory next to the GPU's PCIe
+    root. Best effort: returns the CPU list used, or None."""
+    import torch
+
+    try:
+        pr = torch.cuda.get_device_properties(device)
+        bdf = f"{pr.pci_domain_id:04x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+        text = Path(f"/sys/bus/pci/devices/{bdf}/local_cpulist").read_text().strip()
+        cpus = set()
+        for part in text.split(","):
+            lo, _, hi = part.partition("-")
+            cpus.update(range(int(lo), int(hi or lo) + 1))
+        cpus &= os.sched_getaffinity(0)
+        if cpus and len(cpus) < os.cpu_count():
+            os.sched_setaffinity(0, cpus)
+            return text
+    except Exception:
+        pass
+    return None
+
+
 def run_ours(args, wl):
     import torch
     import torch.distributed as dist
@@ -327,6 +351,9 @@ def run_ours(args, wl):
     backend = os.environ.get("PSTEREO_BENCH_BACKEND", "gloo" if folded else "nccl")
     local %= max(ndev, 1)
     torch.cuda.set_device(local)
+    # N > 1: each rank's host threads on its GPU's NUMA node (N = 1 keeps every
+    # core: its cpu_baseline leg runs the reference on all of them)
+    numa = bind_to_gpu_numa_node(local) if world > 1 else None
     if world > 1:
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -567,6 +594,7 @@ def run_ours(args, wl):
                              "host generator)",
                    "output": "fp32 filtered disparity, NaN = invalid (mask folded in)",
                    "inflight": inflight,
+                   "host_cpus": numa or "unpinned",
                    "l2": (f"inputs {step_in / 1e6:.0f} MB/step per GPU "
                           + ("> 126 MB L2 (no flush needed)" if n_sets == 1 else
                              f"< 126 MB L2: steps cycle over {n_sets} input sets "
