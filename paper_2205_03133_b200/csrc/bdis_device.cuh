@@ -231,6 +231,23 @@ __device__ inline double variance_fit5(const double* delta, const double* p, dou
 // ~1e-15 relative, which is why var_disp is held to 1e-3 rel, not bits.
 __device__ inline double variance_fit(const double* woff, int nwin, int wcenter, const double* res,
                                const uint8_t* ok, double denom) {
+  // The common case first -- the default five-point window {-a, -b, 0, b, a}
+  // with every sample valid -- with the priors in registers (the general
+  // path below compacts the valid samples through a dynamically indexed
+  // array, i.e. local memory). Same operations in the same order.
+  if (nwin == 5 && wcenter == 2 && ok[0] && ok[1] && ok[2] && ok[3] && ok[4] &&
+      woff[2] == 0.0 && woff[0] == -woff[4] && woff[1] == -woff[3]) {
+    double d5[5], p5[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      d5[k] = woff[k];
+      p5[k] = fast_exp(__ddiv_rn(-res[k], denom));
+    }
+#pragma unroll
+    for (int k = 0; k < 5; ++k)
+      if (k != 2 && !(p5[2] > p5[k])) return 2.0;  // kSigmaFallback
+    return variance_fit5(d5, p5, 2.0);
+  }
   double delta[kMaxWin], p[kMaxWin];
   double center_prior = 0.0;
   int n = 0;
