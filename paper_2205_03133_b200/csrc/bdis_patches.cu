@@ -720,7 +720,12 @@ BandPlan plan_bands(const Level& L, const PatchParams& pp, int max_smem_per_cta)
       !getenv("PSTEREO_TUNE_CTAS")) {
     const bool starving =
         (rb <= 2 && (g.size >= 12 || g.nx >= 100)) || (rb <= 3 && g.size >= 16);
-    const bool dense = 4 * g.stride <= g.size && g.nx >= 60;
+    // (s = 12 excepted below 300 patch columns: its instantiation runs the
+    // mean pass two rows at a time at 160 registers and measured faster on
+    // two 192-thread CTAs there -- 640x480 stride 2 / 3: 7.02 vs 7.18 ms and
+    // 3.38 vs 3.54 ms per 128 pairs -- while 1920x1080 stride 2 keeps the
+    // one-CTA shape, profiles/r02/k_patches_experiments.md)
+    const bool dense = 4 * g.stride <= g.size && g.nx >= 60 && !(g.size == 12 && g.nx < 300);
     if (starving || dense) {
       const int r1 = fit(256, 1);
       if (r1 >= rb + 1) {
