@@ -671,12 +671,17 @@ BandPlan plan_bands(const Level& L, const PatchParams& pp, int max_smem_per_cta)
   bp.fpitch = pad4_host(L.w - 1) + 1;            // x in [0, w - 1]
   bp.bpitch = valid ? L.w : 0;
   // measured per level width (patch columns): 192-slot CTAs, two per SM, for
-  // wide levels; 128-slot CTAs, three per SM, for medium ones; 256-slot CTAs
-  // for the narrowest (whole-level bands, one CTA carries all of a pair)
+  // wide levels; 128-slot CTAs, three per SM, for medium ones; 128-slot CTAs,
+  // four per SM, with about 0.8 patches per slot for the narrowest (round 2:
+  // three bands per pair at the coarsest config-2 level instead of one
+  // whole-level CTA, -1% per step; profiles/r02/k_patches_experiments.md)
   const bool medium = g.nx >= 30 && g.nx < 60;
-  int threads = env("PSTEREO_TUNE_THREADS", g.nx < 30 ? 256 : medium ? 128 : 192);
-  int ctas = env("PSTEREO_TUNE_CTAS", medium ? 3 : 2);
-  int ppl10 = env("PSTEREO_TUNE_PPL10", 20);
+  // (not at s = 16: +5%; not for launches of more than 256 pairs, whose
+  // whole-level CTAs already fill several waves: 320x240 x 1024 +1.5%)
+  const bool narrow = g.nx < 30 && g.size <= 12 && pp.n_pairs <= 256;
+  int threads = env("PSTEREO_TUNE_THREADS", narrow || medium ? 128 : g.nx < 30 ? 256 : 192);
+  int ctas = env("PSTEREO_TUNE_CTAS", narrow ? 4 : medium ? 3 : 2);
+  int ppl10 = env("PSTEREO_TUNE_PPL10", narrow ? 8 : 20);
   // tuning runs only: PSTEREO_TUNE_SPEC="e1=192x2,e2=128x3" per level exponent
   if (const char* spec = getenv("PSTEREO_TUNE_SPEC")) {
     char key[16];
