@@ -741,7 +741,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer leg (profiling)")
     ap.add_argument("--no-weak", action="store_true", help="skip the weak-scaling leg (N > 1)")
-    ap.add_argument("--inflight", type=int, default=3,
+    ap.add_argument("--inflight", type=int, default=4,
                     help="batches in flight in the timed leg (one context and stream each)")
     ap.add_argument("--sweep", choices=["c4"], help="BASELINE config-4 sweep, one JSON line "
                     "per case (1 GPU; --batch overrides the throughput batch of 1024)")
