@@ -450,7 +450,10 @@ def run_ours(args, wl):
             dist.barrier()
         return max_over_ranks(e0.elapsed_time(e1), device=None if backend != "nccl" else dev)
 
-    for _ in range(args.warmup):
+    # every in-flight context runs at least one untimed step (its first call
+    # allocates its working set)
+    warm = max(args.warmup, inflight)
+    for _ in range(warm):
         step_inflight()
     torch.cuda.synchronize(dev)
     launches_per_step = m.launch_count()
@@ -594,6 +597,7 @@ def run_ours(args, wl):
                              "host generator)",
                    "output": "fp32 filtered disparity, NaN = invalid (mask folded in)",
                    "inflight": inflight,
+                   "warmup_steps_run": warm,
                    "host_cpus": numa or "unpinned",
                    "l2": (f"inputs {step_in / 1e6:.0f} MB/step per GPU "
                           + ("> 126 MB L2 (no flush needed)" if n_sets == 1 else
