@@ -397,6 +397,9 @@ def run_ours(args, wl):
                                            device=local, **wl["over"])
                          for k in range(1, n_sets)]
     ctxs = [m] + [P.Matcher(cfg, W, H, max(B, 1), device=local) for _ in range(1, inflight)]
+    if inflight > 1:  # the in-flight batches fill the GPU: no extra band split
+        for c in ctxs:
+            c.set_fill_target(0)
     outs_k = [disp] + [torch.empty_like(disp) for _ in range(1, inflight)]
     streams = [stream] + [torch.cuda.Stream(dev) for _ in range(1, inflight)]
     kstep = [0]
@@ -464,6 +467,7 @@ def run_ours(args, wl):
     clk = clocks.stop()
     for c in ctxs[1:]:
         c.close()
+    m.set_fill_target(148)
     del ctxs, outs_k
     step()  # `disp` = this rank's batch (input set 0) for the checks below
     torch.cuda.synchronize(dev)

@@ -149,6 +149,7 @@ def lib() -> C.CDLL:
         L.pstereo_gpu_create.argtypes = [C.c_int, C.POINTER(_Params), C.c_int, C.c_int, C.c_int,
                                          C.POINTER(C.c_void_p)]
         L.pstereo_gpu_destroy.argtypes = [C.c_void_p]
+        L.pstereo_gpu_set_fill_target.argtypes = [C.c_void_p, C.c_int]
         L.pstereo_multi_create.argtypes = [C.POINTER(C.c_int), C.c_int, C.POINTER(_Params),
                                            C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]
         L.pstereo_multi_destroy.argtypes = [C.c_void_p]
@@ -589,6 +590,14 @@ class Matcher:
 
     def launch_count(self) -> int:
         return lib().pstereo_gpu_last_launch_count(self._h)
+
+    def set_fill_target(self, ctas: int):
+        """pstereo_gpu_set_fill_target: spread small launches over >= ctas CTAs
+        (148 = one per SM, best single-call latency; 0 = off, best with
+        several calls in flight)."""
+        rc = lib().pstereo_gpu_set_fill_target(self._h, int(ctas))
+        if rc:
+            _raise(rc, self.last_error())
 
     def set_device_chunks(self, chunks: int):
         """Sub-batches per device call (pstereo_gpu_set_device_chunks)."""

@@ -235,6 +235,7 @@ struct pstereo_ctx {
   // host-buffer pipeline (chunked H2D / compute / D2H)
   int chunk_pairs = 0;
   int device_chunks = 2;  // sub-batches of a device call (PSTEREO_DEVICE_CHUNKS)
+  int fill_sms = 148;     // small launches spread over >= this many CTAs (0: off)
   cudaStream_t s_in = nullptr, s_out = nullptr, s_comp = nullptr;
   // compute_metrics staging
   DevBuf<double> met_f64;
@@ -523,6 +524,12 @@ int pstereo_gpu_metrics(pstereo_ctx* ctx, int n, int w, int h, const double* est
   return PSTEREO_OK;
 }
 
+int pstereo_gpu_set_fill_target(pstereo_ctx* ctx, int ctas) {
+  if (!ctx || ctas < 0) return PSTEREO_EINTERNAL;
+  ctx->fill_sms = ctas;
+  return PSTEREO_OK;
+}
+
 int pstereo_gpu_set_device_chunks(pstereo_ctx* ctx, int chunks) {
   if (!ctx || chunks < 0) return PSTEREO_EINTERNAL;
   ctx->device_chunks = chunks;
@@ -783,6 +790,7 @@ int run_device(pstereo_ctx* ctx, Scratch& sc, const std::vector<LevelGeom>& geo,
   for (int q = 0; q < ctx->nwin; ++q) pp.woff[q] = ctx->woff[q];
   pp.prev_mask = ctx->mask.p;
   pp.all_valid = all_valid;
+  pp.fill_sms = ctx->fill_sms;
   for (size_t li = 0; li < lv.size(); ++li) {
     pp.want_var = prm.estimate_variance && lv[li].e == fe;
     pp.have_prev = li > 0;

@@ -23,6 +23,7 @@ struct PatchParams {
   int have_prev;
   const double* prev_mask;  // spatial mask (s*s doubles, device)
   int all_valid;            // every input pixel valid: skip the 4-tap tests
+  int fill_sms;             // host planning: spread small launches over >= this many CTAs
 };
 
 // Row-band decomposition of one level for k_patches (host-planned).

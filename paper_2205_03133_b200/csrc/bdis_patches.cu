@@ -742,7 +742,7 @@ BandPlan plan_bands(const Level& L, const PatchParams& pp, int max_smem_per_cta)
   }
   // small batches: a CTA's rounds are a latency chain, so spread the level
   // over more, smaller bands until every SM has a CTA (single-frame latency)
-  const int sms = env("PSTEREO_SMS", 148);
+  const int sms = env("PSTEREO_SMS", pp.fill_sms);
   while (rb > 1 && (long long)((g.ny + rb - 1) / rb) * pp.n_pairs < sms) --rb;
   bp.use_smem = bytes_for(rb) <= size_t(max_smem_per_cta);
   bp.rb = rb;
