@@ -419,3 +419,24 @@ def test_ccl_sure_chains(gpu, checker):
         compare_pair(out, 0, pipe, match, cfg)
         chains += chain_count(match["probability"], match["disparity_valid"], thr, gamma, 8)
     assert chains >= 4
+
+
+@pytest.mark.parametrize("w,h,size,overlap,levels", [
+    (2048, 256, 32, 0.75, 2),   # s = 32 (the cap): one patch row of the level needs 413 KB of
+                                # shared memory -> the global-memory instantiation
+    (1536, 192, 24, 0.5, 2),    # runtime size 24 (the 32-entry instantiation), global path
+    (640, 480, 32, 0.75, 2),    # s = 32 at the bench size
+])
+def test_max_patch_and_global_memory_path(gpu, checker, w, h, size, overlap, levels):
+    """Patch sizes at the cap (32) and runtime sizes whose level bands do not
+    fit in shared memory: the k_patches global-memory instantiation, bit for
+    bit against the reference (a gray pair and an RGBA pair with holes)."""
+    P = gpu
+    cfg = P.PipelineConfig(coarsest_exp=levels, finest_exp=1, patch_size=size, overlap=overlap)
+    l, r = P.synth_batch(4, 1, seed0=5, width=w, height=h, channels=1)
+    _check(P, checker, cfg, l, r)
+    l3, r3 = P.synth_batch(4, 1, seed0=6, width=w, height=h, channels=3)
+    alpha = np.full((1, h, w, 1), 255, np.uint8)
+    l4, r4 = np.concatenate([l3, alpha], 3), np.concatenate([r3, alpha], 3)
+    l4[0, h // 3:h // 2, w // 5:w // 4, 3] = 0  # an invalid block (alpha 0)
+    _check(P, checker, cfg, l4, r4)
