@@ -672,8 +672,9 @@ def run_ours(args, wl):
 def run_sweep_c4(args):
     """BASELINE config 4 on one GPU: every resolution at s=8 stride 4 and
     every (patch size, stride) in {8,12,16} x {2,4,6} at 640x480, RGB inputs
-    from the device generator; batch 1 (latency, ms per call) and batch 1024
-    (throughput, pairs/s), device-resident, CUDA events. Beside it, the
+    from the device generator; batch 1 (latency: one call at a time, host
+    wall clock to a completed output, median of 20) and batch 1024
+    (throughput, pairs/s, CUDA events), device-resident. Beside it, the
     reference's run_pipeline on one host core for pair 0, whose outputs the
     GPU's batch-1 call must match bit for bit. One JSON line per case."""
     import torch
@@ -702,15 +703,26 @@ def run_sweep_c4(args):
                 for _ in range(max(args.warmup, 3)):
                     step()
                 torch.cuda.synchronize()
-                reps = 20 if B == 1 else max(3, min(args.steps, 5))
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-                for _ in range(reps):
-                    step()
-                e1.record(stream)
-                torch.cuda.synchronize()
-                ms = e0.elapsed_time(e1) / reps
+                if B == 1:
+                    # latency: one call at a time, host wall clock from the call
+                    # until its output is complete (median of 20)
+                    lat = []
+                    for _ in range(20):
+                        t0 = time.perf_counter()
+                        step()
+                        stream.synchronize()
+                        lat.append((time.perf_counter() - t0) * 1e3)
+                    ms = float(np.median(lat))
+                else:
+                    reps = max(3, min(args.steps, 5))
+                    e0.record(stream)
+                    for _ in range(reps):
+                        step()
+                    e1.record(stream)
+                    torch.cuda.synchronize()
+                    ms = e0.elapsed_time(e1) / reps
             if B == 1:
                 row["latency_ms_b1"] = ms
                 left, right = dl.cpu().numpy(), dr.cpu().numpy()
