@@ -144,11 +144,12 @@ __device__ __forceinline__ Ev eval_patch(const Rows<kSmem>& rw, int w, int s_rt,
     const int xb = base + rpad;  // smem column of tap `base`
     double sum = 0.0;
     const auto* rr = rw.R + r0 * rw.rp;
-    // s = 12: rows two at a time, the next row's taps loading under this
-    // row's chain -- 26-32% faster at s = 12 / stride 4 (configs 3 and 4); the
-    // other sizes measured neutral or slower with it, and so did the residual
-    // pass (profiles/r02/k_patches_experiments.md)
-#pragma unroll(S == 12 ? 2 : 1)
+    // s = 12 and 8: rows two at a time, the next row's taps loading under this
+    // row's chain -- 26-32% faster at s = 12 / stride 4 (configs 3 and 4);
+    // at s = 8 -0.5% on config 2 and -1.3% single-pair latency (+1% on the
+    // variance config 1); s = 10 / 16 measured slower with it, and so did the
+    // residual pass (profiles/r02/k_patches_experiments.md)
+#pragma unroll((S == 12 || S == 8) ? 2 : 1)
     for (int j = 0; j < SA; ++j, rr += rw.rp) {
       double a = (double)rr[rw.s8(xb)];
 #pragma unroll
