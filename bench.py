@@ -674,7 +674,10 @@ def run_sweep_c4(args):
     every (patch size, stride) in {8,12,16} x {2,4,6} at 640x480, RGB inputs
     from the device generator; batch 1 (latency: one call at a time, host
     wall clock to a completed output, median of 20) and batch 1024
-    (throughput, pairs/s, CUDA events), device-resident. Beside it, the
+    (throughput, pairs/s, CUDA events), device-resident. The latency calls
+    replay a CUDA graph of the call (pstereo_gpu_set_graphs, --graphs 0 for
+    eager calls): the per-call host work and launch gaps a repeated caller
+    avoids. Beside it, the
     reference's run_pipeline on one host core for pair 0, whose outputs the
     GPU's batch-1 call must match bit for bit. One JSON line per case."""
     import torch
@@ -690,12 +693,16 @@ def run_sweep_c4(args):
         wl = workload(f"c4:{w}x{h}:{s}:{st}:3:{big}")
         cfg = P.PipelineConfig(**wl["params"])
         row = {"workload": wl["desc"], "exps": f"{cfg.coarsest_exp}..{cfg.finest_exp}",
-               "unit": "pairs/s"}
+               "unit": "pairs/s",
+               "latency_mode": "CUDA graph replay" if args.graphs else "eager calls"}
         for B in (1, big):
             dl, dr = P.synth_batch_gpu(4, B, seed0=0, **wl["over"])
             disp = torch.empty((B, h, w), dtype=torch.float32, device="cuda")
             stream = torch.cuda.Stream()
             with P.Matcher(cfg, w, h, B) as m:
+                if B == 1 and args.graphs:
+                    m.set_graphs(True)  # latency as a repeated-call user sees it
+
                 def step():
                     m.run_device_u8(B, w, h, 3, dl.data_ptr(), dr.data_ptr(),
                                     {"disparity": disp.data_ptr()}, stream=stream.cuda_stream,
@@ -761,6 +768,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer leg (profiling)")
     ap.add_argument("--no-weak", action="store_true", help="skip the weak-scaling leg (N > 1)")
+    ap.add_argument("--graphs", type=int, default=1,
+                    help="--sweep: measure batch-1 latency with CUDA-graph replay "
+                         "(pstereo_gpu_set_graphs; 1) or eager calls (0)")
     ap.add_argument("--inflight", type=int, default=4,
                     help="batches in flight in the timed leg (one context and stream each)")
     ap.add_argument("--sweep", choices=["c4"], help="BASELINE config-4 sweep, one JSON line "

@@ -150,6 +150,7 @@ def lib() -> C.CDLL:
                                          C.POINTER(C.c_void_p)]
         L.pstereo_gpu_destroy.argtypes = [C.c_void_p]
         L.pstereo_gpu_set_fill_target.argtypes = [C.c_void_p, C.c_int]
+        L.pstereo_gpu_set_graphs.argtypes = [C.c_void_p, C.c_int]
         L.pstereo_multi_create.argtypes = [C.POINTER(C.c_int), C.c_int, C.POINTER(_Params),
                                            C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]
         L.pstereo_multi_destroy.argtypes = [C.c_void_p]
@@ -590,6 +591,12 @@ class Matcher:
 
     def launch_count(self) -> int:
         return lib().pstereo_gpu_last_launch_count(self._h)
+
+    def set_graphs(self, on: bool):
+        """pstereo_gpu_set_graphs: replay repeated device-buffer calls as CUDA graphs."""
+        rc = lib().pstereo_gpu_set_graphs(self._h, int(bool(on)))
+        if rc:
+            _raise(rc, self.last_error())
 
     def set_fill_target(self, ctas: int):
         """pstereo_gpu_set_fill_target: spread small launches over >= ctas CTAs
