@@ -557,6 +557,7 @@ def run_ours(args, wl):
     hbm, peak_kind = peaks()
     dims = P.level_dims(cfg, W, H)
     e_f, w_f, h_f = dims[-1]
+    host_expand = os.environ.get("PSTEREO_HOST_EXPAND", "1") != "0" and e_f >= 1
     s_ = cfg.patch_size
     st_ = max(1, int(round(cfg.patch_size * (1 - cfg.overlap))))
     npatch_f = len(_axis(w_f, s_, st_)) * len(_axis(h_f, s_, st_))
@@ -611,8 +612,17 @@ def run_ours(args, wl):
         "full_outputs": {"value": B / (full_ms / 1e3), "unit": "pairs/s", "ms_per_step": full_ms,
                          "planes": "disparity f32 + mask, probability f32, depth f32 + mask"},
         "e2e": {"value": e2e_value, "unit": "pairs/s", "h2d_bytes_per_step": 2 * B * W * H * CH,
-                "d2h_bytes_per_step": B * W * H * 4, "steps": e2e_steps,
-                "output": "fp32 filtered disparity, NaN at invalid pixels"},
+                # the link carries the plane at the finest level's resolution; host
+                # threads replicate it 2^e x 2^e into the caller's full-size buffer
+                "d2h_bytes_per_step": B * w_f * h_f * 4 if host_expand else B * W * H * 4,
+                "host_output_bytes_per_step": B * W * H * 4,
+                "host_expand": (f"on: finest-resolution download ({w_f}x{h_f}), "
+                                f"{P.lib().pstereo_gpu_host_threads()} host threads write the "
+                                f"{W}x{H} plane (upsample_to_full's replication)"
+                                if host_expand else "off: full-resolution download"),
+                "steps": e2e_steps,
+                "output": "fp32 filtered disparity, NaN at invalid pixels, full resolution "
+                          "in pinned host memory"},
         "roofline": {"bound": "hbm", "kernel": f"k_patches, finest level (exp {e_f})",
                      "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                      "traffic": traffic, "peak_kind": peak_kind,

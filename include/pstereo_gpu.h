@@ -231,6 +231,27 @@ int pstereo_gpu_set_profiling(pstereo_ctx* ctx, int enable);
  * sub-batch's finest level); 0 or 1 = one launch sequence. Results are
  * identical either way. Default: PSTEREO_DEVICE_CHUNKS or 2. */
 int pstereo_gpu_set_device_chunks(pstereo_ctx* ctx, int chunks);
+/* Host output buffers with finest_exp >= 1: every full-resolution plane is the
+ * 2^e x 2^e block replication of a finest-level plane (upsample_to_full,
+ * src/coarse_to_fine.cpp:166-180). With enable != 0 (the default;
+ * PSTEREO_HOST_EXPAND=0 turns it off) the planes cross the link at the finest
+ * level's resolution -- a quarter of the D2H bytes at finest_exp 1 -- and a
+ * pool of host threads (PSTEREO_HOST_THREADS, default min(cores / 2, 8); count
+ * via pstereo_gpu_host_threads) writes the blocks into the caller's buffers
+ * while later chunks download. With 0 the device writes full-resolution
+ * planes and the call copies them as they are. The bytes in the caller's
+ * buffers are identical either way. */
+int pstereo_gpu_set_host_expand(pstereo_ctx* ctx, int enable);
+int pstereo_gpu_host_threads(void);
+/* Totals since the pool started: worker milliseconds spent replicating and
+ * frames (one plane of one pair) finished. */
+int pstereo_host_expand_stats(double* busy_ms, long long* frames);
+/* The host-side replication on its own (no device): dst[f][y][x] =
+ * src[f][min(y >> e, fh - 1)][min(x >> e, fw - 1)] for n_frames frames of
+ * elem_size (1, 4 or 8) bytes per element, rows bottom to top when flip_rows;
+ * fw x fh must be W x H halved e times (rounding up). Runs on the pool. */
+int pstereo_host_expand(const void* src, void* dst, int elem_size, int fw, int fh, int W, int H,
+                        int e, int n_frames, int flip_rows);
 /* Small launches: each pyramid level's patch grid is cut into enough row
  * bands that the launch has at least `ctas` CTAs (default 148, one per SM:
  * the lowest latency for a single call). A caller that keeps several calls

@@ -162,6 +162,10 @@ def lib() -> C.CDLL:
         L.pstereo_gpu_last_launch_count.argtypes = [C.c_void_p]
         L.pstereo_gpu_set_profiling.argtypes = [C.c_void_p, C.c_int]
         L.pstereo_gpu_set_device_chunks.argtypes = [C.c_void_p, C.c_int]
+        L.pstereo_gpu_set_host_expand.argtypes = [C.c_void_p, C.c_int]
+        L.pstereo_gpu_host_threads.argtypes = []
+        L.pstereo_host_expand_stats.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_longlong)]
+        L.pstereo_host_expand.argtypes = [C.c_void_p, C.c_void_p] + [C.c_int] * 8
         L.pstereo_gpu_stage_times.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.c_int, i32p]
         L.pstereo_gpu_match_u8.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
                                            C.c_void_p, C.c_void_p, C.c_int, C.c_double,
@@ -246,6 +250,8 @@ ABI_SYMBOLS = [
     "pstereo_gpu_match_f32", "pstereo_gpu_last_launch_count", "pstereo_gpu_set_profiling",
     "pstereo_gpu_stage_times", "pstereo_gpu_stage_name", "pstereo_synth_default",
     "pstereo_gpu_synth", "pstereo_synth_last_error", "pstereo_gpu_set_device_chunks", "pstereo_gpu_render",
+    "pstereo_gpu_set_host_expand", "pstereo_gpu_host_threads", "pstereo_host_expand",
+    "pstereo_host_expand_stats",
     "pstereo_render_last_error", "pstereo_scene_default", "pstereo_scene_validate",
     "pstereo_load_scene_spec", "pstereo_load_calibration", "pstereo_load_image",
     "pstereo_write_pfm", "pstereo_read_pfm", "pstereo_metrics_csv_header",
@@ -609,6 +615,11 @@ class Matcher:
     def set_device_chunks(self, chunks: int):
         """Sub-batches per device call (pstereo_gpu_set_device_chunks)."""
         lib().pstereo_gpu_set_device_chunks(self._h, int(chunks))
+
+    def set_host_expand(self, on: bool):
+        """Host-output calls download finest-resolution planes and replicate them
+        on host threads (pstereo_gpu_set_host_expand; default on)."""
+        lib().pstereo_gpu_set_host_expand(self._h, int(on))
 
     def set_profiling(self, on: bool):
         lib().pstereo_gpu_set_profiling(self._h, int(on))
@@ -1025,3 +1036,23 @@ class MultiMatcher:
         res = _finish_outputs(res, n, self.n_levels, st, fin, cnt, finest_cap)
         res["ms_per_device"] = list(ms)
         return res
+
+
+def host_expand(src: np.ndarray, W: int, H: int, e: int, flip_rows: bool = False) -> np.ndarray:
+    """upsample_to_full's block replication on the host pool (pstereo_host_expand):
+    src is [frames, fh, fw] of a 1-, 4- or 8-byte dtype."""
+    src = np.ascontiguousarray(src)
+    n, fh, fw = src.shape
+    dst = np.empty((n, H, W), src.dtype)
+    rc = lib().pstereo_host_expand(src.ctypes.data, dst.ctypes.data, src.dtype.itemsize, fw, fh,
+                                   W, H, e, n, int(flip_rows))
+    if rc:
+        _raise(rc, "pstereo_host_expand: bad arguments")
+    return dst
+
+
+def host_expand_stats():
+    """(worker ms spent replicating, frames finished) since the pool started."""
+    ms, fr = C.c_double(), C.c_longlong()
+    lib().pstereo_host_expand_stats(C.byref(ms), C.byref(fr))
+    return ms.value, fr.value

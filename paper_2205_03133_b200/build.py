@@ -22,10 +22,10 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 CUDA_SOURCES = ["bdis_kernels.cu", "bdis_patches.cu", "bdis_metrics.cu", "bdis_capi.cu",
                 "bdis_synth.cu", "bdis_render.cu"]
-CXX_SOURCES = ["host_io.cpp", "bdis_multi.cpp"]
+CXX_SOURCES = ["host_io.cpp", "bdis_multi.cpp", "host_expand.cpp"]
 TOOLS = ["cli.cpp"]
 C_SOURCES = ["synth.c"]
-HEADERS = ["bdis_device.cuh", "bdis_kernels.h", "synth_core.h"]
+HEADERS = ["bdis_device.cuh", "bdis_kernels.h", "synth_core.h", "host_expand.h"]
 
 # Bit-exact parity with the x86-64 SSE2 reference needs IEEE double with no
 # FMA contraction anywhere (--fmad=false); the kernels also spell the critical
@@ -64,10 +64,16 @@ def build_gpu_lib(verbose: bool = False, force: bool = False) -> Path:
     objdir.mkdir(parents=True, exist_ok=True)
     objs = []
     log = []
+    hdrs = [CSRC / h for h in HEADERS] + [ROOT / "include" / "pstereo_gpu.h"]
+    fresh = lambda obj, src: not force and not _stale(obj, [CSRC / src, *hdrs])  # noqa: E731
     for src in CUDA_SOURCES:
         obj = objdir / (src + ".o")
-        log.append(_run([NVCC, *NVCC_FLAGS, "-c", str(CSRC / src), "-o", str(obj)], verbose))
         objs.append(obj)
+        plog = objdir / (src + ".ptxas")  # per-source ptxas -v output, joined below
+        if not (fresh(obj, src) and plog.exists()):
+            plog.write_text(_run([NVCC, *NVCC_FLAGS, "-c", str(CSRC / src), "-o", str(obj)],
+                                 verbose))
+        log.append(plog.read_text())
     for src in C_SOURCES:
         obj = objdir / (src + ".o")
         _run(["gcc", "-std=gnu11", "-O2", "-fPIC", "-ffp-contract=off", "-c",

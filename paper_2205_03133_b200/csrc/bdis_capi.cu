@@ -14,11 +14,16 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <deque>
+#include <mutex>
+#include <condition_variable>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/pstereo_gpu.h"
 #include "bdis_kernels.h"
+#include "host_expand.h"
 
 using namespace bdis;
 
@@ -143,6 +148,26 @@ struct DevBuf {
   }
 };
 
+// pinned host staging (grow-only)
+struct HostBuf {
+  uint8_t* p = nullptr;
+  size_t n = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= n && p) return cudaSuccess;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    n = 0;
+    cudaError_t e = cudaHostAlloc((void**)&p, bytes, cudaHostAllocDefault);
+    if (e == cudaSuccess) n = bytes;
+    return e;
+  }
+  void release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
 struct LevelBufs {
   DevBuf<float> left, right, grad;
   DevBuf<uint8_t> lvalid, rvalid, lq, rq, stage;
@@ -224,12 +249,23 @@ struct pstereo_ctx {
   double woff[kMaxWin] = {};
   DevBuf<double> mask;
   // inputs
-  DevBuf<uint8_t> in_u8[2];
+  // host u8 inputs: two staging sets alternating per call, so a call's uploads
+  // start under the previous call's kernels; in_free[set] is recorded on the
+  // call's stream once the kernels reading that set are queued behind it
+  DevBuf<uint8_t> in_u8[2][2];
+  int in_parity = 0;
+  cudaEvent_t in_free[2] = {nullptr, nullptr};
   DevBuf<float> full[2];
   DevBuf<uint8_t> full_valid[2];
   Scratch scr[2];  // [0]: the call's stream, [1]: the pipeline's second compute stream
   // staging for host outputs
   DevBuf<uint8_t> out_stage[2][10];  // alternating per call (async host outputs)
+  // host-side replication (host_expand.h): the planes cross the link at the
+  // finest level's resolution into pinned staging, host threads write the
+  // 2^e x 2^e blocks into the caller's buffers
+  int host_expand = 1;
+  HostBuf host_stage[2][10];
+  ExpandCounter expand_cnt[2];
   // PSTEREO_DEBUG_TIMELINE=1: timed events at the pipeline's chunk boundaries,
   // printed (ms from the first) by pstereo_gpu_wait -- a debugging aid
   bool timeline = false;
@@ -432,6 +468,7 @@ int pstereo_gpu_create(int device, const pstereo_params* p, int max_width, int m
   for (auto& sc : ctx->scr) sc.levels.resize(size_t(p->coarsest_exp) + 1);
   if (const char* v = getenv("PSTEREO_CHUNK_PAIRS")) ctx->chunk_pairs = atoi(v);
   if (const char* v = getenv("PSTEREO_DEVICE_CHUNKS")) ctx->device_chunks = atoi(v);
+  if (const char* v = getenv("PSTEREO_HOST_EXPAND")) ctx->host_expand = atoi(v) != 0;
   if (const char* v = getenv("PSTEREO_DEBUG_TIMELINE")) ctx->timeline = atoi(v) != 0;
   *out = ctx;
   return PSTEREO_OK;
@@ -441,8 +478,15 @@ void pstereo_gpu_destroy(pstereo_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->s_out) cudaStreamSynchronize(ctx->s_out);
+  for (auto& c : ctx->expand_cnt) c.wait();
+  for (auto& set : ctx->host_stage)
+    for (auto& b : set) b.release();
   ctx->mask.release();
-  for (auto& b : ctx->in_u8) b.release();
+  for (auto& set : ctx->in_u8)
+    for (auto& b : set) b.release();
+  for (auto e : ctx->in_free)
+    if (e) cudaEventDestroy(e);
   for (auto& b : ctx->full) b.release();
   for (auto& b : ctx->full_valid) b.release();
   for (auto& sc : ctx->scr) sc.release();
@@ -478,6 +522,7 @@ int pstereo_gpu_wait(pstereo_ctx* ctx, void* stream) {
   if (cudaSetDevice(ctx->device) != cudaSuccess) return fail(ctx, PSTEREO_EINTERNAL, "no device");
   for (cudaStream_t t : {ctx->s_in, ctx->s_comp, ctx->s_out, ctx->stream, (cudaStream_t)stream})
     if (t) CK(cudaStreamSynchronize(t));
+  for (auto& c : ctx->expand_cnt) c.wait();  // host-side replication of async calls
   if (!ctx->tl.empty()) {
     for (auto& m : ctx->tl) {
       float ms = 0.f;
@@ -545,6 +590,38 @@ int pstereo_gpu_metrics(pstereo_ctx* ctx, int n, int w, int h, const double* est
 int pstereo_gpu_set_fill_target(pstereo_ctx* ctx, int ctas) {
   if (!ctx || ctas < 0) return PSTEREO_EINTERNAL;
   ctx->fill_sms = ctas;
+  return PSTEREO_OK;
+}
+
+int pstereo_gpu_set_host_expand(pstereo_ctx* ctx, int enable) {
+  if (!ctx) return PSTEREO_EINTERNAL;
+  ctx->host_expand = enable != 0;
+  return PSTEREO_OK;
+}
+
+int pstereo_gpu_host_threads(void) { return expand_threads(); }
+
+int pstereo_host_expand_stats(double* busy_ms, long long* frames) {
+  if (!busy_ms || !frames) return PSTEREO_EINTERNAL;
+  expand_stats(busy_ms, frames);
+  return PSTEREO_OK;
+}
+
+int pstereo_host_expand(const void* src, void* dst, int elem_size, int fw, int fh, int W, int H,
+                        int e, int n_frames, int flip_rows) {
+  if (!src || !dst || (elem_size != 1 && elem_size != 4 && elem_size != 8) || fw <= 0 || fh <= 0 ||
+      W <= 0 || H <= 0 || e < 0 || e > 8 || n_frames < 0)
+    return PSTEREO_EINTERNAL;
+  // the finest level of a W x H frame after e halvings
+  int w = W, h = H;
+  for (int k = 0; k < e; ++k) w = (w + 1) / 2, h = (h + 1) / 2;
+  if (w != fw || h != fh) return PSTEREO_EINTERNAL;
+  if (n_frames == 0) return PSTEREO_OK;
+  ExpandJob j{src, dst, elem_size, fw, fh, W, H, e, n_frames, flip_rows ? 1 : 0};
+  ExpandCounter c;
+  c.add(n_frames);
+  expand_submit(&j, 1, &c);
+  c.wait();
   return PSTEREO_OK;
 }
 
@@ -867,9 +944,10 @@ int run_device(pstereo_ctx* ctx, Scratch& sc, const std::vector<LevelGeom>& geo,
 
   OutputArgs oa;
   std::memset(&oa, 0, sizeof oa);
-  oa.W = W;
-  oa.H = H;
-  oa.e = fe;
+  const bool compact = (out_flags & 4) != 0;  // finest-resolution planes (host_expand.h)
+  oa.W = compact ? F.w : W;
+  oa.H = compact ? F.h : H;
+  oa.e = compact ? 0 : fe;
   oa.fw = F.w;
   oa.fh = F.h;
   oa.fplane = F.plane;
@@ -929,6 +1007,57 @@ int run_device(pstereo_ctx* ctx, Scratch& sc, const std::vector<LevelGeom>& geo,
   return PSTEREO_OK;
 }
 
+// The replication jobs of one downloaded chunk. A dispatcher thread waits for
+// the chunk's D2H event and hands the jobs to the pool (a host function in
+// the D2H stream measured 0.1-0.4 ms of stream time per chunk: the stream sat
+// idle until the callback thread had run).
+struct ExpandBatch {
+  std::vector<ExpandJob> jobs;
+  ExpandCounter* counter = nullptr;
+  cudaEvent_t ready = nullptr;  // recorded after the chunk's downloads
+  int device = 0;
+};
+
+class ExpandDispatcher {
+ public:
+  static ExpandDispatcher& get() {
+    static ExpandDispatcher* d = new ExpandDispatcher;  // lives for the process
+    return *d;
+  }
+  void push(ExpandBatch* b) {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      q_.push_back(b);
+    }
+    cv_.notify_one();
+  }
+
+ private:
+  ExpandDispatcher() { std::thread([this] { run(); }).detach(); }
+  void run() {
+    int dev = -1;
+    for (;;) {
+      ExpandBatch* b;
+      {
+        std::unique_lock<std::mutex> g(m_);
+        cv_.wait(g, [&] { return !q_.empty(); });
+        b = q_.front();
+        q_.pop_front();
+      }
+      if (b->device != dev) cudaSetDevice(dev = b->device);
+      // poll rather than block: the chunk is ~0.2 ms of copy, and a blocking
+      // wait adds its wake-up latency to every chunk
+      while (cudaEventQuery(b->ready) == cudaErrorNotReady) std::this_thread::yield();
+      cudaEventDestroy(b->ready);
+      expand_submit(b->jobs.data(), int(b->jobs.size()), b->counter);
+      delete b;
+    }
+  }
+  std::mutex m_;
+  std::condition_variable cv_;
+  std::deque<ExpandBatch*> q_;
+};
+
 // Public entry: validates, then either runs the device path directly or --
 // with host buffers -- pipelines chunks of pairs over three streams (H2D of
 // chunk c+1 and D2H of chunk c-1 overlap the kernels of chunk c).
@@ -985,23 +1114,37 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
   if (split) chunk = (n + ctx->device_chunks - 1) / ctx->device_chunks;
   // device input regions
   const uint8_t* dev_u8[2] = {left_u8, right_u8};
+  const bool stage_u8 = left_u8 && host_in;
+  const int in_par = ctx->in_parity;
   if (left_u8 && host_in)
     for (int v = 0; v < 2; ++v) {
-      CK(ctx->in_u8[v].ensure(size_t(n_full) * n * channels));
-      dev_u8[v] = ctx->in_u8[v].p;
+      CK(ctx->in_u8[in_par][v].ensure(size_t(n_full) * n * channels));
+      dev_u8[v] = ctx->in_u8[in_par][v].p;
     }
   if (!left_u8)
     for (int v = 0; v < 2; ++v) {
       CK(ctx->full[v].ensure(size_t(n_full) * n));
       CK(ctx->full_valid[v].ensure(size_t(n_full) * n));
     }
+  // host outputs of a replicated finest level (finest_exp >= 1): the planes
+  // are downloaded at the finest level's resolution and replicated into the
+  // caller's buffers by host threads (host_expand.h) -- a quarter of the D2H
+  // bytes at finest_exp 1
+  const bool compact = host_out && ctx->host_expand && geo.back().e >= 1;
+  const long long n_fin = (long long)geo.back().w * geo.back().h;
+  const long long n_stage = compact ? n_fin : n_full;  // staged pixels per pair
   // device output regions
   void* dev_out[10];
+  uint8_t* host_stage[10] = {};
   for (int q = 0; q < 10; ++q) {
     dev_out[q] = user_ptr[q];
     if (user_ptr[q] && host_out) {
-      CK(ctx->out_stage[ctx->out_parity][q].ensure(size_t(n_full) * n * sizes[q]));
+      CK(ctx->out_stage[ctx->out_parity][q].ensure(size_t(n_stage) * n * sizes[q]));
       dev_out[q] = ctx->out_stage[ctx->out_parity][q].p;
+      if (compact) {
+        CK(ctx->host_stage[ctx->out_parity][q].ensure(size_t(n_stage) * n * sizes[q]));
+        host_stage[q] = ctx->host_stage[ctx->out_parity][q].p;
+      }
     }
   }
   if ((pipelined || split) && !ctx->s_in) {
@@ -1042,15 +1185,22 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
     // before last (async_host): the kernels start only after those copies
     CK(cudaStreamWaitEvent(s, ctx->stage_free[parity], 0));
   }
+  // ... and its pinned host half may still be feeding that call's replication
+  if (compact) ctx->expand_cnt[parity].wait();
   if (pipelined || split) {
     // the helper streams start behind the work already queued on the caller's stream
     CK(cudaEventRecord(ev_start, s));
-    for (cudaStream_t t : {ctx->s_in, ctx->s_comp, ctx->s_out}) CK(cudaStreamWaitEvent(t, ev_start, 0));
+    for (cudaStream_t t : {ctx->s_comp, ctx->s_out}) CK(cudaStreamWaitEvent(t, ev_start, 0));
+    // staged u8 uploads only wait for the kernels that last read their set
+    // (the call before last): they run under the previous call's kernels
+    if (!stage_u8) CK(cudaStreamWaitEvent(ctx->s_in, ev_start, 0));
+    else if (ctx->in_free[in_par]) CK(cudaStreamWaitEvent(ctx->s_in, ctx->in_free[in_par], 0));
   }
   bool used_comp = false;
   for (int c = 0; c < n_chunks; ++c) {
     const int c0 = starts[size_t(c)], nc = starts[size_t(c) + 1] - c0;
     const size_t px0 = size_t(n_full) * c0, pxc = size_t(n_full) * nc;
+    const size_t sx0 = size_t(n_stage) * c0, sxc = size_t(n_stage) * nc;  // staged outputs
     // consecutive chunks alternate between two compute streams / working sets
     const int slot = (pipelined || split) ? (c & 1) : 0;
     cudaStream_t cs = slot ? ctx->s_comp : s;
@@ -1060,7 +1210,7 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
       if (left_u8) {
         if (host_in)
           for (int v = 0; v < 2; ++v)
-            CK(cudaMemcpyAsync(ctx->in_u8[v].p + px0 * channels, (v ? right_u8 : left_u8) + px0 * channels,
+            CK(cudaMemcpyAsync(ctx->in_u8[in_par][v].p + px0 * channels, (v ? right_u8 : left_u8) + px0 * channels,
                                pxc * channels, cudaMemcpyHostToDevice, sc));
       } else {
         const cudaMemcpyKind kind = host_in ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
@@ -1088,7 +1238,7 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
                              left_u8 ? dev_u8[1] + px0 * channels : nullptr};
     void* cout[10];
     for (int q = 0; q < 10; ++q)
-      cout[q] = dev_out[q] ? (uint8_t*)dev_out[q] + px0 * sizes[q] : nullptr;
+      cout[q] = dev_out[q] ? (uint8_t*)dev_out[q] + (host_out ? sx0 : px0) * sizes[q] : nullptr;
     HostCopies hc;
     if (!hstats.empty()) hc.stats = hstats.data() + size_t(c0) * n_levels * 3;
     if (want_finest) {
@@ -1100,18 +1250,53 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
     }
     rc = run_device(ctx, ctx->scr[slot], geo, nc, W, H, channels, cu8, left_u8 ? 0 : c0,
                     have_f32_valid, focal, baseline, f64,
-                    (out->fill_invalid ? 1 : 0) | (out->flip_rows ? 2 : 0), out->invalid_value,
-                    cout, hc, cs);
+                    (out->fill_invalid ? 1 : 0) | (out->flip_rows && !compact ? 2 : 0) |
+                        (compact ? 4 : 0),
+                    out->invalid_value, cout, hc, cs);
     if (rc) return rc;
     if (host_out) {
       mark("compute done c" + std::to_string(c) + (slot ? " (s2)" : " (s1)"), cs);
       CK(cudaEventRecord(ev[2 * c + 1], cs));
       CK(cudaStreamWaitEvent(ctx->s_out, ev[2 * c + 1], 0));
       mark("d2h start c" + std::to_string(c), ctx->s_out);
-      for (int q = 0; q < 10; ++q)
-        if (user_ptr[q])
-          CK(cudaMemcpyAsync((uint8_t*)user_ptr[q] + px0 * sizes[q], cout[q], pxc * sizes[q],
+      if (!compact) {
+        for (int q = 0; q < 10; ++q)
+          if (user_ptr[q])
+            CK(cudaMemcpyAsync((uint8_t*)user_ptr[q] + px0 * sizes[q], cout[q], pxc * sizes[q],
+                               cudaMemcpyDeviceToHost, ctx->s_out));
+      } else {
+        // finest-resolution download; the dispatcher queues this chunk's
+        // replication jobs once the copies have landed
+        auto* ex = new ExpandBatch;
+        ex->counter = &ctx->expand_cnt[parity];
+        for (int q = 0; q < 10; ++q) {
+          if (!user_ptr[q]) continue;
+          CK(cudaMemcpyAsync(host_stage[q] + sx0 * sizes[q], cout[q], sxc * sizes[q],
                              cudaMemcpyDeviceToHost, ctx->s_out));
+          ExpandJob j;
+          j.src = host_stage[q] + sx0 * sizes[q];
+          j.dst = (uint8_t*)user_ptr[q] + px0 * sizes[q];
+          j.esz = int(sizes[q]);
+          j.fw = geo.back().w;
+          j.fh = geo.back().h;
+          j.W = W;
+          j.H = H;
+          j.e = geo.back().e;
+          j.n_pairs = nc;
+          j.flip = out->flip_rows ? 1 : 0;
+          ex->jobs.push_back(j);
+        }
+        ex->counter->add(long(ex->jobs.size()) * nc);
+        ex->device = ctx->device;
+        cudaError_t he = cudaEventCreateWithFlags(&ex->ready, cudaEventDisableTiming);
+        if (he == cudaSuccess) he = cudaEventRecord(ex->ready, ctx->s_out);
+        if (he != cudaSuccess) {
+          ex->counter->done(long(ex->jobs.size()) * nc);
+          delete ex;
+          return cuda_fail(ctx, he, "download event");
+        }
+        ExpandDispatcher::get().push(ex);
+      }
       mark("d2h done c" + std::to_string(c), ctx->s_out);
     }
   }
@@ -1119,6 +1304,12 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
   if (used_comp) {
     CK(cudaEventRecord(ev_comp, ctx->s_comp));
     CK(cudaStreamWaitEvent(s, ev_comp, 0));
+  }
+  if (stage_u8) {
+    if (!ctx->in_free[in_par])
+      CK(cudaEventCreateWithFlags(&ctx->in_free[in_par], cudaEventDisableTiming));
+    CK(cudaEventRecord(ctx->in_free[in_par], s));
+    ctx->in_parity ^= 1;
   }
   // async host outputs: the downloads stay queued on s_out (staging sets
   // alternate per call, so the next call's kernels never touch them)
@@ -1135,6 +1326,7 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
   const bool need_sync = !async && (host_out || !hstats.empty() || want_finest);
   if (need_sync && host_out) CK(cudaStreamSynchronize(ctx->s_out));
   if (need_sync) CK(cudaStreamSynchronize(s));
+  if (need_sync && compact) ctx->expand_cnt[parity].wait();
   if (!hstats.empty()) {
     for (int p = 0; p < n; ++p)
       for (int li = 0; li < n_levels; ++li) {

@@ -14,6 +14,7 @@ hr = torch.from_numpy(right).pin_memory()
 hd = torch.empty((B, H, W), dtype=torch.float32).pin_memory()
 m = P.Matcher(P.PipelineConfig.baseline(0), W, H, B)
 s = torch.cuda.Stream()
+print(f"host threads {P.lib().pstereo_gpu_host_threads()}", flush=True)
 for K in (1, 2, 5, 10, 20):
     for _ in range(2):
         m.run_host_u8(B, W, H, 1, hl.data_ptr(), hr.data_ptr(), {"disparity": hd.data_ptr()},
@@ -28,5 +29,7 @@ for K in (1, 2, 5, 10, 20):
         enq.append(time.perf_counter() - a)
     m.wait(s.cuda_stream)
     dt = time.perf_counter() - t0
+    busy, frames = P.host_expand_stats()
     print(f"K={K}: {dt / K * 1e3:.2f} ms/call, {B * K / dt:.0f} pairs/s, enqueue ms/call "
-          f"{sum(enq) / K * 1e3:.2f} (max {max(enq) * 1e3:.2f})", flush=True)
+          f"{sum(enq) / K * 1e3:.2f} (max {max(enq) * 1e3:.2f}); replication total "
+          f"{busy:.1f} worker-ms / {frames} frames", flush=True)
