@@ -56,6 +56,21 @@ __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wa
 __device__ __forceinline__ void griddep_launch() {
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 }
+// a shared-memory load by window address (address = per-thread column + a
+// warp-uniform row offset: ptxas folds the sum into LDS [R + UR])
+__device__ __forceinline__ float lds_f32(unsigned addr) {
+  float v;
+  asm("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
+// element index -> byte offset, opaque to the optimiser: otherwise it keeps
+// element offsets and re-forms every address with a per-load LEA
+__device__ __forceinline__ unsigned byte_ofs(int elem) {
+  unsigned b;
+  // a rotate (== shift for elem < 2^30): a plain shl is folded back into the LEA
+  asm("shf.l.wrap.b32 %0, %1, %1, 2;" : "=r"(b) : "r"(elem));
+  return b;
+}
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
@@ -142,19 +157,34 @@ __device__ __forceinline__ Ev eval_patch(const Rows<kSmem>& rw, int w, int s_rt,
     const int n = SA * __popc(inb);
     ev.n = n;
     const int xb = base + rpad;  // smem column of tap `base`
+    // Per-thread byte addresses of the patch's tap / template columns in its
+    // first row; the row offset j * pitch is the same for every lane, so it
+    // stays in the uniform datapath and each load is LDS [R + UR] with no
+    // per-load address instruction (measured: 19 of the 120 instructions of a
+    // window-pass row were IMADs forming these addresses)
+    unsigned cR[SA + 1], cL[SA];  // byte offsets of the columns within their arrays
+#pragma unroll
+    for (int i = 0; i <= SA; ++i) cR[i] = byte_ofs(r0 * rw.rp + rw.s8(xb + i));
+#pragma unroll
+    for (int i = 0; i < SA; ++i) cL[i] = byte_ofs(r0 * rw.fp + offT[i]);
+    // uniform parts: array base (shared window) + row offset
+    const unsigned bR = (unsigned)__cvta_generic_to_shared(rw.R);
+    const unsigned bL = (unsigned)__cvta_generic_to_shared(rw.Lf);
+    const unsigned bG = (unsigned)__cvta_generic_to_shared(rw.Gf);
+    const unsigned rp4 = rw.rp * 4, fp4 = rw.fp * 4;
     double sum = 0.0;
-    const auto* rr = rw.R + r0 * rw.rp;
     // s = 12 and 8: rows two at a time, the next row's taps loading under this
     // row's chain -- 26-32% faster at s = 12 / stride 4 (configs 3 and 4);
     // at s = 8 -0.5% on config 2 and -1.3% single-pair latency (+1% on the
     // variance config 1); s = 10 / 16 measured slower with it, and so did the
     // residual pass (profiles/r02/k_patches_experiments.md)
 #pragma unroll((S == 12 || S == 8) ? 2 : 1)
-    for (int j = 0; j < SA; ++j, rr += rw.rp) {
-      double a = (double)rr[rw.s8(xb)];
+    for (int j = 0; j < SA; ++j) {
+      const unsigned oR = bR + j * rp4;
+      double a = (double)lds_f32(cR[0] + oR);
 #pragma unroll
       for (int i = 0; i < SA; ++i) {
-        const double b = (double)rr[rw.s8(xb + i + 1)];
+        const double b = (double)lds_f32(cR[i + 1] + oR);
         // masked columns have cfx = comf = 0: v = +-0 leaves the sum unchanged
         sum = __dadd_rn(sum, __dadd_rn(__dmul_rn(mo[i], a), __dmul_rn(mf[i], b)));
         a = b;
@@ -164,23 +194,21 @@ __device__ __forceinline__ Ev eval_patch(const Rows<kSmem>& rw, int w, int s_rt,
     double ssr = 0.0, jr = 0.0;
     auto pass2 = [&](auto masked) {
       constexpr bool kMask = decltype(masked)::value;
-      const auto* rr = rw.R + r0 * rw.rp;
-      const float* lr = rw.Lf + r0 * rw.fp;
-      const float* gr = rw.Gf + r0 * rw.fp;
 #pragma unroll 1
-      for (int j = 0; j < SA; ++j, rr += rw.rp, lr += rw.fp, gr += rw.fp) {
-        double a = (double)rr[rw.s8(xb)];
+      for (int j = 0; j < SA; ++j) {
+        const unsigned oR = bR + j * rp4, oL = bL + j * fp4, oG = bG + j * fp4;
+        double a = (double)lds_f32(cR[0] + oR);
 #pragma unroll
         for (int i = 0; i < SA; ++i) {
-          const double b = (double)rr[rw.s8(xb + i + 1)];
+          const double b = (double)lds_f32(cR[i + 1] + oR);
           const double v = __dadd_rn(__dmul_rn(mo[i], a), __dmul_rn(mf[i], b));
           a = b;
-          const double t = __dsub_rn((double)lr[offT[i]], mean);
+          const double t = __dsub_rn((double)lds_f32(cL[i] + oL), mean);
           double r = __dsub_rn(__dsub_rn(v, rmean), t);
           // masked columns: r * 0 = +-0 adds nothing to ssr / jr
           if (kMask) r = __dmul_rn(r, mk[i]);
           ssr = __dadd_rn(ssr, __dmul_rn(r, r));
-          if (kJr) jr = __dadd_rn(jr, __dmul_rn((double)gr[offT[i]], r));
+          if (kJr) jr = __dadd_rn(jr, __dmul_rn((double)lds_f32(cL[i] + oG), r));
         }
       }
     };
@@ -311,20 +339,34 @@ __global__ void __launch_bounds__(256, S == -16 ? 2 : 0) k_patches(Level L, Leve
     const int rw2 = w + 1 + 2 * rpad;
     // asynchronous copies (cp.async): every thread queues all of its
     // elements before waiting once, instead of a few loads in flight
+    // (row, column) of the flat index q advance incrementally: no division
+    {
+      int r = tid / rw2, xs = tid - r * rw2;  // xs = x + rpad
+      const int dr = nt / rw2, dx = nt - dr * rw2;
 #pragma unroll 4
-    for (int q = tid; q < nrows * rw2; q += nt) {
-      const int r = q / rw2, x = q - r * rw2 - rpad;
-      float* dst = sR + r * bp.rpitch + Rows<true>::s8(x + rpad);
-      if (x >= 0 && x <= w) cp_async4(dst, gR + (long long)r * (w + 1) + x);
-      else *dst = 0.0f;
+      for (int q = tid; q < nrows * rw2; q += nt) {
+        const int x = xs - rpad;
+        float* dst = sR + r * bp.rpitch + Rows<true>::s8(xs);
+        if (x >= 0 && x <= w) cp_async4(dst, gR + r * (w + 1) + x);
+        else *dst = 0.0f;
+        xs += dx;
+        r += dr;
+        if (xs >= rw2) xs -= rw2, ++r;
+      }
     }
     const float* gl0 = L.left + pbase + (long long)ylo * w;
     const float* gg0 = L.grad + pbase + (long long)ylo * w;
+    {
+      int r = tid / w, x = tid - r * w;
+      const int dr = nt / w, dx = nt - dr * w;
 #pragma unroll 4
-    for (int q = tid; q < nrows * w; q += nt) {
-      const int r = q / w, x = q - r * w;
-      cp_async4(sL + r * bp.fpitch + Rows<true>::s4(x), gl0 + q);
-      cp_async4(sG + r * bp.fpitch + Rows<true>::s4(x), gg0 + q);
+      for (int q = tid; q < nrows * w; q += nt) {
+        cp_async4(sL + r * bp.fpitch + Rows<true>::s4(x), gl0 + q);
+        cp_async4(sG + r * bp.fpitch + Rows<true>::s4(x), gg0 + q);
+        x += dx;
+        r += dr;
+        if (x >= w) x -= w, ++r;
+      }
     }
     cp_async_wait_all();
     for (int r = 0; r < nrows; ++r) {
