@@ -39,6 +39,7 @@ struct BandPlan {
   int rpad;        // zero slots either side of a staged right row (= patch size)
   size_t smem_bytes;
   int npb;         // max patches per band = rb * nx
+  unsigned nx_magic;  // ceil(2^32 / nx): p / nx == umulhi(p, nx_magic) for p < npb
 };
 
 // Shared-memory layout of one k_patches CTA (byte offsets), shared by the
