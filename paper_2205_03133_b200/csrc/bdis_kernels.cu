@@ -446,10 +446,11 @@ __device__ __forceinline__ int run_start(unsigned bits, int row, int lane) {
 // not accepted carry zero weight (prob = u = sigma = 0), which leaves the
 // fusion sums bit-identical to skipping them (sums start at +0.0 and never
 // become -0.0 under round-to-nearest, so adding +0.0 is the identity).
+// One shared array: prob at [0, kTileRec), u at [kTileRec, 2 kTileRec), sigma_k
+// after it -- the three loads of a record share one address register and
+// differ by immediates.
 struct TileRecords {
-  const double* pr;
-  const double* uu;
-  const double* sg;
+  const double* base;
   int ky0, kx0, ncol;
 };
 
@@ -460,8 +461,8 @@ constexpr int kTileRec = 320;  // records staged per tile; more -> global gather
 // unused entries point at the tile's zero column (adds +0.0, the identity).
 template <int K>
 struct ColList {
-  int kxo[K];   // column within the staged records
-  int moff[K];  // x - footprint start (mask column)
+  int kxo[K];   // column within the staged records, in bytes
+  int moff[K];  // x - footprint start (mask column), in bytes
 };
 
 template <int K>
@@ -472,13 +473,13 @@ __device__ __forceinline__ bool col_list(const Grid& g, int x, Cover cx, int kx0
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     if (k < nmain) {
-      cl->kxo[k] = cx.lo + k - kx0;
-      cl->moff[k] = x - (cx.lo + k) * g.stride;
+      cl->kxo[k] = 8 * (cx.lo + k - kx0);
+      cl->moff[k] = 8 * (x - (cx.lo + k) * g.stride);
     } else if (cx.last && k == max(nmain, 0)) {
-      cl->kxo[k] = g.nx - 1 - kx0;
-      cl->moff[k] = x - g.lastx0;
+      cl->kxo[k] = 8 * (g.nx - 1 - kx0);
+      cl->moff[k] = 8 * (x - g.lastx0);
     } else {
-      cl->kxo[k] = zcol;
+      cl->kxo[k] = 8 * zcol;
       cl->moff[k] = 0;
     }
   }
@@ -492,18 +493,18 @@ __device__ __forceinline__ Fused gather_tile(const Grid& g, const TileRecords& r
   const int s = g.size, st = g.stride;
   Fused f{0.0, 0.0, 0.0, 0.0};
   auto row = [&](int ky, int y0) {
-    const double* mrow = mask + (y - y0) * s;
-    const int qrow = (ky - rec.ky0) * rec.ncol;
+    const char* mrow = (const char*)(mask + (y - y0) * s);
+    const char* qrow = (const char*)(rec.base + (ky - rec.ky0) * rec.ncol);
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      const int q = qrow + cl.kxo[k];
-      const double pr = rec.pr[q];
-      const double w = __dmul_rn(pr, mrow[cl.moff[k]]);
+      const double* q = (const double*)(qrow + cl.kxo[k]);
+      const double pr = q[0];
+      const double w = __dmul_rn(pr, *(const double*)(mrow + cl.moff[k]));
       f.sw = __dadd_rn(f.sw, w);
-      f.swu = __dadd_rn(f.swu, __dmul_rn(w, rec.uu[q]));
+      f.swu = __dadd_rn(f.swu, __dmul_rn(w, q[kTileRec]));
       f.swp = __dadd_rn(f.swp, __dmul_rn(w, pr));
       if (kVar) {
-        const double sk = rec.sg[q];
+        const double sk = q[2 * kTileRec];
         f.sw2s = __dadd_rn(f.sw2s, __dmul_rn(__dmul_rn(__dmul_rn(w, w), sk), sk));
       }
     }
@@ -526,7 +527,10 @@ __global__ void __launch_bounds__(kFuseThreads, (!kVar && K <= 3) ? 5 : 4) k_fus
   __shared__ int sl[kTilePx];
   __shared__ int s_area[kTilePx];
   __shared__ unsigned s_bits[kTileH];
-  __shared__ double s_pr[kTileRec], s_u[kTileRec], s_sg[kVar ? kTileRec : 1];
+  __shared__ double s_rec[(kVar ? 3 : 2) * kTileRec];
+  double* const s_pr = s_rec;
+  double* const s_u = s_rec + kTileRec;
+  double* const s_sg = s_rec + (kVar ? 2 * kTileRec : 0);  // (unused without variance)
   __shared__ Cover s_cy[kTileH];
   __shared__ double s_mask[kMaxPatch * kMaxPatch];
   __shared__ int s_nroot;
@@ -574,7 +578,7 @@ __global__ void __launch_bounds__(kFuseThreads, (!kVar && K <= 3) ? 5 : 4) k_fus
     }
   }
   __syncthreads();
-  const TileRecords rec{s_pr, s_u, s_sg, ky0, kx0, pitch};
+  const TileRecords rec{s_rec, ky0, kx0, pitch};
   const long long pbase = pair * L.plane;
 #pragma unroll 1
   for (int i = 0; i < kFuseRows; ++i) {
