@@ -1,4 +1,5 @@
-"""Key metrics of an ncu --set full report (first kernel), for profiles/ notes."""
+"""Key metrics of an ncu --set full report (first kernel, or the launch whose
+index is the second argument), for profiles/ notes."""
 import csv
 import io
 import subprocess
@@ -8,7 +9,7 @@ rep = sys.argv[1]
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                      text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
-hdr, units, vals = rows[0], rows[1], rows[2]
+hdr, units, vals = rows[0], rows[1], rows[2 + (int(sys.argv[2]) if len(sys.argv) > 2 else 0)]
 want = [
     "Kernel Name", "gpu__time_duration.sum", "launch__grid_size", "launch__block_size",
     "launch__registers_per_thread", "launch__shared_mem_per_block_dynamic",
