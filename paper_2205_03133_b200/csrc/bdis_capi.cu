@@ -15,6 +15,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <deque>
+#include <memory>
 #include <mutex>
 #include <condition_variable>
 #include <string>
@@ -1267,7 +1268,7 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
       } else {
         // finest-resolution download; the dispatcher queues this chunk's
         // replication jobs once the copies have landed
-        auto* ex = new ExpandBatch;
+        std::unique_ptr<ExpandBatch> ex(new ExpandBatch);
         ex->counter = &ctx->expand_cnt[parity];
         for (int q = 0; q < 10; ++q) {
           if (!user_ptr[q]) continue;
@@ -1292,10 +1293,9 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
         if (he == cudaSuccess) he = cudaEventRecord(ex->ready, ctx->s_out);
         if (he != cudaSuccess) {
           ex->counter->done(long(ex->jobs.size()) * nc);
-          delete ex;
           return cuda_fail(ctx, he, "download event");
         }
-        ExpandDispatcher::get().push(ex);
+        ExpandDispatcher::get().push(ex.release());
       }
       mark("d2h done c" + std::to_string(c), ctx->s_out);
     }

@@ -91,3 +91,35 @@ def test_host_outputs_identical_with_and_without_host_expand(gpu, w, h, ce, fe, 
     # flipped rows are the unflipped planes bottom to top
     assert np.array_equal(res[True, True]["disparity"].view(np.uint8),
                           np.ascontiguousarray(res[True, False]["disparity"][:, ::-1]).view(np.uint8))
+
+
+@pytest.mark.gpu
+def test_async_calls_alternating_download_modes(gpu):
+    """Back-to-back async_host calls that alternate between the
+    finest-resolution download (+ host replication) and the full-resolution
+    download share the context's staging sets; every call's planes must equal
+    the synchronous result of its own batch."""
+    import torch
+
+    P = gpu
+    n, w, h, calls = 24, 320, 240, 6
+    cfg = P.PipelineConfig.baseline(0)
+    planes = ("disparity", "disparity_valid", "probability")
+    with P.Matcher(cfg, w, h, n) as m:
+        batches = [P.synth_batch(0, n, seed0=500 + k * n, width=w, height=h) for k in range(calls)]
+        want = [m.run_batch(l, r, dtype=P.F32, want=planes, invalid_value=-1.0) for l, r in batches]
+        pinned = [(torch.from_numpy(l).pin_memory(), torch.from_numpy(r).pin_memory())
+                  for l, r in batches]
+        outs = [{k: torch.full((n, h, w), 7, dtype=torch.uint8 if "valid" in k
+                               else torch.float32).pin_memory() for k in planes}
+                for _ in range(calls)]
+        for k, ((hl, hr), o) in enumerate(zip(pinned, outs)):
+            m.set_host_expand(k % 2 == 0)
+            m.run_host_u8(n, w, h, 1, hl.data_ptr(), hr.data_ptr(),
+                          {q: v.data_ptr() for q, v in o.items()}, dtype=P.F32,
+                          invalid_value=-1.0, async_host=True)
+        m.wait()
+    for k in range(calls):
+        for name in planes:
+            a, b = want[k][name], outs[k][name].numpy()
+            assert np.array_equal(a.view(np.uint8), b.view(np.uint8)), (k, name)
