@@ -567,7 +567,7 @@ __global__ void __launch_bounds__(256, S == -16 ? 2 : 0) k_patches(Level L, Leve
   // lanes take window samples (src/window_posterior.cpp:10-36) of patches that
   // converged in earlier rounds. Idle warps go straight to the barrier, so a
   // long solve keeps one warp busy, not a quarter of every warp.
-  enum { cNPool, cConv, cNAct, cPoolNext = 4, cWNext = 6, cWAvail = 8, cAlive = 10 };
+  enum { cNPool, cConv, cNAct, cPoolNext = 4, cWNext = 6, cWAvail = 8, cAlive = 10, cFit = 30 };
   {
     const int n_pool = counters[cNPool];
     const int n0 = min(n_pool, nt);
@@ -763,7 +763,12 @@ __global__ void __launch_bounds__(256, S == -16 ? 2 : 0) k_patches(Level L, Leve
           u_out = st_u[p];
           prob_out = pr;
           post_out = posterior;
-          if (pp.want_var) sig_out = variance_fit(pp.woff, nwin, pp.wcenter, res, ok, denom);
+          if (pp.want_var) {
+            // the fit runs below on densely packed lanes: here only ~half the
+            // lanes hold an accepted patch (measured 13 of 32 active)
+            st_hess[p] = denom;  // the Hessian is dead after phase 2
+            pool[atomicAdd(&counters[cFit], 1)] = p;
+          }
           stage = kAccepted;
         }
       }
@@ -774,6 +779,16 @@ __global__ void __launch_bounds__(256, S == -16 ? 2 : 0) k_patches(Level L, Leve
     L.prob[rec] = prob_out;
     L.post[rec] = post_out;
     L.sigma[rec] = sig_out;
+  }
+  if (pp.want_var) {
+    // estimate_patch_variance (src/depth_variance.cpp:94-170) of the accepted patches
+    __syncthreads();
+    const int nfit = counters[cFit];
+    for (int q = tid; q < nfit; q += nt) {
+      const int p = pool[q];
+      L.sigma[rec0 + p] = variance_fit(pp.woff, nwin, pp.wcenter, st_wres + p * nwin,
+                                       st_wok + p * nwin, st_hess[p]);
+    }
   }
 }
 
