@@ -236,7 +236,7 @@ int pstereo_gpu_set_device_chunks(pstereo_ctx* ctx, int chunks);
  * src/coarse_to_fine.cpp:166-180). With enable != 0 (the default;
  * PSTEREO_HOST_EXPAND=0 turns it off) the planes cross the link at the finest
  * level's resolution -- a quarter of the D2H bytes at finest_exp 1 -- and a
- * pool of host threads (PSTEREO_HOST_THREADS, default min(cores / 2, 8); count
+ * pool of host threads (PSTEREO_HOST_THREADS, default min(3 cores / 8, 6); count
  * via pstereo_gpu_host_threads) writes the blocks into the caller's buffers
  * while later chunks download. With 0 the device writes full-resolution
  * planes and the call copies them as they are. The bytes in the caller's

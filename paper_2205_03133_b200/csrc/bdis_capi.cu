@@ -1104,7 +1104,13 @@ int run(pstereo_ctx* ctx, int n, int W, int H, int channels, const uint8_t* left
   // chunking: one chunk for the device path, else pairs per chunk
   int chunk = n;
   if (pipelined) {
-    chunk = ctx->chunk_pairs > 0 ? ctx->chunk_pairs : 32;
+    // 32 pairs per chunk for the lowest single-call latency; queued
+    // (async_host) calls with host-side replication run 96-pair chunks -- fewer,
+    // larger bursts for the replication workers and better-filled kernels
+    // (measured 4.3 -> 3.7 ms per 256-pair call, profiles/r02/e2e_host_expand.txt)
+    const bool queued_compact = !out->on_device && out->async_host && ctx->host_expand &&
+                                geo.back().e >= 1;
+    chunk = ctx->chunk_pairs > 0 ? ctx->chunk_pairs : (queued_compact ? 96 : 32);
     if (chunk > n) chunk = n;
   }
   // device path: optionally split the batch into sub-batches alternating over

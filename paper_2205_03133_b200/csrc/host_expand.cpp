@@ -193,10 +193,11 @@ class Pool {
 
  private:
   Pool() {
-    // measured on the 16-core bench host: 6-8 workers are the best (more only
-    // add memory-controller contention against the H2D DMA reads)
-    int n = int(std::thread::hardware_concurrency()) / 2;
-    n = std::max(1, std::min(n, 8));
+    // measured on the 16-core bench host: 5-6 workers are the best (4 cannot
+    // keep up, 7 and more add memory-controller contention against the H2D
+    // DMA reads)
+    int n = int(std::thread::hardware_concurrency()) * 3 / 8;
+    n = std::max(1, std::min(n, 6));
     if (const char* v = std::getenv("PSTEREO_HOST_THREADS")) n = std::max(1, std::atoi(v));
     for (int t = 0; t < n; ++t) threads_.emplace_back([this] { run(); });
     for (auto& t : threads_) t.detach();

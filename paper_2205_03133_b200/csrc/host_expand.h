@@ -42,8 +42,8 @@ void expand_frame(const ExpandJob& j, int pair);
 // frames finish (the caller has already add()ed n_pairs per job)
 void expand_submit(const ExpandJob* jobs, int n, ExpandCounter* c);
 
-// worker threads of the pool (PSTEREO_HOST_THREADS, default: half the host's
-// cores, at most 8); started on first use
+// worker threads of the pool (PSTEREO_HOST_THREADS, default: 3/8 of the
+// host's cores, at most 6); started on first use
 int expand_threads();
 
 // totals since the pool started: worker time inside expand_frame, frames done

@@ -15,7 +15,7 @@ hd = torch.empty((B, H, W), dtype=torch.float32).pin_memory()
 m = P.Matcher(P.PipelineConfig.baseline(0), W, H, B)
 s = torch.cuda.Stream()
 print(f"host threads {P.lib().pstereo_gpu_host_threads()}", flush=True)
-for K in (1, 2, 5, 10, 20):
+for K in ([int(v) for v in sys.argv[1].split(",")] if len(sys.argv) > 1 else (1, 2, 5, 10, 20)):
     for _ in range(2):
         m.run_host_u8(B, W, H, 1, hl.data_ptr(), hr.data_ptr(), {"disparity": hd.data_ptr()},
                       stream=s.cuda_stream, invalid_value=float("nan"), async_host=True)
