@@ -786,7 +786,7 @@ int run_device(pstereo_ctx* ctx, Scratch& sc, const std::vector<LevelGeom>& geo,
     L.plane = (long long)G.w * G.h;
     const size_t np = size_t(L.plane) * n;
     CK(B.grad.ensure(np));
-    CK(B.rpad.ensure(size_t(G.w + 1) * G.h * n));
+    CK(B.rpad.ensure(size_t(rpad_pitch(G.w)) * G.h * n));
     if (G.e == 0 && !fused) {
       L.left = left_u8 ? sc.gray[0].p : fsrc[0];
       L.right = left_u8 ? sc.gray[1].p : fsrc[1];
@@ -1508,7 +1508,7 @@ extern "C" int pstereo_debug_eval_residual(int device, int width, int height, co
   bool ok = dl.ensure(px) == cudaSuccess && dr.ensure(px) == cudaSuccess &&
             dg.ensure(px) == cudaSuccess && lv.ensure(px) == cudaSuccess &&
             rv.ensure(px) == cudaSuccess && lq.ensure(px) == cudaSuccess &&
-            rq.ensure(px) == cudaSuccess && rd.ensure(size_t(width + 1) * height) == cudaSuccess &&
+            rq.ensure(px) == cudaSuccess && rd.ensure(size_t(rpad_pitch(width)) * height) == cudaSuccess &&
             dq_u.ensure(nq) == cudaSuccess && d_msq.ensure(nq) == cudaSuccess &&
             d_jr.ensure(nq) == cudaSuccess && dqx.ensure(nq) == cudaSuccess &&
             dqy.ensure(nq) == cudaSuccess && d_n.ensure(nq) == cudaSuccess;

@@ -25,6 +25,11 @@ struct Grid {
   int lastx0, lasty0;
 };
 
+// Row pitch (floats) of the padded right view: w + 1 values (the duplicated
+// last column) rounded up to a multiple of four, so rows start 16-byte aligned
+// and the pyramid stores them as float4.
+__host__ __device__ __forceinline__ int rpad_pitch(int w) { return (w + 4) & ~3; }
+
 // One pyramid level of a batch of pairs: planes are [pair][h][w].
 struct Level {
   int e, w, h;
@@ -36,7 +41,7 @@ struct Level {
   float* grad;     // gradient_x of left (src/pyramid.cpp:30-42)
   uint8_t* lq;     // 4-tap validity of left at (x,y) (inc/image.hpp:68-69)
   uint8_t* rq;     // 4-tap validity of right at (x,y)
-  float* rpad;     // right view, rows of w+1 (rpad[w] = rpad[w-1]: the
+  float* rpad;     // right view, rows of rpad_pitch(w) (rpad[w] = rpad[w-1]: the
                    // x1 = min(x0+1, w-1) clamp of inc/image.hpp:60)
   Grid g;
   // per-patch records [pair][ny][nx] (PatchEstimate, inc/coarse_to_fine.hpp:39-47)

@@ -111,7 +111,7 @@ __global__ void k_level_tables(Level L) {
   L.lq[base + i] = (lv[p00] && lv[p10] && lv[p01] && lv[p11]) ? 1 : 0;
   L.rq[base + i] = (rv[p00] && rv[p10] && rv[p01] && rv[p11]) ? 1 : 0;
   const float* r = L.right + base;
-  float* rp = L.rpad + blockIdx.y * (long long)(w + 1) * h + (long long)y * (w + 1);
+  float* rp = L.rpad + blockIdx.y * (long long)rpad_pitch(w) * h + (long long)y * rpad_pitch(w);
   rp[x] = r[p00];
   if (x == w - 1) rp[w] = r[p00];
 }
@@ -175,7 +175,8 @@ __global__ void __launch_bounds__(256, kRGB ? 4 : 8) k_pyramid(PyrArgs a) {
   auto store = [&](int e, int y0, int rows, const float* Lb, const float* Rb) {
     const int w = a.ws[e];
     const long long pl = pair * (long long)w * a.hs[e];
-    const long long pr = pair * (long long)(w + 1) * a.hs[e];
+    const int rpw = rpad_pitch(w);
+    const long long pr = pair * (long long)rpw * a.hs[e];
     if ((w & 3) == 0 && w >= 8 && ((Rb - Lb) & 3) == 0 && ((Lb - sbuf) & 3) == 0) {
       // four pixels per thread: 16-byte stores of L and G (rows of 4k floats)
       const int qw = w >> 2;
@@ -197,11 +198,8 @@ __global__ void __launch_bounds__(256, kRGB ? 4 : 8) k_pyramid(PyrArgs a) {
         *(float4*)(a.L[e] + o) = l4;
         *(float4*)(a.G[e] + o) = make_float4(g[0], g[1], g[2], g[3]);
         const float4 r4 = *(const float4*)(Rb + r * w + x);
-        float* rp = a.Rp[e] + pr + (long long)(y0 + r) * (w + 1) + x;
-        rp[0] = r4.x;
-        rp[1] = r4.y;
-        rp[2] = r4.z;
-        rp[3] = r4.w;
+        float* rp = a.Rp[e] + pr + (long long)(y0 + r) * rpw + x;
+        *(float4*)rp = r4;  // rows of rpad_pitch(w) floats start 16-byte aligned
         if (x + 4 == w) rp[4] = r4.w;
       }
       return;
@@ -220,7 +218,7 @@ __global__ void __launch_bounds__(256, kRGB ? 4 : 8) k_pyramid(PyrArgs a) {
       a.L[e][o] = l;
       a.G[e][o] = g;
       const float rv = Rb[r * w + x];
-      float* rp = a.Rp[e] + pr + (long long)(y0 + r) * (w + 1);
+      float* rp = a.Rp[e] + pr + (long long)(y0 + r) * rpw;
       rp[x] = rv;
       if (x == w - 1) rp[w] = rv;
     }
@@ -233,7 +231,7 @@ __global__ void __launch_bounds__(256, kRGB ? 4 : 8) k_pyramid(PyrArgs a) {
     if (fe == 0) {
       const int r0 = band << ce, r1 = min(r0 + (1 << ce), a.H);
       const int W = a.W;
-      const long long pl = pair * (long long)W * a.H, pr = pair * (long long)(W + 1) * a.H;
+      const long long pl = pair * (long long)W * a.H, pr = pair * (long long)rpad_pitch(W) * a.H;
       for (int q = tid; q < (r1 - r0) * W; q += nt) {
         const int y = r0 + q / W, x = q % W;
         const float l = src_px<kU8>(a, lut, 0, pair, x, y);
@@ -248,7 +246,7 @@ __global__ void __launch_bounds__(256, kRGB ? 4 : 8) k_pyramid(PyrArgs a) {
         a.L[0][o] = l;
         a.G[0][o] = g;
         const float rv = src_px<kU8>(a, lut, 1, pair, x, y);
-        float* rp = a.Rp[0] + pr + (long long)y * (W + 1);
+        float* rp = a.Rp[0] + pr + (long long)y * rpad_pitch(W);
         rp[x] = rv;
         if (x == W - 1) rp[W] = rv;
       }

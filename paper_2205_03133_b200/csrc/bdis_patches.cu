@@ -88,7 +88,7 @@ template <bool kSmem>
 struct Rows {
   // fp32 rows in shared memory, padded (slot x + x/32: neighbouring patches
   // read columns 4 apart, which unpadded is a 4-way bank conflict), or the
-  // level planes in global memory (right view as rows of w+1).
+  // level planes in global memory (right view as rows of rpad_pitch(w)).
   const float* R;    // right view
   const float* Lf;   // left view
   const float* Gf;   // gradient of the left view
@@ -376,7 +376,8 @@ __global__ void __launch_bounds__(256, S == -16 ? 2 : 0) k_patches(Level L, Leve
   int rofs;  // row index of image row y in rw is y - rofs
   if constexpr (kSmem) {
     // ---- stage the band (coalesced global reads, padded shared writes)
-    const float* gR = L.rpad + pair * (long long)(w + 1) * h + (long long)ylo * (w + 1);
+    const int gpitch = rpad_pitch(w);
+    const float* gR = L.rpad + pair * (long long)gpitch * h + (long long)ylo * gpitch;
     // right rows with rpad zero slots either side (x in [-rpad, w + rpad])
     const int rw2 = w + 1 + 2 * rpad;
     // asynchronous copies (cp.async): every thread queues all of its
@@ -389,7 +390,7 @@ __global__ void __launch_bounds__(256, S == -16 ? 2 : 0) k_patches(Level L, Leve
       for (int q = tid; q < nrows * rw2; q += nt) {
         const int x = xs - rpad;
         float* dst = sR + r * bp.rpitch + Rows<true>::s8(xs);
-        if (x >= 0 && x <= w) cp_async4(dst, gR + r * (w + 1) + x);
+        if (x >= 0 && x <= w) cp_async4(dst, gR + r * gpitch + x);
         else *dst = 0.0f;
         xs += dx;
         r += dr;
@@ -431,12 +432,12 @@ __global__ void __launch_bounds__(256, S == -16 ? 2 : 0) k_patches(Level L, Leve
     rw.bp = bp.bpitch;
     rofs = ylo;
   } else {
-    rw.R = L.rpad + pair * (long long)(w + 1) * h;
+    rw.R = L.rpad + pair * (long long)rpad_pitch(w) * h;
     rw.Lf = L.left + pbase;
     rw.Gf = L.grad + pbase;
     rw.lq = L.lq + pbase;
     rw.rq = L.rq + pbase;
-    rw.rp = w + 1;
+    rw.rp = rpad_pitch(w);
     rw.fp = w;
     rw.bp = w;
     rofs = 0;
@@ -956,7 +957,7 @@ __global__ void k_debug_eval(Level L, int size, int nq, const int* __restrict__ 
   rw.Gf = L.grad;
   rw.lq = L.lq;
   rw.rq = L.rq;
-  rw.rp = L.w + 1;
+  rw.rp = rpad_pitch(L.w);
   rw.fp = L.w;
   rw.bp = L.w;
   const int x0 = qx[q], y0 = qy[q];
