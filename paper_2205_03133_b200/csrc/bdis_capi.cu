@@ -755,6 +755,7 @@ int run_device(pstereo_ctx* ctx, Scratch& sc, const std::vector<LevelGeom>& geo,
   for (int e = 0; e <= ce; ++e) {
     pa.ws[e] = ws[e];
     pa.hs[e] = hs[e];
+    pa.wmagic[e] = (unsigned)((0x100000000ull + (unsigned)ws[e] - 1) / (unsigned)ws[e]);
   }
   pa.buf_floats = ce >= 1 ? (1 << (ce - 1)) * ws[1] : 0;
   // levels 2 and 4 alternate into a second, smaller buffer

@@ -158,7 +158,9 @@ __global__ void __launch_bounds__(256, kRGB ? 4 : 8) k_pyramid(PyrArgs a) {
   const int tid = threadIdx.x, nt = blockDim.x;
   const int ce = a.ce, fe = a.fe;
   // level-1 rows of this band live in buf0 (L then R), level e >= 2 alternate
-  float* buf[2] = {sbuf, sbuf + 2 * a.buf_floats};
+  // (pointer arithmetic on sbuf, not an indexed pointer array: that went to
+  // local memory and turned the cascade's loads into generic LD)
+  auto buf_of = [&](int k) { return sbuf + (k ? 2 * a.buf_floats : 0); };
   // grayscale lookup tables after the level buffers (8-byte aligned)
   double* c3 = (double*)(sbuf + ((2 * a.buf_floats + 2 * a.buf1_floats + 1) & ~1));
   float* g1 = (float*)(c3 + 768);
@@ -256,8 +258,8 @@ __global__ void __launch_bounds__(256, kRGB ? 4 : 8) k_pyramid(PyrArgs a) {
     {
       const int w = a.ws[1], h = a.hs[1];
       const int y0 = band << (ce - 1), rows = min(1 << (ce - 1), h - y0);
-      float* Lb = buf[0];
-      float* Rb = buf[0] + a.buf_floats;
+      float* Lb = buf_of(0);
+      float* Rb = Lb + a.buf_floats;
       if (kRGB) {
         // RGB rasters, W % 8 == 0, even H: 24 source bytes (8 pixels) of two
         // rows per view, three 8-byte loads each, give 4 level-1 pixels; the
@@ -332,14 +334,16 @@ __global__ void __launch_bounds__(256, kRGB ? 4 : 8) k_pyramid(PyrArgs a) {
     for (int e = 2; e <= ce; ++e) {
       const int pw = a.ws[e - 1], ph = a.hs[e - 1];
       const int py0 = band << (ce - e + 1);
-      const float* PL = buf[(e - 2) & 1];
+      const float* PL = buf_of((e - 2) & 1);
       const float* PR = PL + (((e - 2) & 1) ? a.buf1_floats : a.buf_floats);
       const int w = a.ws[e], h = a.hs[e];
       const int y0 = band << (ce - e), rows = min(1 << (ce - e), h - y0);
-      float* Lb = buf[(e - 1) & 1];
+      float* Lb = buf_of((e - 1) & 1);
       float* Rb = Lb + (((e - 1) & 1) ? a.buf1_floats : a.buf_floats);
+      const unsigned wm = a.wmagic[e];
       for (int q = tid; q < rows * w; q += nt) {
-        const int y = y0 + q / w, x = q % w;
+        const int qr = (int)__umulhi((unsigned)q, wm);  // q / w (q * w < 2^32)
+        const int y = y0 + qr, x = q - qr * w;
         const int x0 = 2 * x, x1 = min(2 * x + 1, pw - 1);
         const int r0 = 2 * y - py0, r1 = min(2 * y + 1, ph - 1) - py0;
         Lb[q] = down4(PL[r0 * pw + x0], PL[r0 * pw + x1], PL[r1 * pw + x0], PL[r1 * pw + x1]);

@@ -98,6 +98,7 @@ struct PyrArgs {
   const float* f0l;
   const float* f0r;
   int ws[kMaxLevels], hs[kMaxLevels];
+  unsigned wmagic[kMaxLevels];  // ceil(2^32 / ws[e]): q / ws[e] == umulhi(q, wmagic[e]) in a band
   float* L[kMaxLevels];
   float* G[kMaxLevels];
   float* Rp[kMaxLevels];
