@@ -283,9 +283,18 @@ __global__ void __launch_bounds__(256, kRGB ? 4 : 8) k_pyramid(PyrArgs a) {
               bw[2 * k + 1] = b.y;
             }
             auto byte = [](const unsigned* wd, int n) { return (wd[n >> 2] >> (8 * (n & 3))) & 255u; };
+            // the channel products computed, not looked up: 96 random 8-byte
+            // table reads per thread made this path shared-memory-bandwidth
+            // bound (bank conflicts; issue 33%). (double)q is exact as
+            // (2^52 + q) - 2^52, so q * coefficient is the table's value.
+            auto prod = [](unsigned q, double coef) {
+              return __dmul_rn(coef, __dsub_rn(__hiloint2double(0x43300000, (int)q),
+                                               4503599627370496.0));
+            };
             auto luma = [&](const unsigned* wd, int px) {
-              const double sum = __dadd_rn(__dadd_rn(c3[byte(wd, 3 * px)], c3[256 + byte(wd, 3 * px + 1)]),
-                                           c3[512 + byte(wd, 3 * px + 2)]);
+              const double sum = __dadd_rn(__dadd_rn(prod(byte(wd, 3 * px), 0.299),
+                                                     prod(byte(wd, 3 * px + 1), 0.587)),
+                                           prod(byte(wd, 3 * px + 2), 0.114));
               return __double2float_rn(__dmul_rn(sum, 1.0 / 255.0));
             };
             float o[4];
