@@ -123,6 +123,26 @@ def bytes_per_pair(wl) -> int:
 # ---------------------------------------------------------------------------
 # CPU reference (oracle/_ref = the reference's own sources, else the C port)
 
+def workload_config(wl, B: int, world: int) -> dict:
+    """The line's `config`: the workload both arms run, identical in the two
+    arms' lines (arm-specific details go under `run`)."""
+    nb = -(-B // world)
+    step_in = 2 * nb * wl["W"] * wl["H"] * wl["C"]
+    n_sets = input_sets(step_in)
+    return {"workload": wl["desc"], "global_batch": B, "per_gpu_batch": nb,
+            "parallelism": f"pair-sharded x{world}, contiguous blocks, no collective",
+            "l2": (f"inputs {step_in / 1e6:.0f} MB/step per GPU "
+                   + ("> 126 MB L2 (no flush needed)" if n_sets == 1 else
+                      f"< 126 MB L2: steps cycle over {n_sets} input sets "
+                      f"({n_sets * step_in / 1e6:.0f} MB > 2x L2)"))}
+
+
+def input_sets(step_in: int) -> int:
+    """Distinct input sets the timed steps cycle over, so that no step reads
+    L2-resident inputs: one when a step's inputs exceed the 126 MB L2."""
+    return 1 if step_in > 126e6 else -(-int(2 * 126e6) // max(step_in, 1))
+
+
 def _cpu_oracle():
     from oracle import pyoracle
 
@@ -197,8 +217,8 @@ def run_reference_arm(args, wl):
         "n_gpus": max(args.gpus, world), "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * total_t / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": wl["desc"], "global_batch": B,
-                   "parallelism": f"{cores} host threads (pair-parallel)"},
+        "config": workload_config(wl, B, max(args.gpus, world)),
+        "run": {"arm": "the reference's run_pipeline on the host", "host_threads": cores},
         "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": cores, "kind": kind,
                          "sample": sample},
         "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0,
@@ -392,7 +412,7 @@ def run_ours(args, wl):
     # more than twice the L2, so no timed step reads L2-resident inputs.
     inflight = max(1, args.inflight)
     step_in = 2 * nb * W * H * CH
-    n_sets = 1 if step_in > 126e6 else -(-int(2 * 126e6) // max(step_in, 1))
+    n_sets = input_sets(step_in)
     sets = [(dl, dr)] + [P.synth_batch_gpu(wl["gen"], nb, seed0=shard.start + k * max(B, 1),
                                            device=local, **wl["over"])
                          for k in range(1, n_sets)]
@@ -598,18 +618,14 @@ def run_ours(args, wl):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded BASELINE generator, see DESIGN.md)",
-        "config": {"workload": wl["desc"], "global_batch": B, "per_gpu_batch": nb,
-                   "parallelism": f"pair-sharded x{world}, contiguous blocks, no collective",
-                   "inputs": "generated on device (pstereo_gpu_synth, byte-identical to the "
-                             "host generator)",
-                   "output": "fp32 filtered disparity, NaN = invalid (mask folded in)",
-                   "inflight": inflight,
-                   "warmup_steps_run": warm,
-                   "host_cpus": numa or "unpinned",
-                   "l2": (f"inputs {step_in / 1e6:.0f} MB/step per GPU "
-                          + ("> 126 MB L2 (no flush needed)" if n_sets == 1 else
-                             f"< 126 MB L2: steps cycle over {n_sets} input sets "
-                             f"({n_sets * step_in / 1e6:.0f} MB > 2x L2)"))},
+        "config": workload_config(wl, B, world),
+        "run": {"arm": "B200 kernels through the C ABI",
+                "inputs": "generated on device (pstereo_gpu_synth, byte-identical to the "
+                          "host generator)",
+                "output": "fp32 filtered disparity, NaN = invalid (mask folded in)",
+                "inflight": inflight,
+                "warmup_steps_run": warm,
+                "host_cpus": numa or "unpinned"},
         "gpu_launches": launches_per_step * args.steps,
         "full_outputs": {"value": B / (full_ms / 1e3), "unit": "pairs/s", "ms_per_step": full_ms,
                          "planes": "disparity f32 + mask, probability f32, depth f32 + mask"},
